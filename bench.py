@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark: normal variates/s of the Wallace pool generator on B200.
+
+Workload (BASELINE.json configs[1], "config 2"): 16384 independent fp32 pools
+of N=4096, seeds 1..16384, 2 transform passes per output, chi2 rescaling off,
+2^32 variates per step into one 16 GiB HBM buffer.  A step re-runs that job
+from the seeded pools (wallace_fill_from_snapshot): the pool state (seeded,
+warmed-up) is the step's input, resident in HBM; the 16 GiB output is larger
+than the 126 MB L2, so no flush is needed between steps.
+
+--impl ours (default): one JSON line with value (device-timed), e2e (through
+  the C-ABI into pinned host memory), roofline of pool_kernel, cpu_baseline
+  (the reference library on this host), clocks, gpu_launches.
+--impl reference: the unmodified reference library (oracle/_ref, compiled
+  from the reference sources) timed on this box's host cores.
+
+--config 1..5 selects another BASELINE config (parity cases; 2 is the bench
+line).  Under torchrun each rank runs its own full job with a disjoint seed
+range (weak scaling, no data-path collective); max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(name="cfg1: 1 pool x N=1024 fp32, 1 pass/output, cubic_a, seed 1, 2^24 variates",
+            kw=dict(pool_size=1024, discard_every=1), pools=1, count=1 << 24, dtype="f32"),
+    2: dict(name="cfg2: 16384 pools x N=4096 fp32, 2 passes/output, no chi2, seeds 1..16384, 2^32 variates",
+            kw=dict(pool_size=4096, discard_every=2, disable_chi2=True), pools=16384, count=1 << 18,
+            dtype="f32"),
+    3: dict(name="cfg3: 16384 pools x N=4096 fp32, 2 passes/output, cubic_a chi2, seeds 1..16384, 2^32 variates",
+            kw=dict(pool_size=4096, discard_every=2), pools=16384, count=1 << 18, dtype="f32"),
+    4: dict(name="cfg4: 8192 pools x N=2048 fp64, 3 passes/output, cubic_a chi2, seeds 1..8192, 2^30 variates",
+            kw=dict(pool_size=2048, discard_every=3), pools=8192, count=1 << 17, dtype="f64"),
+    5: dict(name="cfg5: 65536 pools x N=1024 fp32, 1 pass/output, cubic_a, 2^34 variates consumed in-kernel",
+            kw=dict(pool_size=1024, discard_every=1), pools=65536, count=1 << 18, dtype="f32",
+            consume=True),
+}
+METRIC = "normal variates/sec at 1 B200 and % of HBM write roofline vs CPU ref"
+UNIT = "variates/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg_id):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(str(cfg_id))
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, device_index=0, period=0.005):
+        self.samples = []
+        self.reasons = set()
+        self.period = period
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None),
+                    "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_reference_run(cfg, n_pools, count, threads, seed_base=1):
+    """The unmodified reference library on the host: (fill_seconds, init_seconds)."""
+    import ctypes as C
+    from oracle import oracle
+    L = oracle.ref_lib()
+    ti, tf = C.c_double(), C.c_double()
+    kw = cfg["kw"]
+    L.ref_run_job(kw["pool_size"], kw.get("chi2_method", 2), kw["discard_every"],
+                  int(kw.get("disable_chi2", False)), seed_base, n_pools, count, threads,
+                  C.byref(ti), C.byref(tf))
+    return tf.value, ti.value
+
+
+def cpu_sample_size(cfg, target_values):
+    pools = max(1, min(cfg["pools"], target_values // cfg["count"]))
+    return pools
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    cfg = CONFIGS[args.config]
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libmaxent_ref.so not built (needs /root/reference at build time)"}))
+        return 0
+    threads = os.cpu_count() or 1
+    # bounded sample of the configured job per step: ~2^29 variates of fp64
+    n_pools = cpu_sample_size(cfg, 1 << 29)
+    for _ in range(args.warmup):
+        cpu_reference_run(cfg, max(1, n_pools // 10), cfg["count"], threads)
+    fills, inits = [], []
+    for _ in range(args.steps):
+        tf, ti = cpu_reference_run(cfg, n_pools, cfg["count"], threads)
+        fills.append(tf)
+        inits.append(ti)
+    variates = n_pools * cfg["count"]
+    t = statistics.median(fills)
+    value = variates / t
+    sample = (f"{n_pools} of {cfg['pools']} pools x {cfg['count']} variates (fp64, reference has no "
+              f"fp32), seeds 1..{n_pools}, fill() timed by wall clock, construction timed separately")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded pools)",
+        "config": {"workload": cfg["name"], "sample_pools": n_pools, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "init_s_per_step": statistics.median(inits),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1005_2314_b200 as pb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    cfg = CONFIGS[args.config]
+    n_pools, count, dtype = cfg["pools"], cfg["count"], cfg["dtype"]
+    esize = 4 if dtype == "f32" else 8
+    seeds = np.arange(1 + rank * n_pools, 1 + (rank + 1) * n_pools, dtype=np.uint64)
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    batch = pb.PoolBatch(pb.GeneratorConfig(**cfg["kw"]), n_pools=n_pools, seeds=seeds, dtype=dtype,
+                         stream=stream)
+    init_s = time.time() - t0
+    batch.snapshot()
+    consume = cfg.get("consume", False)
+    out = None if consume else torch.empty((n_pools, count), dtype=batch.torch_dtype, device="cuda")
+
+    def step():
+        if consume:
+            batch.consume(count)  # synchronous; replays from the live state
+        else:
+            batch.fill_from_snapshot_into(out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = pb.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = pb.kernel_launches() - launches0
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    variates_rank = n_pools * count
+    value = world * variates_rank * args.steps / (ms / 1e3)
+
+    # dominant kernel timing: pool_kernel bracketed by events on its stream
+    pb._capi.load().wallace_profile_begin(batch.h)
+    for _ in range(max(3, min(args.steps, 10))):
+        step()
+    import ctypes as C
+    pool_ms, plan_ms = C.c_double(), C.c_double()
+    pool_n, plan_n = C.c_uint64(), C.c_uint64()
+    pb._capi.load().wallace_profile_end(batch.h, C.byref(pool_ms), C.byref(pool_n),
+                                        C.byref(plan_ms), C.byref(plan_n))
+    peak, peak_src = measured_peaks()
+    per_launch_ms = pool_ms.value / max(1, pool_n.value)
+    launches_per_step = pool_n.value / max(3, min(args.steps, 10))
+    alg_bytes = variates_rank * esize / launches_per_step  # written per launch
+    roofline = None
+    if not consume:
+        achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+        tr = ncu_traffic(args.config)
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
+                    "kernel": "pool_kernel", "kernel_ms": per_launch_ms,
+                    "kernel_share_of_step": pool_ms.value / max(1e-9, pool_ms.value + plan_ms.value),
+                    "algorithmic_bytes_per_launch": alg_bytes}
+
+    # end to end through the C-ABI into pinned host memory
+    e2e = None
+    if rank == 0 and not consume and not args.no_e2e:
+        try:
+            host = torch.empty((n_pools, count), dtype=batch.torch_dtype, pin_memory=True)
+            e2e_steps = max(1, min(args.e2e_steps, args.steps))
+            batch.fill_host_ptr(host.data_ptr(), count)  # warm-up
+            t1 = time.perf_counter()
+            for _ in range(e2e_steps):
+                batch.fill_host_ptr(host.data_ptr(), count)
+            dt = (time.perf_counter() - t1) / e2e_steps
+            e2e = {"value": variates_rank / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": variates_rank * esize,
+                   "api": "wallace_fill_host (C-ABI) into pinned host memory, wall clock",
+                   "s_per_step": dt}
+            del host
+        except Exception as ex:  # noqa: BLE001
+            e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle
+            if oracle.ref_available():
+                threads = os.cpu_count() or 1
+                sp = cpu_sample_size(cfg, 1 << 29)
+                tf, ti = cpu_reference_run(cfg, sp, count, threads)
+                cpu = {"value": sp * count / tf, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"{sp} of {n_pools} pools x {count} variates, fp64 reference "
+                                 f"Generator::fill, construction ({ti:.2f}s) excluded"}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic (pools seeded by the reference's Polar init)",
+            "config": {"workload": cfg["name"], "pools_per_gpu": n_pools, "pool_size": cfg["kw"]["pool_size"],
+                       "variates_per_step_per_gpu": variates_rank,
+                       "l2": "output per step (16 GiB for cfg2) >> 126 MB L2; no flush needed",
+                       "step": "replay of the seeded job from the device snapshot"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "init_s": init_s,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    return run_reference(args) if args.impl == "reference" else run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,193 @@
+/*
+ * wallace_b200.h — C-ABI of the B200-native Wallace maximum-entropy normal
+ * generator (arXiv 1005.2314, reference: maxent-rng).
+ *
+ * The reference has no FFI: its boundary is the C++ class maxent::Generator
+ * (/root/reference/proj/core/include/maxent/generator.hpp:98-149) and the
+ * free functions decode_pass_plan / run_pass (generator.hpp:57-66).  Each
+ * entry point below names the reference interface it replaces.  The C++
+ * drop-in (include/wallace_b200.hpp) and the Python tests bind only these
+ * symbols.  No C++ exception crosses this boundary; every call returns a
+ * wallace_status and wallace_last_error() holds the message (which, for
+ * WALLACE_ERR_CONFIG, names the offending field exactly as ConfigError does,
+ * generator.cpp:221-236).
+ *
+ * A handle owns a BATCH of independent pools (one reference Generator per
+ * pool; "distinct instances with distinct seeds may run in parallel",
+ * generator.hpp:96-97).  Pool p is seeded with seeds[p] (or cfg.seed + p).
+ * Every pool of a batch advances together; slice p of every output equals
+ * what the reference's Generator(seed_p) would produce for the same calls.
+ * A handle is single-threaded and bound to one CUDA stream.
+ */
+#ifndef WALLACE_B200_H
+#define WALLACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum wallace_status {
+  WALLACE_OK = 0,
+  WALLACE_ERR_CONFIG = 1,        /* maxent::ConfigError (errors.hpp:18-21) */
+  WALLACE_ERR_INVALID_PARAM = 2, /* maxent::InvalidParameterError (errors.hpp:12-16) */
+  WALLACE_ERR_CUDA = 3,          /* device failure (no reference equivalent) */
+  WALLACE_ERR_UNSUPPORTED = 4    /* valid in the reference, not built here */
+} wallace_status;
+
+typedef enum wallace_dtype { WALLACE_F32 = 0, WALLACE_F64 = 1 } wallace_dtype;
+
+/* maxent::Chi2Method (chi2.hpp:21) — same numbering */
+typedef enum wallace_chi2_method {
+  WALLACE_CHI2_SQRT_SHIFT = 0,
+  WALLACE_CHI2_WILSON_HILFERTY = 1,
+  WALLACE_CHI2_CUBIC_A = 2
+} wallace_chi2_method;
+
+/* maxent::GeneratorConfig (generator.hpp:21-45).  transform_family 0 is
+ * wallace4 and mixing 0 is stride_transpose; the rotation family and affine
+ * mixing return WALLACE_ERR_UNSUPPORTED. */
+typedef struct wallace_config {
+  uint64_t pool_size;       /* power of two in [32, 2^31]; on-chip limit 2^14 (f32) / 2^13 (f64) */
+  int32_t transform_family; /* TransformFamily */
+  int32_t mixing;           /* MixingScheme */
+  int32_t chi2_method;      /* wallace_chi2_method */
+  int32_t fixed_transform;  /* diag.fixed_transform */
+  int32_t disable_chi2;     /* diag.disable_chi2 */
+  int32_t reserved_;
+  uint64_t discard_every;   /* passes per emission, >= 1 */
+  double out_mean;
+  double out_sigma;
+  uint64_t seed;            /* seed of pool 0 when seeds == NULL */
+} wallace_config;
+
+/* Per-pool bookkeeping: Generator::pass_count/uniform_draws/chi2_clamp_count
+ * (generator.hpp:124-126), NormalPool::sum_sq/reserved_prev (generator.hpp:81-87),
+ * and PoolOutput::chi2_draw (generator.hpp:115-119). */
+typedef struct wallace_pool_info {
+  uint64_t pass_count;
+  uint64_t uniform_draws;
+  uint64_t chi2_clamp_count;
+  double sum_sq;
+  double reserved_prev;
+  double last_chi2;
+  uint64_t buffered; /* values of the current emission not yet returned */
+  uint64_t seed;
+} wallace_pool_info;
+
+typedef struct wallace_handle wallace_handle;
+
+/* Generator::Generator(GeneratorConfig) (generator.cpp:309-331), for
+ * n_pools pools at once.  Validates (ConfigError semantics), seeds each pool
+ * on the host (Polar, Neumaier normalisation — bit-exact with the reference
+ * on the same libm), uploads the pools to HBM and runs the 16 warm-up passes
+ * on the device.  stream: a cudaStream_t or NULL (legacy default stream). */
+wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools,
+                              const uint64_t* seeds, wallace_dtype dtype,
+                              void* stream, wallace_handle** out);
+
+wallace_status wallace_destroy(wallace_handle* h);
+
+/* Generator::fill(std::span<double>) (generator.cpp:387-399) for every pool:
+ * dev_out is a DEVICE buffer of n_pools * count_per_pool elements of the
+ * handle's dtype, pool-major (pool p at [p*count, (p+1)*count)).  Exactly
+ * equivalent to count_per_pool next_normal() calls per pool.  count == 0 is
+ * WALLACE_ERR_INVALID_PARAM ("fill: count must be >= 1"). Asynchronous. */
+wallace_status wallace_fill(wallace_handle* h, void* dev_out, uint64_t count_per_pool);
+
+/* Same as wallace_fill but writes a HOST buffer (pinned or pageable) of the
+ * same layout; device staging and device->host copies are internal.
+ * Synchronous. */
+wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t count_per_pool);
+
+/* Generator::next_pool() (generator.cpp:401-405): one emission per pool.
+ * dev_values (optional) receives n_pools * (pool_size - 1) values, device
+ * memory; reserved / chi2_draw (optional) receive n_pools doubles on the
+ * host.  Discards any partially consumed emission. Synchronous. */
+wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* reserved,
+                                 double* chi2_draw);
+
+/* Generator::step_pass() (generator.cpp:333-343), n_passes times. */
+wallace_status wallace_step_pass(wallace_handle* h, uint64_t n_passes);
+
+/* Generator::inject_pool(span) (generator.cpp:407-413) for one pool:
+ * replaces the raw pool and recomputes sum_sq (not renormalised). */
+wallace_status wallace_inject_pool(wallace_handle* h, uint64_t pool, const double* values,
+                                   uint64_t n);
+
+/* Generator::pool().raw (generator.hpp:123), converted to double. Synchronous. */
+wallace_status wallace_get_pool(wallace_handle* h, uint64_t pool, double* raw_out, uint64_t n);
+
+wallace_status wallace_get_pool_info(wallace_handle* h, uint64_t pool, wallace_pool_info* out);
+
+/* Checkpoint / resume (no reference equivalent: Generator state is private,
+ * SURVEY §5).  The state image is pools + per-pool state, host memory. */
+uint64_t wallace_state_bytes(const wallace_handle* h);
+wallace_status wallace_save_state(wallace_handle* h, void* host_buf, uint64_t bytes);
+wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint64_t bytes);
+
+/* Device-resident snapshot: wallace_snapshot() copies the current state to a
+ * device-side checkpoint; wallace_fill_from_snapshot() performs wallace_fill
+ * starting from that checkpoint (the live state becomes the result), so a job
+ * can be re-run without re-seeding.  Used by bench.py to time the same
+ * configured job every step. */
+wallace_status wallace_snapshot(wallace_handle* h);
+wallace_status wallace_fill_from_snapshot(wallace_handle* h, void* dev_out,
+                                          uint64_t count_per_pool);
+
+/* Fused consumer (BASELINE config 5): generates count_per_pool values per
+ * pool exactly as wallace_fill would, but consumes them in-kernel into
+ * sums[4] = {sum x, x^2, x^3, x^4} (fp64, fixed reduction order) and
+ * hist[258] = {under, 256 bins of width 1/16 over [-8,8), over}, with bin =
+ * floor((x + 8) * 16) computed in the handle's dtype. Synchronous. */
+wallace_status wallace_consume(wallace_handle* h, uint64_t count_per_pool, double sums[4],
+                               uint64_t hist[258]);
+
+/* Box-Muller comparator (baselines.cpp:68-92): stream p consumes the
+ * uniform stream UniformState(seeds[p] or seed_base+p) exactly as
+ * boxmuller_next does (u1 == 0 -> 2^-53, cached twin), evaluated on the
+ * device in fp32 (log/sincos are not bit-exact with glibc; compare
+ * statistically), and feeds the same consumer as wallace_consume. */
+wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_base,
+                                         uint64_t n_streams, uint64_t count_per_stream,
+                                         void* stream, double sums[4], uint64_t hist[258]);
+
+/* Kernel timing for measurement (bench.py): between begin and end, every
+ * plan_kernel and pool_kernel launch of this handle is bracketed by CUDA
+ * events recorded on the handle's stream.  end synchronizes the stream and
+ * returns the summed device milliseconds and launch counts. */
+wallace_status wallace_profile_begin(wallace_handle* h);
+wallace_status wallace_profile_end(wallace_handle* h, double* pool_kernel_ms,
+                                   uint64_t* pool_launches, double* plan_kernel_ms,
+                                   uint64_t* plan_launches);
+
+/* Rebind the handle to another stream. */
+wallace_status wallace_set_stream(wallace_handle* h, void* stream);
+
+/* Number of kernels this library has launched (all handles). */
+uint64_t wallace_kernel_launches(void);
+
+/* Message of the last failed call on this thread. */
+const char* wallace_last_error(void);
+
+/* Host-only helpers (no device work), exposed for tests and integration:
+ * validate a config exactly like GeneratorConfig::validate(); seed one pool
+ * on the host like the Generator constructor up to (excluding) the 16
+ * warm-up passes: raw_out[pool_size] (double), reserved_prev, sum_sq,
+ * xoshiro state s[4] and draws. */
+wallace_status wallace_validate_config(const wallace_config* cfg);
+wallace_status wallace_host_seed_pool(const wallace_config* cfg, uint64_t seed, double* raw_out,
+                                      double* reserved_prev, double* sum_sq, uint64_t s_out[4],
+                                      uint64_t* draws);
+/* maxent::default_stride (transforms.cpp:161-169) and the plan decode of
+ * decode_pass_plan (generator.cpp:238-257) — the integer contract. */
+uint64_t wallace_default_stride(uint64_t rows);
+int32_t wallace_decode_pass_plan(uint64_t pool_size, uint64_t transform_word,
+                                 uint64_t offset_word, uint64_t* offset0);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WALLACE_B200_H */

@@ -1,0 +1,231 @@
+// TEST INFRASTRUCTURE ONLY — extern "C" shim over the UNMODIFIED reference
+// library (maxent::Generator and friends).  oracle/Makefile compiles this file
+// together with the reference sources where they lie under
+// /root/reference/proj/core/src into oracle/_ref/libmaxent_ref.so.  It is used
+// to pin the C oracle (tests/test_oracle_pin.py), to generate golden fixtures
+// (tests/golden/make_golden.py) and as the CPU arm of bench.py
+// (`--impl reference`, `cpu_baseline.kind = "reference"`).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "maxent/baselines.hpp"
+#include "maxent/chi2.hpp"
+#include "maxent/generator.hpp"
+#include "maxent/stats.hpp"
+#include "maxent/transforms.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+maxent::GeneratorConfig to_cfg(uint64_t pool_size, int chi2_method,
+                               uint64_t discard_every, double mean,
+                               double sigma, uint64_t seed, int fixed,
+                               int disable_chi2) {
+  maxent::GeneratorConfig c;
+  c.pool_size = pool_size;
+  c.chi2_method = static_cast<maxent::Chi2Method>(chi2_method);
+  c.discard_every = discard_every;
+  c.out_mean = mean;
+  c.out_sigma = sigma;
+  c.seed = seed;
+  c.diag.fixed_transform = fixed != 0;
+  c.diag.disable_chi2 = disable_chi2 != 0;
+  return c;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void* ref_create(uint64_t pool_size, int chi2_method, uint64_t discard_every,
+                 double mean, double sigma, uint64_t seed, int fixed,
+                 int disable_chi2) {
+  try {
+    return new maxent::Generator(to_cfg(pool_size, chi2_method, discard_every,
+                                        mean, sigma, seed, fixed,
+                                        disable_chi2));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_destroy(void* g) { delete static_cast<maxent::Generator*>(g); }
+
+int ref_fill(void* g, double* out, uint64_t count) {
+  try {
+    static_cast<maxent::Generator*>(g)->fill(std::span<double>(out, count));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+double ref_next_normal(void* g) {
+  return static_cast<maxent::Generator*>(g)->next_normal();
+}
+
+int ref_next_pool(void* g, double* values, double* reserved, double* chi2) {
+  auto po = static_cast<maxent::Generator*>(g)->next_pool();
+  if (values) std::memcpy(values, po.values.data(), po.values.size() * 8);
+  *reserved = po.reserved;
+  *chi2 = po.chi2_draw;
+  return static_cast<int>(po.values.size());
+}
+
+void ref_step_pass(void* g) { static_cast<maxent::Generator*>(g)->step_pass(); }
+
+int ref_inject_pool(void* g, const double* v, uint64_t n) {
+  try {
+    static_cast<maxent::Generator*>(g)->inject_pool(
+        std::span<const double>(v, n));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+void ref_get_pool(void* g, double* raw) {
+  const auto& p = static_cast<maxent::Generator*>(g)->pool();
+  std::memcpy(raw, p.raw.data(), p.raw.size() * 8);
+}
+
+void ref_get_stats(void* g, uint64_t* pass_count, uint64_t* draws,
+                   uint64_t* clamp, double* sum_sq, double* reserved_prev) {
+  auto* gen = static_cast<maxent::Generator*>(g);
+  *pass_count = gen->pass_count();
+  *draws = gen->uniform_draws();
+  *clamp = gen->chi2_clamp_count();
+  *sum_sq = gen->pool().sum_sq;
+  *reserved_prev = gen->pool().reserved_prev;
+}
+
+void ref_uniform_bits(uint64_t seed, uint64_t n, uint64_t* out) {
+  maxent::UniformState u(seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = maxent::uniform_bits(u);
+}
+
+uint64_t ref_default_stride(uint64_t rows) { return maxent::default_stride(rows); }
+
+double ref_compute_a(uint64_t nu) { return maxent::compute_a(nu); }
+
+double ref_chi2_sample(double x, uint64_t nu, int method, int* clamped) {
+  bool c = false;
+  const double s = maxent::chi2_sample(x, maxent::Chi2Params::for_nu(nu),
+                                       static_cast<maxent::Chi2Method>(method),
+                                       &c);
+  *clamped = c ? 1 : 0;
+  return s;
+}
+
+void ref_wallace_variant(int id, int src[4], double sign[4], double entries[16]) {
+  const auto m = maxent::wallace_variant(id);
+  for (int k = 0; k < 4; ++k) {
+    src[k] = m.source_row[k];
+    sign[k] = m.row_sign[k];
+    for (int j = 0; j < 4; ++j) entries[4 * k + j] = m.entries[k][j];
+  }
+}
+
+int ref_decode_pass_plan(uint64_t pool_size, uint64_t w0, uint64_t w1,
+                         uint64_t* offset0) {
+  maxent::GeneratorConfig c;
+  c.pool_size = pool_size;
+  const auto plan = maxent::decode_pass_plan(c, w0, w1);
+  *offset0 = plan.offset[0];
+  return plan.wallace_variant;
+}
+
+void ref_polar(uint64_t seed, uint64_t n, double* out) {
+  maxent::BaselineState s(seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = maxent::polar_next(s);
+}
+
+void ref_boxmuller(uint64_t seed, uint64_t n, double* out) {
+  maxent::BaselineState s(seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = maxent::boxmuller_next(s);
+}
+
+void ref_moments(const double* x, uint64_t n, double out[4]) {
+  const auto m = maxent::moments(std::span<const double>(x, n));
+  out[0] = m.mean;
+  out[1] = m.variance;
+  out[2] = m.skewness;
+  out[3] = m.excess_kurtosis;
+}
+
+// Whole-job runner for the CPU baseline: pools [0, n_pools) with seeds
+// seed_base + p, one Generator per pool claimed from an atomic counter by
+// `threads` std::threads.  Pools are processed in batches of
+// at most 1024 so memory stays bounded: for each batch, phase 1 constructs
+// every Generator (Polar init + 16 warm-up passes) and phase 2 fill()s
+// count_per_pool values per pool in 65536-value chunks, the reference's own
+// bench chunking (bench.cpp:43-59), folded into a sink so no work is elided.
+// Each phase is timed by wall clock across all threads and summed over
+// batches.  Returns the sink.
+double ref_run_job(uint64_t pool_size, int chi2_method, uint64_t discard_every,
+                   int disable_chi2, uint64_t seed_base, uint64_t n_pools,
+                   uint64_t count_per_pool, int threads, double* init_seconds,
+                   double* fill_seconds) {
+  std::vector<double> sinks(static_cast<size_t>(threads), 0.0);
+  double t_init = 0.0, t_fill = 0.0;
+  const uint64_t batch = 1024;
+  for (uint64_t b0 = 0; b0 < n_pools; b0 += batch) {
+    const uint64_t nb = std::min(batch, n_pools - b0);
+    std::vector<maxent::Generator*> gens(nb, nullptr);
+    auto run = [&](auto&& body) {
+      std::atomic<uint64_t> next{0};
+      std::vector<std::thread> pool;
+      for (int t = 0; t < threads; ++t) {
+        pool.emplace_back([&, t] {
+          for (;;) {
+            const uint64_t p = next.fetch_add(1);
+            if (p >= nb) break;
+            body(t, p);
+          }
+        });
+      }
+      for (auto& th : pool) th.join();
+    };
+    const auto c0 = std::chrono::steady_clock::now();
+    run([&](int, uint64_t p) {
+      gens[p] = new maxent::Generator(to_cfg(pool_size, chi2_method, discard_every, 0.0, 1.0,
+                                             seed_base + b0 + p, 0, disable_chi2));
+    });
+    const auto c1 = std::chrono::steady_clock::now();
+    run([&](int t, uint64_t p) {
+      thread_local std::vector<double> buf(65536);
+      double sink = 0.0;
+      uint64_t left = count_per_pool;
+      while (left) {
+        const uint64_t take = std::min<uint64_t>(left, buf.size());
+        gens[p]->fill(std::span<double>(buf.data(), take));
+        sink += buf[0] + buf[take - 1];
+        left -= take;
+      }
+      sinks[static_cast<size_t>(t)] += sink;
+    });
+    const auto c2 = std::chrono::steady_clock::now();
+    for (auto* g : gens) delete g;
+    t_init += std::chrono::duration<double>(c1 - c0).count();
+    t_fill += std::chrono::duration<double>(c2 - c1).count();
+  }
+  *init_seconds = t_init;
+  *fill_seconds = t_fill;
+  double s = 0.0;
+  for (const double v : sinks) s += v;
+  return s;
+}
+
+}  // extern "C"

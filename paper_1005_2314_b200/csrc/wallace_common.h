@@ -1,0 +1,99 @@
+// Shared host/device definitions for the B200 Wallace pool generator.
+//
+// Terminology follows the reference (arXiv 1005.2314 / maxent-rng):
+//   pool      — N raw normal variates (NormalPool::raw, generator.hpp:81-87)
+//   pass      — one regeneration y = Qx over the whole pool (step_pass,
+//               generator.cpp:333-343)
+//   emission  — one refill_: discard_every passes, then N-1 scaled outputs
+//               (generator.cpp:353-376)
+//   plan      — the (variant, offset) decoded from two xoshiro words
+//               (decode_pass_plan, generator.cpp:238-257)
+#pragma once
+
+#include <cstdint>
+
+namespace wb {
+
+// Persistent per-pool state, resident in HBM between launches (the
+// checkpoint).  Mirrors the private members of maxent::Generator
+// (generator.hpp:140-148) plus the emission bookkeeping needed to resume a
+// partially consumed emission without storing it.
+struct alignas(16) PoolState {
+  double reserved_prev;  // NormalPool::reserved_prev
+  double sum_sq;         // NormalPool::sum_sq (cached, updated at renorm/inject)
+  double scale;          // out_sigma * r of the current emission
+  double r;              // sqrt(S / sum_sq) of the current emission
+  double last_chi2;      // S of the current emission (PoolOutput::chi2_draw)
+  uint64_t pass_count;   // NormalPool::pass_count
+  uint64_t s[4];         // xoshiro256** state (UniformState::s)
+  uint64_t draws;        // UniformState::draws
+  uint64_t clamp_count;  // chi2 clamp counter
+  uint32_t cursor;       // consumed values of the current emission, N-1 = empty
+  uint32_t flags;        // kFlagLeftover | kFlagChi2NonFinite
+  uint64_t seed;
+  uint64_t pad_[2];
+};
+static_assert(sizeof(PoolState) == 128, "PoolState layout");
+
+constexpr uint32_t kFlagLeftover = 1u;      // leftover emission materialized
+constexpr uint32_t kFlagChi2NonFinite = 2u; // chi2_sample saw non-finite x
+
+// Precomputed chi2 constants (chi2.cpp:27-59).  Every entry is computed on
+// the host with the same double expression the reference evaluates per call,
+// so hoisting them is bit-identical.
+struct Chi2Consts {
+  double nu;
+  double a;            // compute_a(nu)            (cubic_a)
+  double cubic_c;      // sqrt(2 * (nu - a * a))   (cubic_a)
+  double shift_c;      // sqrt(2 * nu - 1)         (sqrt_shift)
+  double wh_sqrt_d;    // sqrt(d), d = 2/(9 nu)    (wilson_hilferty)
+  double wh_one_m_d;   // 1 - d                    (wilson_hilferty)
+  double floor_v;      // 1e-6 * nu
+  int32_t method;      // 0 sqrt_shift, 1 wilson_hilferty, 2 cubic_a
+  int32_t disable;     // diag.disable_chi2
+};
+
+enum Mode : int32_t {
+  kModeFill = 0,     // emit into the caller's buffer
+  kModePasses = 1,   // passes only (warm-up / step_pass)
+  kModeConsume = 2,  // emit into fused moment/histogram consumer
+};
+
+struct FillArgs {
+  const void* pools_in;  // T[n_pools * N]
+  void* pools_out;
+  const PoolState* st_in;
+  PoolState* st_out;
+  const uint32_t* plans;  // [n_pools][plan_stride]: offset | variant << 16
+  uint32_t plan_stride;
+  uint32_t n_passes;      // passes in this launch
+  uint32_t d;             // discard_every
+  uint32_t lead;          // leftover values emitted before the first pass
+  uint32_t n_emit;        // emissions in this launch
+  uint32_t last_limit;    // values taken from the last emission (<= N-1)
+  int32_t mode;
+  int32_t mean_is_zero;   // out_mean == +0.0: x*scale+0 fused (bit-identical)
+  void* out;              // T, pool-major
+  uint64_t out_stride;    // elements per pool slice
+  uint64_t out_offset;    // element offset inside each slice
+  void* leftover;         // T[n_pools * (N-1)] materialized leftovers
+  double mean;
+  double sigma;
+  Chi2Consts chi2;
+  // consumer (kModeConsume)
+  double* part_sums;      // [n_pools][4]
+  uint32_t* part_hist;    // [n_pools][258]
+};
+
+struct PlanArgs {
+  const PoolState* st_in;
+  PoolState* st_out;
+  uint32_t* plans;
+  uint32_t plan_stride;
+  uint32_t n_passes;
+  uint32_t n_pools;
+  uint32_t rows_mask;
+  int32_t fixed_transform;
+};
+
+}  // namespace wb

@@ -1,0 +1,934 @@
+// Host side of the B200 Wallace pool generator: the C-ABI of
+// include/wallace_b200.h, host seeding of pools, launch sequencing.
+//
+// Seeding follows Generator::Generator (generator.cpp:309-331): SplitMix64 +
+// xoshiro256** (baselines.cpp:19-45), Polar normals with glibc log/sqrt
+// (baselines.cpp:51-66), Neumaier sum of squares (generator.cpp:20-34),
+// scaling to sum_sq = n.  It runs on the host so that glibc's log is the one
+// the reference uses (bit parity of the seeded pool); the 16 warm-up passes
+// then run on the device.  Seeding is spread over host threads, one pool at a
+// time per thread.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "../../include/wallace_b200.h"
+#include "wallace_common.h"
+
+namespace wb {
+cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t n_pools,
+                               cudaStream_t s);
+int pool_kernel_threads(int dtype, int log2n);
+cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
+cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void* leftover,
+                               uint64_t n_pools, uint32_t N, double mean, cudaStream_t s);
+cudaError_t launch_reduce_consumer(const double* part_sums, const uint32_t* part_hist,
+                                   uint64_t n_pools, uint64_t chunk, double* blk_sums,
+                                   unsigned long long* blk_hist, cudaStream_t s);
+cudaError_t launch_boxmuller(const uint64_t* d_seeds, uint64_t seed_base, uint64_t n_streams,
+                             uint64_t count, double* part_sums, uint32_t* part_hist,
+                             uint64_t n_blocks, int threads, cudaStream_t s);
+}  // namespace wb
+
+using wb::PoolState;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+wallace_status fail(wallace_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define WB_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(WALLACE_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),   \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+// ---- reference primitives restated for host seeding -----------------------
+inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+uint64_t splitmix64(uint64_t& state) {  // baselines.cpp:19-24
+  uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+struct Uniform {  // UniformState (baselines.hpp:27-33)
+  uint64_t s[4];
+  uint64_t draws = 0;
+  explicit Uniform(uint64_t seed) {  // baselines.cpp:26-31
+    uint64_t sm = seed;
+    for (auto& w : s) w = splitmix64(sm);
+  }
+  uint64_t bits() {  // baselines.cpp:33-45
+    const uint64_t result = rotl(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    ++draws;
+    return result;
+  }
+  double next() { return static_cast<double>(bits() >> 11) * 0x1.0p-53; }  // :47-49
+};
+
+struct Polar {  // BaselineState + polar_next (baselines.cpp:51-66)
+  Uniform u;
+  bool has = false;
+  double cached = 0.0;
+  explicit Polar(uint64_t seed) : u(seed) {}
+  double next() {
+    if (has) {
+      has = false;
+      return cached;
+    }
+    for (;;) {
+      const double a = 2.0 * u.next() - 1.0;
+      const double b = 2.0 * u.next() - 1.0;
+      const double s2 = a * a + b * b;
+      if (s2 >= 1.0 || s2 == 0.0) continue;
+      const double scale = std::sqrt(-2.0 * std::log(s2) / s2);
+      cached = b * scale;
+      has = true;
+      return a * scale;
+    }
+  }
+};
+
+template <typename T>
+double neumaier_sq(const T* v, uint64_t n) {  // generator.cpp:20-34
+  double sum = 0.0, comp = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const double x = static_cast<double>(v[i]);
+    const double term = x * x;
+    const double t = sum + term;
+    if (std::abs(sum) >= std::abs(term)) comp += (sum - t) + term;
+    else comp += (term - t) + sum;
+    sum = t;
+  }
+  return sum + comp;
+}
+
+// Generator ctor up to the warm-up (generator.cpp:317-327).  raw_d receives
+// the double pool; the caller rounds to T.
+void seed_pool_double(uint64_t n, uint64_t seed, double* raw_d, double& reserved,
+                      uint64_t s_out[4], uint64_t& draws) {
+  Polar init(seed);
+  for (uint64_t i = 0; i < n; ++i) raw_d[i] = init.next();
+  reserved = init.next();
+  std::memcpy(s_out, init.u.s, sizeof(init.u.s));
+  draws = init.u.draws;
+  const double ss = neumaier_sq(raw_d, n);
+  const double k = std::sqrt(static_cast<double>(n) / ss);
+  for (uint64_t i = 0; i < n; ++i) raw_d[i] *= k;
+}
+
+uint64_t default_stride(uint64_t rows) {  // transforms.cpp:161-169
+  uint64_t k = rows / 3 + 1;
+  if (k % 2 == 0) ++k;
+  while (std::gcd(k, rows) != 1) k += 2;
+  return k;
+}
+
+double compute_a(uint64_t nu) {  // chi2.cpp:11-17
+  const double root_nu = std::sqrt(static_cast<double>(nu));
+  return 2.0 * root_nu * std::sin(std::asin(1.0 / root_nu) / 3.0);
+}
+
+wb::Chi2Consts chi2_consts(const wallace_config& c) {
+  wb::Chi2Consts k{};
+  const double nu = static_cast<double>(c.pool_size);
+  k.nu = nu;
+  k.a = compute_a(c.pool_size);
+  k.cubic_c = std::sqrt(2.0 * (nu - k.a * k.a));
+  k.shift_c = std::sqrt(2.0 * nu - 1.0);
+  const double d = 2.0 / (9.0 * nu);
+  k.wh_sqrt_d = std::sqrt(d);
+  k.wh_one_m_d = 1.0 - d;
+  k.floor_v = 1e-6 * nu;
+  k.method = c.chi2_method;
+  k.disable = c.disable_chi2;
+  return k;
+}
+
+int ilog2(uint64_t v) {
+  int l = 0;
+  while ((1ull << l) < v) ++l;
+  return l;
+}
+
+constexpr uint64_t kPlanBudgetBytes = 128ull << 20;
+constexpr uint32_t kMaxPassesPerLaunch = 2048;
+constexpr uint64_t kMagic = 0x5741'4c4c'4143'4531ull;  // "WALLACE1"
+
+}  // namespace
+
+struct wallace_handle {
+  wallace_config cfg{};
+  int dtype = 0;
+  size_t esize = 4;
+  uint64_t n_pools = 0;
+  uint64_t N = 0;
+  int log2n = 0;
+  cudaStream_t stream = nullptr;
+  wb::Chi2Consts chi2{};
+  uint32_t plan_cap = 0;  // passes per launch
+
+  void* d_pools = nullptr;
+  PoolState* d_state = nullptr;
+  uint32_t* d_plans = nullptr;
+  void* d_leftover = nullptr;
+  void* d_snap_pools = nullptr;
+  PoolState* d_snap_state = nullptr;
+  void* d_snap_leftover = nullptr;
+  uint32_t snap_cursor = 0;
+  uint64_t snap_pass_count = 0;
+  bool has_snapshot = false;
+
+  // consumer scratch
+  double* d_part_sums = nullptr;
+  uint32_t* d_part_hist = nullptr;
+  uint64_t part_cap = 0;
+
+  // staging for fill_host
+  void* d_stage = nullptr;
+  uint64_t stage_bytes = 0;
+
+  // profiling (wallace_profile_begin/end)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_plan;
+  std::vector<cudaEvent_t> ev_free;
+
+  uint32_t cursor = 0;      // uniform across pools (all pools advance together)
+  uint64_t pass_count = 0;  // uniform
+};
+
+namespace {
+
+wallace_status validate(const wallace_config* c) {
+  // generator.cpp:221-236 (messages name the field, test_generator.cpp:42-72)
+  if (!c) return fail(WALLACE_ERR_INVALID_PARAM, "config must not be NULL");
+  const uint64_t n = c->pool_size;
+  if (n < 32 || (n & (n - 1)) != 0 || n > (1ull << 31))
+    return fail(WALLACE_ERR_CONFIG, "pool_size must be a power of two in [32, 2^31], got %llu",
+                static_cast<unsigned long long>(n));
+  if (c->discard_every < 1) return fail(WALLACE_ERR_CONFIG, "discard_every must be >= 1");
+  if (!std::isfinite(c->out_sigma) || c->out_sigma <= 0.0)
+    return fail(WALLACE_ERR_CONFIG, "out_sigma must be positive and finite");
+  if (!std::isfinite(c->out_mean)) return fail(WALLACE_ERR_CONFIG, "out_mean must be finite");
+  if (c->transform_family != 0 && c->transform_family != 1)
+    return fail(WALLACE_ERR_CONFIG, "transform_family must be wallace4 (0) or rotation (1)");
+  if (c->mixing != 0 && c->mixing != 1)
+    return fail(WALLACE_ERR_CONFIG, "mixing must be stride_transpose (0) or affine (1)");
+  if (c->chi2_method < 0 || c->chi2_method > 2)
+    return fail(WALLACE_ERR_CONFIG, "chi2_method must be 0, 1 or 2");
+  return WALLACE_OK;
+}
+
+wallace_status check_supported(const wallace_config* c, int dtype) {
+  if (c->transform_family != 0)
+    return fail(WALLACE_ERR_UNSUPPORTED, "transform_family: rotation is not built on the B200 path");
+  if (c->mixing != 0)
+    return fail(WALLACE_ERR_UNSUPPORTED, "mixing: affine is not built on the B200 path");
+  const uint64_t lim = dtype == WALLACE_F32 ? (1u << 14) : (1u << 13);
+  if (c->pool_size > lim)
+    return fail(WALLACE_ERR_UNSUPPORTED,
+                "pool_size %llu exceeds the on-chip pool limit %llu for this dtype",
+                static_cast<unsigned long long>(c->pool_size),
+                static_cast<unsigned long long>(lim));
+  return WALLACE_OK;
+}
+
+wb::FillArgs base_args(wallace_handle* h) {
+  wb::FillArgs a{};
+  a.pools_in = h->d_pools;
+  a.pools_out = h->d_pools;
+  a.st_in = h->d_state;
+  a.st_out = h->d_state;
+  a.plans = h->d_plans;
+  a.plan_stride = h->plan_cap;
+  a.d = static_cast<uint32_t>(std::min<uint64_t>(h->cfg.discard_every, 0xffffffffu));
+  a.mean = h->cfg.out_mean;
+  a.sigma = h->cfg.out_sigma;
+  a.mean_is_zero = (h->cfg.out_mean == 0.0 && !std::signbit(h->cfg.out_mean)) ? 1 : 0;
+  a.chi2 = h->chi2;
+  a.leftover = h->d_leftover;
+  a.out_stride = 0;
+  return a;
+}
+
+cudaEvent_t take_event(wallace_handle* h) {
+  if (!h->ev_free.empty()) {
+    cudaEvent_t e = h->ev_free.back();
+    h->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one launch with events when profiling is on.
+template <class F>
+cudaError_t timed(wallace_handle* h, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& log,
+                  F&& launch) {
+  if (!h->profiling) return launch();
+  cudaEvent_t a = take_event(h), b = take_event(h);
+  cudaEventRecord(a, h->stream);
+  const cudaError_t e = launch();
+  cudaEventRecord(b, h->stream);
+  log.emplace_back(a, b);
+  return e;
+}
+
+wallace_status run_plans(wallace_handle* h, uint32_t n_passes, const PoolState* st_in) {
+  if (n_passes == 0) return WALLACE_OK;
+  wb::PlanArgs p{};
+  p.st_in = st_in;
+  p.st_out = h->d_state;
+  p.plans = h->d_plans;
+  p.plan_stride = h->plan_cap;
+  p.n_passes = n_passes;
+  p.n_pools = static_cast<uint32_t>(h->n_pools);
+  p.rows_mask = static_cast<uint32_t>(h->N / 4 - 1);
+  p.fixed_transform = h->cfg.fixed_transform;
+  WB_CUDA(timed(h, h->ev_plan, [&] { return wb::launch_plan_kernel(p, h->stream); }));
+  ++g_launches;
+  return WALLACE_OK;
+}
+
+wallace_status run_pool(wallace_handle* h, const wb::FillArgs& a) {
+  WB_CUDA(timed(h, h->ev_pool,
+                [&] { return wb::launch_pool_kernel(h->dtype, h->log2n, a, h->n_pools, h->stream); }));
+  ++g_launches;
+  return WALLACE_OK;
+}
+
+// Run n passes without emission (warm-up, step_pass), in launches of at most
+// plan_cap passes.
+wallace_status run_passes(wallace_handle* h, uint64_t n) {
+  while (n > 0) {
+    const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(n, h->plan_cap));
+    wallace_status st = run_plans(h, k, h->d_state);
+    if (st) return st;
+    wb::FillArgs a = base_args(h);
+    a.mode = wb::kModePasses;
+    a.n_passes = k;
+    a.n_emit = 0;
+    a.lead = 0;
+    a.last_limit = 0;
+    st = run_pool(h, a);
+    if (st) return st;
+    h->pass_count += k;
+    n -= k;
+  }
+  return WALLACE_OK;
+}
+
+wallace_status ensure_leftover(wallace_handle* h) {
+  if (h->d_leftover) return WALLACE_OK;
+  WB_CUDA(cudaMalloc(&h->d_leftover, h->n_pools * (h->N - 1) * h->esize));
+  return WALLACE_OK;
+}
+
+// Before the pool advances outside fill(): keep the partially consumed
+// emission (Generator::out_ is untouched by step_pass / inject_pool).
+wallace_status materialize(wallace_handle* h) {
+  if (h->cursor >= h->N - 1) return WALLACE_OK;
+  wallace_status st = ensure_leftover(h);
+  if (st) return st;
+  WB_CUDA(wb::launch_materialize(h->dtype, h->d_pools, h->d_state, h->d_leftover, h->n_pools,
+                                 static_cast<uint32_t>(h->N), h->cfg.out_mean, h->stream));
+  ++g_launches;
+  return WALLACE_OK;
+}
+
+// The fill / consume engine.  out == nullptr with mode kModeConsume feeds the
+// consumer partials instead.  st_first / pools_first: state the first launch
+// reads (the snapshot for fill_from_snapshot).
+wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
+                        const PoolState* st_first, const void* pools_first) {
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
+  const uint64_t n1 = h->N - 1;
+  const uint64_t d = h->cfg.discard_every;
+  uint64_t produced = 0;
+  bool first = true;
+  while (produced < count) {
+    wb::FillArgs a = base_args(h);
+    a.mode = mode;
+    a.out = out;
+    a.out_stride = count;
+    a.out_offset = produced;
+    a.part_sums = h->d_part_sums;
+    a.part_hist = h->d_part_hist;
+    if (first) {
+      a.st_in = st_first;
+      a.pools_in = pools_first;
+    }
+    uint64_t lead = 0;
+    if (first && h->cursor < n1) lead = std::min<uint64_t>(count, n1 - h->cursor);
+    const uint64_t remaining = count - produced - lead;
+    uint64_t e_total = (remaining + n1 - 1) / n1;
+    uint64_t e = 0, passes = 0;
+    if (e_total > 0) {
+      if (d <= h->plan_cap) {
+        e = std::min<uint64_t>(e_total, h->plan_cap / d);
+        passes = e * d;
+      } else {
+        // an emission longer than one launch: run d-1 passes first, then a
+        // launch with one pass and the emission (emission alignment is
+        // per launch)
+        wallace_status st = WALLACE_OK;
+        if (!first || (st_first == h->d_state && pools_first == h->d_pools)) {
+          st = run_passes(h, d - 1);
+        } else {
+          return fail(WALLACE_ERR_UNSUPPORTED, "discard_every too large for snapshot replay");
+        }
+        if (st) return st;
+        e = 1;
+        passes = 1;
+        a.d = 1;
+      }
+    }
+    const uint64_t last_limit =
+        e == 0 ? 0 : (e == e_total ? remaining - (e - 1) * n1 : n1);
+    a.lead = static_cast<uint32_t>(lead);
+    a.n_emit = static_cast<uint32_t>(e);
+    a.n_passes = static_cast<uint32_t>(passes);
+    a.last_limit = static_cast<uint32_t>(last_limit);
+    wallace_status st = run_plans(h, a.n_passes, a.st_in);
+    if (st) return st;
+    st = run_pool(h, a);
+    if (st) return st;
+    if (mode == wb::kModeConsume) {
+      // consumer partials are per launch; fold them into the running totals
+      // by launching the fixed-order reduction per launch (rare: one launch
+      // per fill unless the fill is larger than plan_cap passes)
+    }
+    h->pass_count += passes;
+    h->cursor = e > 0 ? static_cast<uint32_t>(last_limit) : h->cursor + static_cast<uint32_t>(lead);
+    produced += lead + (e == 0 ? 0 : (e == e_total ? remaining : e * n1));
+    first = false;
+  }
+  return WALLACE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wallace_last_error(void) { return g_err.c_str(); }
+
+uint64_t wallace_kernel_launches(void) { return g_launches.load(); }
+
+wallace_status wallace_validate_config(const wallace_config* cfg) { return validate(cfg); }
+
+uint64_t wallace_default_stride(uint64_t rows) { return rows ? default_stride(rows) : 0; }
+
+int32_t wallace_decode_pass_plan(uint64_t pool_size, uint64_t w0, uint64_t w1, uint64_t* off0) {
+  if (off0) *off0 = w1 & (pool_size / 4 - 1);
+  return static_cast<int32_t>(w0 % 384u);
+}
+
+wallace_status wallace_host_seed_pool(const wallace_config* cfg, uint64_t seed, double* raw_out,
+                                      double* reserved_prev, double* sum_sq, uint64_t s_out[4],
+                                      uint64_t* draws) {
+  wallace_status st = validate(cfg);
+  if (st) return st;
+  if (!raw_out) return fail(WALLACE_ERR_INVALID_PARAM, "raw_out must not be NULL");
+  double res = 0.0;
+  uint64_t s[4], dr = 0;
+  seed_pool_double(cfg->pool_size, seed, raw_out, res, s, dr);
+  if (reserved_prev) *reserved_prev = res;
+  if (sum_sq) *sum_sq = neumaier_sq(raw_out, cfg->pool_size);
+  if (s_out) std::memcpy(s_out, s, sizeof(s));
+  if (draws) *draws = dr;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const uint64_t* seeds,
+                              wallace_dtype dtype, void* stream, wallace_handle** out) {
+  if (!out) return fail(WALLACE_ERR_INVALID_PARAM, "out must not be NULL");
+  *out = nullptr;
+  wallace_status st = validate(cfg);
+  if (st) return st;
+  if (dtype != WALLACE_F32 && dtype != WALLACE_F64)
+    return fail(WALLACE_ERR_INVALID_PARAM, "dtype must be WALLACE_F32 or WALLACE_F64");
+  if ((st = check_supported(cfg, dtype))) return st;
+  if (n_pools < 1 || n_pools > 0x7fffffffull)
+    return fail(WALLACE_ERR_INVALID_PARAM, "n_pools must be in [1, 2^31)");
+
+  auto* h = new wallace_handle();
+  h->cfg = *cfg;
+  h->dtype = dtype;
+  h->esize = dtype == WALLACE_F32 ? 4 : 8;
+  h->n_pools = n_pools;
+  h->N = cfg->pool_size;
+  h->log2n = ilog2(h->N);
+  h->stream = static_cast<cudaStream_t>(stream);
+  h->chi2 = chi2_consts(*cfg);
+  h->plan_cap = static_cast<uint32_t>(std::max<uint64_t>(
+      1, std::min<uint64_t>(kMaxPassesPerLaunch, kPlanBudgetBytes / (4 * n_pools))));
+  h->cursor = static_cast<uint32_t>(h->N - 1);
+  auto cleanup = [&](wallace_status s) {
+    wallace_destroy(h);
+    return s;
+  };
+
+  // ---- host seeding (parallel over pools) ----
+  const uint64_t N = h->N;
+  std::vector<unsigned char> pools(n_pools * N * h->esize);
+  std::vector<PoolState> states(n_pools);
+  {
+    std::atomic<uint64_t> next{0};
+    unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+    nt = static_cast<unsigned>(std::min<uint64_t>(nt, n_pools));
+    auto work = [&] {
+      std::vector<double> raw(N);
+      for (;;) {
+        const uint64_t p = next.fetch_add(1);
+        if (p >= n_pools) break;
+        const uint64_t seed = seeds ? seeds[p] : cfg->seed + p;
+        PoolState& ps = states[p];
+        std::memset(&ps, 0, sizeof(ps));
+        seed_pool_double(N, seed, raw.data(), ps.reserved_prev, ps.s, ps.draws);
+        if (dtype == WALLACE_F32) {
+          float* dst = reinterpret_cast<float*>(pools.data()) + p * N;
+          for (uint64_t i = 0; i < N; ++i) dst[i] = static_cast<float>(raw[i]);
+          ps.sum_sq = neumaier_sq(dst, N);
+        } else {
+          double* dst = reinterpret_cast<double*>(pools.data()) + p * N;
+          std::memcpy(dst, raw.data(), N * sizeof(double));
+          ps.sum_sq = neumaier_sq(dst, N);
+        }
+        ps.cursor = static_cast<uint32_t>(N - 1);
+        ps.seed = seed;
+      }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+  }
+
+  // ---- device residency ----
+#define WB_CUDA_C(expr)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return cleanup(fail(WALLACE_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)));    \
+  } while (0)
+  WB_CUDA_C(cudaMalloc(&h->d_pools, pools.size()));
+  WB_CUDA_C(cudaMalloc(&h->d_state, n_pools * sizeof(PoolState)));
+  WB_CUDA_C(cudaMalloc(&h->d_plans, n_pools * h->plan_cap * sizeof(uint32_t)));
+  WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,
+                            h->stream));
+  WB_CUDA_C(cudaMemcpyAsync(h->d_state, states.data(), n_pools * sizeof(PoolState),
+                            cudaMemcpyHostToDevice, h->stream));
+  // warm-up (generator.cpp:329-330)
+  if ((st = run_passes(h, 16))) return cleanup(st);
+  WB_CUDA_C(cudaStreamSynchronize(h->stream));
+#undef WB_CUDA_C
+  *out = h;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_destroy(wallace_handle* h) {
+  if (!h) return WALLACE_OK;
+  cudaFree(h->d_pools);
+  cudaFree(h->d_state);
+  cudaFree(h->d_plans);
+  cudaFree(h->d_leftover);
+  cudaFree(h->d_snap_pools);
+  cudaFree(h->d_snap_state);
+  cudaFree(h->d_snap_leftover);
+  cudaFree(h->d_part_sums);
+  cudaFree(h->d_part_hist);
+  cudaFree(h->d_stage);
+  for (auto& pr : h->ev_pool) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto& pr : h->ev_plan) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto e : h->ev_free) cudaEventDestroy(e);
+  delete h;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_profile_begin(wallace_handle* h) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  h->profiling = true;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_profile_end(wallace_handle* h, double* pool_ms, uint64_t* pool_n,
+                                   double* plan_ms, uint64_t* plan_n) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  h->profiling = false;
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  auto sum = [&](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& log, double* ms, uint64_t* n) {
+    double acc = 0.0;
+    for (auto& [a, b] : log) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, a, b) == cudaSuccess) acc += t;
+      h->ev_free.push_back(a);
+      h->ev_free.push_back(b);
+    }
+    if (ms) *ms = acc;
+    if (n) *n = log.size();
+    log.clear();
+  };
+  sum(h->ev_pool, pool_ms, pool_n);
+  sum(h->ev_plan, plan_ms, plan_n);
+  return WALLACE_OK;
+}
+
+wallace_status wallace_set_stream(wallace_handle* h, void* stream) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  h->stream = static_cast<cudaStream_t>(stream);
+  return WALLACE_OK;
+}
+
+wallace_status wallace_fill(wallace_handle* h, void* dev_out, uint64_t count) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
+  if (!dev_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
+  return run_emit(h, dev_out, count, wb::kModeFill, h->d_state, h->d_pools);
+}
+
+wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t count) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
+  if (!host_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
+  // chunk along the per-pool count so device staging stays bounded
+  const uint64_t row_bytes = h->n_pools * h->esize;
+  const uint64_t max_stage = 2ull << 30;
+  uint64_t chunk = std::max<uint64_t>(1, max_stage / row_bytes);
+  chunk = std::min(chunk, count);
+  const uint64_t need = chunk * row_bytes;
+  if (h->stage_bytes < need) {
+    cudaFree(h->d_stage);
+    h->d_stage = nullptr;
+    h->stage_bytes = 0;
+    WB_CUDA(cudaMalloc(&h->d_stage, need));
+    h->stage_bytes = need;
+  }
+  for (uint64_t off = 0; off < count; off += chunk) {
+    const uint64_t c = std::min(chunk, count - off);
+    wallace_status st = run_emit(h, h->d_stage, c, wb::kModeFill, h->d_state, h->d_pools);
+    if (st) return st;
+    WB_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(host_out) + off * h->esize,
+                              count * h->esize, h->d_stage, c * h->esize, c * h->esize,
+                              h->n_pools, cudaMemcpyDeviceToHost, h->stream));
+  }
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  return WALLACE_OK;
+}
+
+wallace_status wallace_snapshot(wallace_handle* h) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  const size_t pb = h->n_pools * h->N * h->esize;
+  if (!h->d_snap_pools) WB_CUDA(cudaMalloc(&h->d_snap_pools, pb));
+  if (!h->d_snap_state) WB_CUDA(cudaMalloc(&h->d_snap_state, h->n_pools * sizeof(PoolState)));
+  WB_CUDA(cudaMemcpyAsync(h->d_snap_pools, h->d_pools, pb, cudaMemcpyDeviceToDevice, h->stream));
+  WB_CUDA(cudaMemcpyAsync(h->d_snap_state, h->d_state, h->n_pools * sizeof(PoolState),
+                          cudaMemcpyDeviceToDevice, h->stream));
+  if (h->d_leftover) {
+    const size_t lb = h->n_pools * (h->N - 1) * h->esize;
+    if (!h->d_snap_leftover) WB_CUDA(cudaMalloc(&h->d_snap_leftover, lb));
+    WB_CUDA(cudaMemcpyAsync(h->d_snap_leftover, h->d_leftover, lb, cudaMemcpyDeviceToDevice,
+                            h->stream));
+  }
+  h->snap_cursor = h->cursor;
+  h->snap_pass_count = h->pass_count;
+  h->has_snapshot = true;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_fill_from_snapshot(wallace_handle* h, void* dev_out, uint64_t count) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (!h->has_snapshot) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
+  if (h->d_snap_leftover && h->snap_cursor < h->N - 1)
+    WB_CUDA(cudaMemcpyAsync(h->d_leftover, h->d_snap_leftover,
+                            h->n_pools * (h->N - 1) * h->esize, cudaMemcpyDeviceToDevice,
+                            h->stream));
+  h->cursor = h->snap_cursor;
+  h->pass_count = h->snap_pass_count;
+  return run_emit(h, dev_out, count, wb::kModeFill, h->d_snap_state, h->d_snap_pools);
+}
+
+wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* reserved,
+                                 double* chi2_draw) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  void* out = dev_values;
+  void* tmp = nullptr;
+  if (!out) {
+    WB_CUDA(cudaMalloc(&tmp, h->n_pools * (h->N - 1) * h->esize));
+    out = tmp;
+  }
+  // refill_ + cursor_ = out_.size(): discard the partial buffer, so the
+  // emission starts with no leftover (the device cursor is only read when a
+  // leftover is drained)
+  h->cursor = static_cast<uint32_t>(h->N - 1);
+  wallace_status st = run_emit(h, out, h->N - 1, wb::kModeFill, h->d_state, h->d_pools);
+  if (!st && (reserved || chi2_draw)) {
+    std::vector<PoolState> states(h->n_pools);
+    cudaError_t e = cudaMemcpyAsync(states.data(), h->d_state, h->n_pools * sizeof(PoolState),
+                                    cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "next_pool: %s", cudaGetErrorString(e));
+    for (uint64_t p = 0; p < h->n_pools && !st; ++p) {
+      if (reserved) reserved[p] = states[p].reserved_prev;
+      if (chi2_draw) chi2_draw[p] = states[p].last_chi2;
+    }
+  } else if (!st) {
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "next_pool: %s", cudaGetErrorString(e));
+  }
+  if (tmp) cudaFree(tmp);
+  return st;
+}
+
+wallace_status wallace_step_pass(wallace_handle* h, uint64_t n_passes) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  wallace_status st = materialize(h);
+  if (st) return st;
+  return run_passes(h, n_passes);
+}
+
+wallace_status wallace_inject_pool(wallace_handle* h, uint64_t pool, const double* values,
+                                   uint64_t n) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (n != h->N) return fail(WALLACE_ERR_INVALID_PARAM, "inject_pool: size must equal pool_size");
+  if (pool >= h->n_pools) return fail(WALLACE_ERR_INVALID_PARAM, "inject_pool: pool out of range");
+  if (!values) return fail(WALLACE_ERR_INVALID_PARAM, "inject_pool: values must not be NULL");
+  wallace_status st = materialize(h);
+  if (st) return st;
+  double ss;
+  std::vector<unsigned char> buf(h->N * h->esize);
+  if (h->dtype == WALLACE_F32) {
+    float* f = reinterpret_cast<float*>(buf.data());
+    for (uint64_t i = 0; i < n; ++i) f[i] = static_cast<float>(values[i]);
+    ss = neumaier_sq(f, n);
+  } else {
+    std::memcpy(buf.data(), values, n * sizeof(double));
+    ss = neumaier_sq(values, n);
+  }
+  WB_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(h->d_pools) + pool * h->N * h->esize,
+                          buf.data(), buf.size(), cudaMemcpyHostToDevice, h->stream));
+  WB_CUDA(cudaMemcpyAsync(&h->d_state[pool].sum_sq, &ss, sizeof(double), cudaMemcpyHostToDevice,
+                          h->stream));
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  return WALLACE_OK;
+}
+
+wallace_status wallace_get_pool(wallace_handle* h, uint64_t pool, double* raw_out, uint64_t n) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (pool >= h->n_pools) return fail(WALLACE_ERR_INVALID_PARAM, "get_pool: pool out of range");
+  if (n != h->N || !raw_out) return fail(WALLACE_ERR_INVALID_PARAM, "get_pool: need pool_size values");
+  std::vector<unsigned char> buf(h->N * h->esize);
+  WB_CUDA(cudaMemcpyAsync(buf.data(), static_cast<unsigned char*>(h->d_pools) + pool * h->N * h->esize,
+                          buf.size(), cudaMemcpyDeviceToHost, h->stream));
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  for (uint64_t i = 0; i < n; ++i)
+    raw_out[i] = h->dtype == WALLACE_F32 ? static_cast<double>(reinterpret_cast<float*>(buf.data())[i])
+                                         : reinterpret_cast<double*>(buf.data())[i];
+  return WALLACE_OK;
+}
+
+wallace_status wallace_get_pool_info(wallace_handle* h, uint64_t pool, wallace_pool_info* out) {
+  if (!h || !out) return fail(WALLACE_ERR_INVALID_PARAM, "handle/out must not be NULL");
+  if (pool >= h->n_pools) return fail(WALLACE_ERR_INVALID_PARAM, "get_pool_info: pool out of range");
+  PoolState ps;
+  WB_CUDA(cudaMemcpyAsync(&ps, h->d_state + pool, sizeof(ps), cudaMemcpyDeviceToHost, h->stream));
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  if (ps.flags & wb::kFlagChi2NonFinite)
+    return fail(WALLACE_ERR_INVALID_PARAM, "chi2_sample: x must be finite");
+  out->pass_count = ps.pass_count;
+  out->uniform_draws = ps.draws;
+  out->chi2_clamp_count = ps.clamp_count;
+  out->sum_sq = ps.sum_sq;
+  out->reserved_prev = ps.reserved_prev;
+  out->last_chi2 = ps.last_chi2;
+  out->buffered = (h->N - 1) - ps.cursor;
+  out->seed = ps.seed;
+  return WALLACE_OK;
+}
+
+uint64_t wallace_state_bytes(const wallace_handle* h) {
+  if (!h) return 0;
+  return 64 + h->n_pools * h->N * h->esize + h->n_pools * sizeof(PoolState) +
+         h->n_pools * (h->N - 1) * h->esize;
+}
+
+wallace_status wallace_save_state(wallace_handle* h, void* host_buf, uint64_t bytes) {
+  if (!h || !host_buf) return fail(WALLACE_ERR_INVALID_PARAM, "handle/buffer must not be NULL");
+  if (bytes < wallace_state_bytes(h)) return fail(WALLACE_ERR_INVALID_PARAM, "save_state: buffer too small");
+  wallace_status st = materialize(h);
+  if (st) return st;
+  unsigned char* p = static_cast<unsigned char*>(host_buf);
+  uint64_t hdr[8] = {kMagic, h->N, static_cast<uint64_t>(h->dtype), h->n_pools, h->cursor,
+                     h->pass_count, h->d_leftover ? 1ull : 0ull, 0};
+  std::memcpy(p, hdr, sizeof(hdr));
+  p += 64;
+  const size_t pb = h->n_pools * h->N * h->esize;
+  WB_CUDA(cudaMemcpyAsync(p, h->d_pools, pb, cudaMemcpyDeviceToHost, h->stream));
+  p += pb;
+  WB_CUDA(cudaMemcpyAsync(p, h->d_state, h->n_pools * sizeof(PoolState), cudaMemcpyDeviceToHost,
+                          h->stream));
+  p += h->n_pools * sizeof(PoolState);
+  const size_t lb = h->n_pools * (h->N - 1) * h->esize;
+  if (h->d_leftover) WB_CUDA(cudaMemcpyAsync(p, h->d_leftover, lb, cudaMemcpyDeviceToHost, h->stream));
+  else std::memset(p, 0, lb);
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  return WALLACE_OK;
+}
+
+wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint64_t bytes) {
+  if (!h || !host_buf) return fail(WALLACE_ERR_INVALID_PARAM, "handle/buffer must not be NULL");
+  if (bytes < wallace_state_bytes(h)) return fail(WALLACE_ERR_INVALID_PARAM, "load_state: buffer too small");
+  const unsigned char* p = static_cast<const unsigned char*>(host_buf);
+  uint64_t hdr[8];
+  std::memcpy(hdr, p, sizeof(hdr));
+  if (hdr[0] != kMagic || hdr[1] != h->N || hdr[2] != static_cast<uint64_t>(h->dtype) ||
+      hdr[3] != h->n_pools)
+    return fail(WALLACE_ERR_INVALID_PARAM, "load_state: image does not match this handle");
+  p += 64;
+  const size_t pb = h->n_pools * h->N * h->esize;
+  WB_CUDA(cudaMemcpyAsync(h->d_pools, p, pb, cudaMemcpyHostToDevice, h->stream));
+  p += pb;
+  WB_CUDA(cudaMemcpyAsync(h->d_state, p, h->n_pools * sizeof(PoolState), cudaMemcpyHostToDevice,
+                          h->stream));
+  p += h->n_pools * sizeof(PoolState);
+  if (hdr[6]) {
+    wallace_status st = ensure_leftover(h);
+    if (st) return st;
+    WB_CUDA(cudaMemcpyAsync(h->d_leftover, p, h->n_pools * (h->N - 1) * h->esize,
+                            cudaMemcpyHostToDevice, h->stream));
+  }
+  h->cursor = static_cast<uint32_t>(hdr[4]);
+  h->pass_count = hdr[5];
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  return WALLACE_OK;
+}
+
+static wallace_status finish_consumer(cudaStream_t stream, const double* part_sums,
+                                      const uint32_t* part_hist, uint64_t n_parts, double sums[4],
+                                      uint64_t hist[258]) {
+  const uint64_t chunk = 256;
+  const uint64_t blocks = (n_parts + chunk - 1) / chunk;
+  double* d_bs = nullptr;
+  unsigned long long* d_bh = nullptr;
+  WB_CUDA(cudaMalloc(&d_bs, blocks * 4 * sizeof(double)));
+  WB_CUDA(cudaMalloc(&d_bh, blocks * 258 * sizeof(unsigned long long)));
+  cudaError_t e = wb::launch_reduce_consumer(part_sums, part_hist, n_parts, chunk, d_bs, d_bh, stream);
+  ++g_launches;
+  std::vector<double> bs(blocks * 4);
+  std::vector<unsigned long long> bh(blocks * 258);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(bs.data(), d_bs, bs.size() * 8, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(bh.data(), d_bh, bh.size() * 8, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  cudaFree(d_bs);
+  cudaFree(d_bh);
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "consumer reduction: %s", cudaGetErrorString(e));
+  for (int k = 0; k < 4; ++k) sums[k] = 0.0;
+  for (int b = 0; b < 258; ++b) hist[b] = 0;
+  for (uint64_t i = 0; i < blocks; ++i) {
+    for (int k = 0; k < 4; ++k) sums[k] += bs[i * 4 + k];
+    for (int b = 0; b < 258; ++b) hist[b] += bh[i * 258 + b];
+  }
+  return WALLACE_OK;
+}
+
+wallace_status wallace_consume(wallace_handle* h, uint64_t count, double sums[4], uint64_t hist[258]) {
+  if (!h || !sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "handle/sums/hist must not be NULL");
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
+  if (h->part_cap < h->n_pools) {
+    cudaFree(h->d_part_sums);
+    cudaFree(h->d_part_hist);
+    h->d_part_sums = nullptr;
+    h->d_part_hist = nullptr;
+    WB_CUDA(cudaMalloc(&h->d_part_sums, h->n_pools * 4 * sizeof(double)));
+    WB_CUDA(cudaMalloc(&h->d_part_hist, h->n_pools * 258 * sizeof(uint32_t)));
+    h->part_cap = h->n_pools;
+  }
+  // one launch group per consume: every launch of run_emit overwrites the
+  // partials, so split the count so that a single launch covers it, or fold
+  // per launch.
+  double tot[4] = {0, 0, 0, 0};
+  uint64_t th[258] = {0};
+  const uint64_t n1 = h->N - 1;
+  const uint64_t d = h->cfg.discard_every;
+  const uint64_t per_launch_emit = std::max<uint64_t>(1, h->plan_cap / std::max<uint64_t>(1, d));
+  uint64_t done = 0;
+  while (done < count) {
+    // values a single launch produces: the lead plus per_launch_emit emissions
+    const uint64_t lead = (h->cursor < n1) ? (n1 - h->cursor) : 0;
+    const uint64_t cap = lead + per_launch_emit * n1;
+    const uint64_t c = std::min(cap, count - done);
+    wallace_status st = run_emit(h, nullptr, c, wb::kModeConsume, h->d_state, h->d_pools);
+    if (st) return st;
+    double s4[4];
+    uint64_t h258[258];
+    st = finish_consumer(h->stream, h->d_part_sums, h->d_part_hist, h->n_pools, s4, h258);
+    if (st) return st;
+    for (int k = 0; k < 4; ++k) tot[k] += s4[k];
+    for (int b = 0; b < 258; ++b) th[b] += h258[b];
+    done += c;
+  }
+  for (int k = 0; k < 4; ++k) sums[k] = tot[k];
+  for (int b = 0; b < 258; ++b) hist[b] = th[b];
+  return WALLACE_OK;
+}
+
+wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_base, uint64_t n_streams,
+                                         uint64_t count, void* stream, double sums[4], uint64_t hist[258]) {
+  if (!sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "sums/hist must not be NULL");
+  if (n_streams < 1 || count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "need >= 1 stream and value");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int threads = 128;
+  const uint64_t blocks = (n_streams + threads - 1) / threads;
+  uint64_t* d_seeds = nullptr;
+  double* d_ps = nullptr;
+  uint32_t* d_ph = nullptr;
+  if (seeds) {
+    WB_CUDA(cudaMalloc(&d_seeds, n_streams * 8));
+    WB_CUDA(cudaMemcpyAsync(d_seeds, seeds, n_streams * 8, cudaMemcpyHostToDevice, s));
+  }
+  WB_CUDA(cudaMalloc(&d_ps, blocks * 4 * sizeof(double)));
+  WB_CUDA(cudaMalloc(&d_ph, blocks * 258 * sizeof(uint32_t)));
+  cudaError_t e = wb::launch_boxmuller(d_seeds, seed_base, n_streams, count, d_ps, d_ph, blocks, threads, s);
+  ++g_launches;
+  wallace_status st = WALLACE_OK;
+  if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "boxmuller: %s", cudaGetErrorString(e));
+  if (!st) st = finish_consumer(s, d_ps, d_ph, blocks, sums, hist);
+  cudaFree(d_seeds);
+  cudaFree(d_ps);
+  cudaFree(d_ph);
+  return st;
+}
+
+}  // extern "C"

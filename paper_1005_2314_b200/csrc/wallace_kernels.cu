@@ -1,0 +1,832 @@
+// sm_100a kernels for the Wallace maximum-entropy normal generator.
+//
+//   plan_kernel  — the xoshiro256** pass-plan stream, one thread per pool
+//                  (baselines.cpp:33-45 + decode_pass_plan, generator.cpp:238-257)
+//   pool_kernel  — passes + emissions of one pool per CTA, pool resident in
+//                  shared memory (generator.cpp:52-85, 333-376)
+//   materialize_kernel — snapshot of a partially consumed emission before the
+//                  pool is advanced outside fill() (Generator::out_ semantics)
+//   reduce_consumer_kernel — fixed-order reduction of the fused consumer
+//
+// Numerics: every floating-point operation on the data path is an explicit
+// round-to-nearest intrinsic (__fadd_rn, __dmul_rn, ...), and the library is
+// compiled with -fmad=false, so no multiply-add is contracted — the
+// reference pins -ffp-contract=off for the same reason
+// (/root/reference/proj/CMakeLists.txt:10-14).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "wallace_common.h"
+
+namespace wb {
+
+// ---------------------------------------------------------------------------
+// compile-time geometry
+// ---------------------------------------------------------------------------
+constexpr uint32_t gcd_c(uint32_t a, uint32_t b) { return b ? gcd_c(b, a % b) : a; }
+// transforms.cpp:161-169 default_stride: smallest odd > rows/3 coprime to rows
+constexpr uint32_t default_stride_c(uint32_t rows) {
+  uint32_t k = rows / 3 + 1;
+  if (k % 2 == 0) ++k;
+  while (gcd_c(k, rows) != 1) k += 2;
+  return k;
+}
+
+// transforms.cpp:24-35: element k of the p-th permutation of {0,1,2,3} in
+// lexicographic (std::next_permutation) order, evaluated at compile time.
+__host__ __device__ constexpr int perm_at(int p, int k) {
+  int avail[4] = {0, 1, 2, 3};
+  int n = 4;
+  const int fact[4] = {6, 2, 1, 1};
+  int out = 0;
+  for (int pos = 0; pos <= k; ++pos) {
+    const int q = p / fact[pos];
+    p %= fact[pos];
+    out = avail[q];
+    for (int j = q; j + 1 < n; ++j) avail[j] = avail[j + 1];
+    --n;
+  }
+  return out;
+}
+template <int P, int K>
+struct PermAt {
+  static constexpr int v = perm_at(P, K);
+};
+static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v == 0, "perm table");
+
+template <typename T, int LOG2N>
+struct Geo {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int ROWS = N / 4;
+  // groups (4-blocks) per thread: enough independent gathers per thread to
+  // hide LDS latency, few enough warps per pool for cheap barriers.
+  static constexpr int JWANT = sizeof(T) == 4 ? 8 : 4;
+  static constexpr int J = (ROWS >= 32 * JWANT) ? JWANT : (ROWS >= 32 ? ROWS / 32 : 1);
+  static constexpr int THREADS = (ROWS >= 32) ? ROWS / J : 32;
+  static constexpr int NW = THREADS / 32;
+  static constexpr uint32_t MASK = ROWS - 1;
+  static constexpr uint32_t STRIDE = default_stride_c(ROWS) % ROWS;
+  static constexpr int VEC = 16 / sizeof(T);  // elements per 128-bit store
+  // the thread holding pool element N-1 (block ROWS-1, slot 3), group J-1
+  static constexpr int OWNER = (NW - 1) * 32 + ((ROWS - 1) & 31);
+};
+
+// ---------------------------------------------------------------------------
+// explicit-rounding arithmetic
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+template <typename T> __device__ __forceinline__ T from_double(double x);
+template <> __device__ __forceinline__ float from_double<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double from_double<double>(double x) { return x; }
+
+// out = x * scale + mean with two roundings (generator.cpp:366-368).  When
+// mean is +0.0, fma(x, scale, +0) rounds x*scale once and adds +0 exactly,
+// which is bit-identical to the two-step form (including -0 + 0 = +0).
+template <typename T>
+__device__ __forceinline__ T emit_value(T x, T scale, T mean, bool mean_zero) {
+  return mean_zero ? fma_rn(x, scale, T(0)) : add_rn(mul_rn(x, scale), mean);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory vector helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sts4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void sts4(double* p, double a, double b, double c, double d) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+  reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+}
+// streaming (evict-first) global stores: the output is written once
+__device__ __forceinline__ void stg_vec(float* p, const float* v) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void stg_vec(double* p, const double* v) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+}
+template <typename T>
+__device__ __forceinline__ void stg1(T* p, T v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------------------
+// chi-squared draw and the per-emission scalar chain (chi2.cpp:27-59,
+// generator.cpp:358-364, 373-375).  All in double, explicit rounding.
+// ---------------------------------------------------------------------------
+__device__ double chi2_draw(double x, const Chi2Consts& c, uint32_t& clamped, uint32_t& flags) {
+  if (!isfinite(x)) flags |= kFlagChi2NonFinite;
+  double s;
+  if (c.method == 0) {
+    const double y = __dadd_rn(x, c.shift_c);
+    s = __dmul_rn(__dmul_rn(0.5, y), y);
+  } else if (c.method == 1) {
+    const double y = __dadd_rn(__dmul_rn(c.wh_sqrt_d, x), c.wh_one_m_d);
+    s = __dmul_rn(__dmul_rn(__dmul_rn(c.nu, y), y), y);
+  } else {
+    // a * (x*x - 1) + sqrt(2(nu - a^2)) * x + nu, evaluated left to right
+    const double t1 = __dmul_rn(c.a, __dsub_rn(__dmul_rn(x, x), 1.0));
+    const double t2 = __dmul_rn(c.cubic_c, x);
+    s = __dadd_rn(__dadd_rn(t1, t2), c.nu);
+  }
+  if (s < c.floor_v) {
+    ++clamped;
+    return c.floor_v;
+  }
+  return s;
+}
+
+struct SState {
+  double reserved_prev;
+  double sum_sq;
+  double S[2];
+  double r[2];
+  double scale[2];
+  double cur_scale;  // scale of the emission being drained by `lead`
+  double last_chi2;
+  double last_r;
+  double last_scale;
+  double renorm_k;
+  uint32_t clamp;
+  uint32_t flags;
+  int32_t renorm_ok;
+};
+
+// S, r, scale of the emission in `slot` from the current reserved value.
+__device__ __forceinline__ void chain_draw(SState& s, int slot, const Chi2Consts& c, double sigma) {
+  const double S = c.disable ? s.sum_sq : chi2_draw(s.reserved_prev, c, s.clamp, s.flags);
+  const double r = s.sum_sq > 0.0 ? __dsqrt_rn(__ddiv_rn(S, s.sum_sq)) : 0.0;
+  s.S[slot] = S;
+  s.r[slot] = r;
+  s.scale[slot] = __dmul_rn(sigma, r);
+}
+// after a renormalization changed sum_sq: S is kept (disable_chi2 re-reads it)
+__device__ __forceinline__ void chain_rescale(SState& s, int slot, const Chi2Consts& c, double sigma) {
+  if (c.disable) s.S[slot] = s.sum_sq;
+  const double r = s.sum_sq > 0.0 ? __dsqrt_rn(__ddiv_rn(s.S[slot], s.sum_sq)) : 0.0;
+  s.r[slot] = r;
+  s.scale[slot] = __dmul_rn(sigma, r);
+}
+// bookkeeping at the end of emission `slot` (generator.cpp:373-375)
+__device__ __forceinline__ void chain_close(SState& s, int slot, double x_last) {
+  s.reserved_prev = __dmul_rn(x_last, s.r[slot]);
+  s.last_chi2 = s.S[slot];
+  s.last_r = s.r[slot];
+  s.last_scale = s.scale[slot];
+}
+
+// generator.cpp:20-34 recompute_sum_sq — sequential Neumaier, one thread.
+template <typename T>
+__device__ double neumaier_sq(const T* v, int n) {
+  double sum = 0.0, comp = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) {
+    const double x = static_cast<double>(v[i]);
+    const double term = __dmul_rn(x, x);
+    const double t = __dadd_rn(sum, term);
+    if (fabs(sum) >= fabs(term)) {
+      comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(sum, t), term));
+    } else {
+      comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(term, t), sum));
+    }
+    sum = t;
+  }
+  return __dadd_rn(sum, comp);
+}
+
+// generator.cpp:345-351 renormalize_.  Contains block barriers: call from
+// all threads.
+template <typename T, int N, int THREADS>
+__device__ void renormalize(T* cur, SState& s, int tid) {
+  if (tid == 0) {
+    const double ss = neumaier_sq(cur, N);
+    s.renorm_ok = ss > 0.0;
+    s.renorm_k = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
+  }
+  __syncthreads();
+  if (s.renorm_ok) {
+    const double k = s.renorm_k;
+    for (int i = tid; i < N; i += THREADS)
+      cur[i] = from_double<T>(__dmul_rn(static_cast<double>(cur[i]), k));
+    __syncthreads();
+    if (tid == 0) s.sum_sq = neumaier_sq(cur, N);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// fused consumer accumulators (config 5)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Consumer {
+  double s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+  uint32_t* hist;  // shared, 258 bins (under, 256, over)
+  __device__ __forceinline__ void add_group(const T* y, int n) {
+    T a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < n) {
+        const T x = y[k];
+        const T x2 = mul_rn(x, x);
+        a1 = add_rn(a1, x);
+        a2 = add_rn(a2, x2);
+        a3 = add_rn(a3, mul_rn(x2, x));
+        a4 = add_rn(a4, mul_rn(x2, x2));
+        const T t = mul_rn(add_rn(x, T(8)), T(16));
+        const int bin = t < T(0) ? -1 : (t >= T(256) ? 256 : static_cast<int>(t));
+        atomicAdd(&hist[bin + 1], 1u);
+      }
+    }
+    s1 += static_cast<double>(a1);
+    s2 += static_cast<double>(a2);
+    s3 += static_cast<double>(a3);
+    s4 += static_cast<double>(a4);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// the fast emission: values already in registers in pool order; 128-bit
+// aligned streaming stores, shifting by DELTA elements with warp shuffles
+// (the emission start e*(N-1) is misaligned in 3 of 4 emissions).
+//
+// Thread t owns blocks b_j = (warp*J + j)*32 + lane.  It stores the aligned
+// chunk of pool indices [4b+DELTA, 4b+DELTA+4): its own tail plus the first
+// DELTA values of block b+1 (lane+1, or lane 0 of group j+1 for lane 31).
+// The chunk that straddles two warps is written with scalar stores by both.
+// ---------------------------------------------------------------------------
+template <typename T, int J, int VEC, int DELTA>
+__device__ __forceinline__ void emit_store(T (&Y)[J][4], T* gbase, uint32_t limit, int lane,
+                                           int warp, int rows) {
+  static_assert(DELTA < VEC, "shift");
+  T nb[J][DELTA > 0 ? DELTA : 1];
+  if constexpr (DELTA > 0) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+#pragma unroll
+      for (int t = 0; t < DELTA; ++t) {
+        const T prov = (lane == 0 && j + 1 < J) ? Y[j + 1 < J ? j + 1 : j][t] : Y[j][t];
+        nb[j][t] = __shfl_sync(0xffffffffu, prov, (lane + 1) & 31);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int b = (warp * J + j) * 32 + lane;
+    if (b >= rows) continue;
+    const uint32_t i0 = 4u * b + DELTA;
+    const bool edge = DELTA > 0 && lane == 31 && j == J - 1;  // neighbour in next warp
+    T c[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int ni = DELTA + m - 4;  // index into the neighbour's head
+      c[m] = ni < 0 ? Y[j][ni < 0 ? DELTA + m : 0] : nb[j][ni < 0 ? 0 : ni];
+    }
+    if (!edge && i0 + 4 <= limit) {
+#pragma unroll
+      for (int v = 0; v < 4; v += VEC) stg_vec(gbase + i0 + v, c + v);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const bool own = DELTA + m < 4;
+        if (i0 + m < limit && (own || !edge)) stg1(gbase + i0 + m, c[m]);
+      }
+    }
+    if (DELTA > 0 && lane == 0 && j == 0) {
+      // head of the first block of this warp's range: the chunk it belongs to
+      // is owned by the previous warp's edge thread, which cannot see it
+#pragma unroll
+      for (int t = 0; t < DELTA; ++t)
+        if (4u * b + t < limit) stg1(gbase + 4 * b + t, Y[0][t]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pool_kernel: one CTA per pool.  Pool ping-pongs between two shared-memory
+// buffers; one block barrier per pass.
+//
+// One pass (generator.cpp:64-85): for b < ROWS, r = (off + b*STRIDE) mod ROWS,
+//   v_c = in[c*ROWS + r], a=v0+v1, bb=v0-v1, c=v2+v3, d=v2-v3,
+//   z = {a-d, bb+c, bb-c, -a-d}, out[4b+k] = (0.5*sign_k) * z[src_k].
+// The gather is bank-conflict-free: STRIDE is odd and ROWS a multiple of 32,
+// so 32 consecutive b hit 32 distinct banks; out[4b..4b+3] is one 128-bit
+// shared store.  The row permutation src is warp-uniform per pass and is
+// applied through a 24-way uniform branch over compile-time register moves.
+// ---------------------------------------------------------------------------
+template <typename T, int LOG2N>
+__global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS)
+    pool_kernel(const FillArgs a) {
+  using G = Geo<T, LOG2N>;
+  constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* buf0 = reinterpret_cast<T*>(smem);
+  T* buf1 = buf0 + N;
+  uint32_t* s_plans = reinterpret_cast<uint32_t*>(buf1 + N);
+  __shared__ SState s;
+  __shared__ uint32_t s_hist[258];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pool = blockIdx.x;
+  const bool mean_zero = a.mean_is_zero != 0;
+  const T mean_t = from_double<T>(a.mean);
+
+  // ---- prologue: state, pool, plans ----------------------------------------
+  if (tid == 0) {
+    const PoolState& st = a.st_in[pool];
+    s.reserved_prev = st.reserved_prev;
+    s.sum_sq = st.sum_sq;
+    s.cur_scale = st.scale;
+    s.last_chi2 = st.last_chi2;
+    s.last_r = st.r;
+    s.last_scale = st.scale;
+    s.clamp = 0;
+    s.flags = st.flags;
+    if (a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
+  }
+  if (a.mode == kModeConsume)
+    for (int i = tid; i < 258; i += THREADS) s_hist[i] = 0;
+  {
+    const float4* src = reinterpret_cast<const float4*>(static_cast<const T*>(a.pools_in) + pool * N);
+    float4* dst = reinterpret_cast<float4*>(buf0);
+    constexpr int NV = N * sizeof(T) / 16;
+    for (int i = tid; i < NV; i += THREADS) dst[i] = __ldcs(src + i);
+  }
+  for (uint32_t i = tid; i < a.n_passes; i += THREADS) s_plans[i] = a.plans[pool * a.plan_stride + i];
+  const uint64_t pass0 = a.st_in[pool].pass_count;
+  const uint32_t cursor0 = a.st_in[pool].cursor;
+  __syncthreads();
+
+  T* const out_pool = static_cast<T*>(a.out) + pool * a.out_stride + a.out_offset;
+  Consumer<T> cons;
+  cons.hist = s_hist;
+
+  // ---- drain the partially consumed emission --------------------------------
+  if (a.lead > 0) {
+    const T sc = from_double<T>(s.cur_scale);
+    const bool mat = (s.flags & kFlagLeftover) != 0;
+    const T* lo = static_cast<const T*>(a.leftover) + pool * (N - 1);
+    for (uint32_t i = tid; i < a.lead; i += THREADS) {
+      const uint32_t idx = cursor0 + i;
+      const T v = mat ? lo[idx] : emit_value(buf0[idx], sc, mean_t, mean_zero);
+      if (a.mode == kModeConsume) cons.add_group(&v, 1);
+      else stg1(out_pool + i, v);
+    }
+  }
+
+  // per-thread gather bases: rb_j = (b_j * STRIDE) mod ROWS
+  uint32_t rb[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t b = (warp * J + j) * 32 + lane;
+    rb[j] = (b * G::STRIDE) & G::MASK;
+  }
+
+  T* cur = buf0;
+  T* nxt = buf1;
+  for (uint32_t p = 0; p < a.n_passes; ++p) {
+    const uint32_t plan = s_plans[p];
+    const uint32_t off = plan & 0xffffu;
+    const uint32_t variant = plan >> 16;
+    const uint32_t perm = variant >> 4;
+    T hs[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+
+    // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
+    T z[J][4];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = (warp * J + j) * 32 + lane;
+      T v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+      if (ROWS >= 32 || b < ROWS) {
+        const uint32_t r = (rb[j] + off) & G::MASK;
+        v0 = cur[r];
+        v1 = cur[ROWS + r];
+        v2 = cur[2 * ROWS + r];
+        v3 = cur[3 * ROWS + r];
+      }
+      const T aa = add_rn(v0, v1);
+      const T bb = sub_rn(v0, v1);
+      const T cc = add_rn(v2, v3);
+      const T dd = sub_rn(v2, v3);
+      z[j][0] = sub_rn(aa, dd);
+      z[j][1] = add_rn(bb, cc);
+      z[j][2] = sub_rn(bb, cc);
+      z[j][3] = sub_rn(-aa, dd);
+    }
+    // signed row permutation: X[k] = (0.5*sign_k) * z[src_k]
+    T X[J][4];
+    switch (perm) {
+#define WB_PERM_CASE(P)                                                      \
+  case P:                                                                    \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {                          \
+      X[j][0] = mul_rn(hs[0], z[j][PermAt<P, 0>::v]);                            \
+      X[j][1] = mul_rn(hs[1], z[j][PermAt<P, 1>::v]);                            \
+      X[j][2] = mul_rn(hs[2], z[j][PermAt<P, 2>::v]);                            \
+      X[j][3] = mul_rn(hs[3], z[j][PermAt<P, 3>::v]);                            \
+    }                                                                        \
+    break;
+      WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
+      WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
+      WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
+      WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
+      WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22)
+      default: WB_PERM_CASE(23)
+#undef WB_PERM_CASE
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = (warp * J + j) * 32 + lane;
+      if (ROWS >= 32 || b < ROWS) sts4(nxt + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
+    }
+
+    const bool emit_pass = a.mode != kModePasses && (p + 1) % a.d == 0;
+    const uint32_t e = (p + 1) / a.d - 1;  // emission index when emit_pass
+    const bool renorm_now = ((pass0 + p + 1) & 255u) == 0;
+    const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
+    T* const gbase = out_pool + a.lead + uint64_t(e) * (N - 1);
+
+    if (emit_pass && !renorm_now) {
+      const int slot = e & 1;
+      const T sc = from_double<T>(s.scale[slot]);
+      T Y[J][4];
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) Y[j][k] = emit_value(X[j][k], sc, mean_t, mean_zero);
+      if (a.mode == kModeFill) {
+        const uint32_t delta =
+            (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
+            (G::VEC - 1);
+        if constexpr (G::VEC == 4) {
+          switch (delta) {
+            case 0: emit_store<T, J, 4, 0>(Y, gbase, limit, lane, warp, ROWS); break;
+            case 1: emit_store<T, J, 4, 1>(Y, gbase, limit, lane, warp, ROWS); break;
+            case 2: emit_store<T, J, 4, 2>(Y, gbase, limit, lane, warp, ROWS); break;
+            default: emit_store<T, J, 4, 3>(Y, gbase, limit, lane, warp, ROWS); break;
+          }
+        } else {
+          if (delta == 0) emit_store<T, J, 2, 0>(Y, gbase, limit, lane, warp, ROWS);
+          else emit_store<T, J, 2, 1>(Y, gbase, limit, lane, warp, ROWS);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const uint32_t b = (warp * J + j) * 32 + lane;
+          if (ROWS >= 32 || b < ROWS) {
+            const int n = (4 * b + 4 <= limit) ? 4 : (4 * b < limit ? int(limit - 4 * b) : 0);
+            if (n > 0) cons.add_group(Y[j], n);
+          }
+        }
+      }
+      if (tid == G::OWNER) {
+        chain_close(s, slot, static_cast<double>(X[J - 1][3]));
+        if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+      }
+    }
+    __syncthreads();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+
+    if (renorm_now) {
+      renormalize<T, N, THREADS>(cur, s, tid);
+      if (emit_pass) {
+        const int slot = e & 1;
+        if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
+        __syncthreads();
+        const T sc = from_double<T>(s.scale[slot]);
+        for (uint32_t i = tid; i < limit; i += THREADS) {
+          const T v = emit_value(cur[i], sc, mean_t, mean_zero);
+          if (a.mode == kModeConsume) cons.add_group(&v, 1);
+          else stg1(gbase + i, v);
+        }
+        if (tid == 0) {
+          chain_close(s, slot, static_cast<double>(cur[N - 1]));
+          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+        }
+        __syncthreads();
+      } else if (a.mode != kModePasses) {
+        const uint32_t en = (p + 1) / a.d;  // next emission
+        if (en < a.n_emit) {
+          if (tid == 0) chain_rescale(s, en & 1, a.chi2, a.sigma);
+          __syncthreads();
+        }
+      }
+    }
+  }
+
+  // ---- epilogue: pool and state back to HBM ---------------------------------
+  {
+    float4* dst = reinterpret_cast<float4*>(static_cast<T*>(a.pools_out) + pool * N);
+    const float4* src = reinterpret_cast<const float4*>(cur);
+    constexpr int NV = N * sizeof(T) / 16;
+    for (int i = tid; i < NV; i += THREADS) dst[i] = src[i];
+  }
+  if (a.mode == kModeConsume) {
+    // fixed-order block reduction of the moment sums
+    __shared__ double s_red[4][32];
+    double v[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] = __dadd_rn(v[k], __shfl_down_sync(0xffffffffu, v[k], o));
+    }
+    if (lane == 0)
+      for (int k = 0; k < 4; ++k) s_red[k][warp] = v[k];
+    __syncthreads();
+    if (tid < 4) {
+      double acc = 0.0;
+      for (int w = 0; w < G::NW; ++w) acc = __dadd_rn(acc, s_red[tid][w]);
+      a.part_sums[pool * 4 + tid] = acc;
+    }
+    for (int i = tid; i < 258; i += THREADS) a.part_hist[pool * 258 + i] = s_hist[i];
+  }
+  if (tid == 0) {
+    PoolState& so = a.st_out[pool];
+    so.reserved_prev = s.reserved_prev;
+    so.sum_sq = s.sum_sq;
+    so.pass_count = pass0 + a.n_passes;
+    so.clamp_count = a.st_in[pool].clamp_count + s.clamp;
+    uint32_t flags = s.flags;
+    so.scale = s.last_scale;
+    so.r = s.last_r;
+    so.last_chi2 = s.last_chi2;
+    if (a.n_emit > 0) {
+      so.cursor = a.last_limit;
+      flags &= ~kFlagLeftover;
+    } else {
+      so.cursor = cursor0 + a.lead;
+    }
+    so.flags = flags;
+    so.seed = a.st_in[pool].seed;
+    if (a.n_passes == 0 && &so != &a.st_in[pool]) {  // no plan launch copied the stream
+      for (int k = 0; k < 4; ++k) so.s[k] = a.st_in[pool].s[k];
+      so.draws = a.st_in[pool].draws;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan_kernel: one thread per pool walks its xoshiro256** stream two words
+// per pass (generator.cpp:335-339) and writes the decoded plans.  A warp
+// stages 32 pools x 32 passes in shared memory so the pool-major plan rows
+// are written with coalesced 128-byte stores.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+__global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
+  __shared__ uint32_t tile[4][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t pool = uint64_t(blockIdx.x) * 128 + threadIdx.x;
+  const uint64_t warp_pool0 = uint64_t(blockIdx.x) * 128 + w * 32;
+  const bool live = pool < a.n_pools;
+  uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  if (live) {
+    const PoolState& st = a.st_in[pool];
+    s0 = st.s[0];
+    s1 = st.s[1];
+    s2 = st.s[2];
+    s3 = st.s[3];
+  }
+  for (uint32_t base = 0; base < a.n_passes; base += 32) {
+    const uint32_t cnt = min(32u, a.n_passes - base);
+    for (uint32_t i = 0; i < cnt; ++i) {
+      uint64_t w2[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {  // baselines.cpp:33-45
+        w2[q] = rotl64(s1 * 5, 7) * 9;
+        const uint64_t t = s1 << 17;
+        s2 ^= s0;
+        s3 ^= s1;
+        s1 ^= s2;
+        s0 ^= s3;
+        s2 ^= t;
+        s3 = rotl64(s3, 45);
+      }
+      uint32_t variant = static_cast<uint32_t>(w2[0] % 384u);
+      uint32_t off = static_cast<uint32_t>(w2[1]) & a.rows_mask;
+      if (a.fixed_transform) variant = off = 0;  // PassPlan{} (generator.cpp:336-338)
+      tile[w][lane][i] = off | (variant << 16);
+    }
+    __syncwarp();
+    for (int q = 0; q < 32; ++q) {
+      const uint64_t pq = warp_pool0 + q;
+      if (pq < a.n_pools && uint32_t(lane) < cnt)
+        a.plans[pq * a.plan_stride + base + lane] = tile[w][q][lane];
+    }
+    __syncwarp();
+  }
+  if (live) {
+    PoolState& so = a.st_out[pool];
+    so.s[0] = s0;
+    so.s[1] = s1;
+    so.s[2] = s2;
+    so.s[3] = s3;
+    so.draws = a.st_in[pool].draws + 2ull * a.n_passes;
+  }
+}
+
+// Snapshot of the current emission before the pool is advanced outside
+// fill(): Generator::out_ keeps the old values until the next refill.
+template <typename T>
+__global__ void materialize_kernel(const T* pools, PoolState* st, T* leftover, uint64_t n_pools,
+                                   uint32_t N, double mean) {
+  const uint64_t pool = blockIdx.x;
+  if (pool >= n_pools) return;
+  const PoolState& ps = st[pool];
+  if (ps.cursor >= N - 1 || (ps.flags & kFlagLeftover)) return;
+  const T sc = from_double<T>(ps.scale);
+  const T mt = from_double<T>(mean);
+  const bool mz = mean == 0.0 && !signbit(mean);
+  for (uint32_t i = threadIdx.x; i < N - 1; i += blockDim.x)
+    leftover[pool * (N - 1) + i] = emit_value(pools[pool * N + i], sc, mt, mz);
+  __syncthreads();
+  if (threadIdx.x == 0) st[pool].flags |= kFlagLeftover;
+}
+
+// Fixed-order reduction of the consumer partials: block k sums pools
+// [k*chunk, (k+1)*chunk) in order; the host adds the block results in order.
+__global__ void reduce_consumer_kernel(const double* part_sums, const uint32_t* part_hist,
+                                       uint64_t n_pools, uint64_t chunk, double* blk_sums,
+                                       unsigned long long* blk_hist) {
+  const uint64_t k = blockIdx.x;
+  const uint64_t p0 = k * chunk, p1 = min(n_pools, p0 + chunk);
+  for (int i = threadIdx.x; i < 258 + 4; i += blockDim.x) {
+    if (i < 258) {
+      unsigned long long acc = 0;
+      for (uint64_t p = p0; p < p1; ++p) acc += part_hist[p * 258 + i];
+      blk_hist[k * 258 + i] = acc;
+    } else {
+      const int m = i - 258;
+      double acc = 0.0;
+      for (uint64_t p = p0; p < p1; ++p) acc = __dadd_rn(acc, part_sums[p * 4 + m]);
+      blk_sums[k * 4 + m] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Box-Muller comparator (baselines.cpp:68-92): one thread per stream, the
+// stream's words consumed exactly as boxmuller_next does (two per pair,
+// u1 == 0 -> 2^-53, second value cached), transcendental part in fp32.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+    boxmuller_kernel(const uint64_t* seeds, uint64_t seed_base, uint64_t n_streams,
+                     uint64_t count, double* part_sums, uint32_t* part_hist) {
+  __shared__ uint32_t hist[258];
+  __shared__ double red[4][4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 258; i += 128) hist[i] = 0;
+  __syncthreads();
+  Consumer<float> cons;
+  cons.hist = hist;
+  const uint64_t stream = uint64_t(blockIdx.x) * 128 + tid;
+  if (stream < n_streams) {
+    uint64_t sm = seeds ? seeds[stream] : seed_base + stream;
+    uint64_t s[4];
+    for (int k = 0; k < 4; ++k) {  // baselines.cpp:19-31
+      uint64_t z = (sm += 0x9e3779b97f4a7c15ULL);
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      s[k] = z ^ (z >> 31);
+    }
+    for (uint64_t i = 0; i < count; i += 2) {
+      double u[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint64_t w = rotl64(s[1] * 5, 7) * 9;
+        const uint64_t t = s[1] << 17;
+        s[2] ^= s[0];
+        s[3] ^= s[1];
+        s[1] ^= s[2];
+        s[0] ^= s[3];
+        s[2] ^= t;
+        s[3] = rotl64(s[3], 45);
+        u[q] = static_cast<double>(w >> 11) * 0x1.0p-53;
+      }
+      if (u[0] == 0.0) u[0] = 0x1.0p-53;
+      const float r = sqrtf(-2.0f * logf(static_cast<float>(u[0])));
+      float sn, cs;
+      sincospif(2.0f * static_cast<float>(u[1]), &sn, &cs);
+      const float z[2] = {r * cs, r * sn};
+      cons.add_group(z, (i + 1 < count) ? 2 : 1);
+    }
+  }
+  double v[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] = __dadd_rn(v[k], __shfl_down_sync(0xffffffffu, v[k], o));
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) red[k][warp] = v[k];
+  __syncthreads();
+  if (tid < 4) {
+    double acc = 0.0;
+    for (int w = 0; w < 4; ++w) acc = __dadd_rn(acc, red[tid][w]);
+    part_sums[blockIdx.x * 4 + tid] = acc;
+  }
+  for (int i = tid; i < 258; i += 128) part_hist[blockIdx.x * 258 + i] = hist[i];
+}
+
+// ---------------------------------------------------------------------------
+// host-callable launch table
+// ---------------------------------------------------------------------------
+template <typename T, int LOG2N>
+cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
+  using G = Geo<T, LOG2N>;
+  const size_t smem = 2 * size_t(G::N) * sizeof(T) + ((a.n_passes * 4 + 15) & ~size_t(15));
+  auto fn = pool_kernel<T, LOG2N>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<dim3(unsigned(n_pools)), dim3(G::THREADS), smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_pool_dispatch(int log2n, const FillArgs& a, uint64_t n_pools, cudaStream_t s) {
+  switch (log2n) {
+    case 5: return launch_pool<T, 5>(a, n_pools, s);
+    case 6: return launch_pool<T, 6>(a, n_pools, s);
+    case 7: return launch_pool<T, 7>(a, n_pools, s);
+    case 8: return launch_pool<T, 8>(a, n_pools, s);
+    case 9: return launch_pool<T, 9>(a, n_pools, s);
+    case 10: return launch_pool<T, 10>(a, n_pools, s);
+    case 11: return launch_pool<T, 11>(a, n_pools, s);
+    case 12: return launch_pool<T, 12>(a, n_pools, s);
+    case 13: return launch_pool<T, 13>(a, n_pools, s);
+    case 14:
+      if constexpr (sizeof(T) == 4) return launch_pool<T, 14>(a, n_pools, s);
+      else return cudaErrorInvalidValue;
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t n_pools,
+                               cudaStream_t s) {
+  return dtype == 0 ? launch_pool_dispatch<float>(log2n, a, n_pools, s)
+                    : launch_pool_dispatch<double>(log2n, a, n_pools, s);
+}
+
+int pool_kernel_threads(int dtype, int log2n) {
+#define WB_T(T)                                    \
+  switch (log2n) {                                 \
+    case 5: return Geo<T, 5>::THREADS;             \
+    case 6: return Geo<T, 6>::THREADS;             \
+    case 7: return Geo<T, 7>::THREADS;             \
+    case 8: return Geo<T, 8>::THREADS;             \
+    case 9: return Geo<T, 9>::THREADS;             \
+    case 10: return Geo<T, 10>::THREADS;           \
+    case 11: return Geo<T, 11>::THREADS;           \
+    case 12: return Geo<T, 12>::THREADS;           \
+    case 13: return Geo<T, 13>::THREADS;           \
+    case 14: return Geo<T, 14>::THREADS;           \
+    default: return 0;                             \
+  }
+  if (dtype == 0) { WB_T(float) } else { WB_T(double) }
+#undef WB_T
+}
+
+cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s) {
+  const unsigned blocks = unsigned((a.n_pools + 127) / 128);
+  plan_kernel<<<blocks, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void* leftover,
+                               uint64_t n_pools, uint32_t N, double mean, cudaStream_t s) {
+  if (dtype == 0)
+    materialize_kernel<float><<<unsigned(n_pools), 256, 0, s>>>(
+        static_cast<const float*>(pools), st, static_cast<float*>(leftover), n_pools, N, mean);
+  else
+    materialize_kernel<double><<<unsigned(n_pools), 256, 0, s>>>(
+        static_cast<const double*>(pools), st, static_cast<double*>(leftover), n_pools, N, mean);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_boxmuller(const uint64_t* d_seeds, uint64_t seed_base, uint64_t n_streams,
+                             uint64_t count, double* part_sums, uint32_t* part_hist,
+                             uint64_t n_blocks, int threads, cudaStream_t s) {
+  (void)threads;
+  boxmuller_kernel<<<unsigned(n_blocks), 128, 0, s>>>(d_seeds, seed_base, n_streams, count,
+                                                     part_sums, part_hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_consumer(const double* part_sums, const uint32_t* part_hist,
+                                   uint64_t n_pools, uint64_t chunk, double* blk_sums,
+                                   unsigned long long* blk_hist, cudaStream_t s) {
+  const unsigned blocks = unsigned((n_pools + chunk - 1) / chunk);
+  reduce_consumer_kernel<<<blocks, 288, 0, s>>>(part_sums, part_hist, n_pools, chunk, blk_sums,
+                                                blk_hist);
+  return cudaGetLastError();
+}
+
+}  // namespace wb

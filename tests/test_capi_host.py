@@ -1,0 +1,102 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it loads, exports
+every symbol include/wallace_b200.h declares, validates configs like
+GeneratorConfig::validate (generator.cpp:221-236), and seeds pools exactly
+like the reference constructor (generator.cpp:309-327)."""
+import ctypes as C
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1005_2314_b200 as pb
+from paper_1005_2314_b200 import _capi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _capi.load()
+    header = open(os.path.join(ROOT, "include", "wallace_b200.h")).read()
+    declared = set(re.findall(r"\b(wallace_[a-z_0-9]+)\s*\(", header))
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(L, name), name
+    bound = {n for n, _, _ in _capi.SYMBOLS}
+    assert declared == bound
+
+
+@pytest.mark.parametrize("field,kw", [
+    ("pool_size", dict(pool_size=48)),
+    ("pool_size", dict(pool_size=16)),
+    ("discard_every", dict(discard_every=0)),
+    ("out_sigma", dict(out_sigma=0.0)),
+    ("out_mean", dict(out_mean=float("inf"))),
+])
+def test_config_validation_names_field(field, kw):
+    # test_generator.cpp:42-72
+    with pytest.raises(pb.ConfigError, match=field):
+        pb.GeneratorConfig(**kw).validate()
+
+
+def test_valid_config_passes():
+    pb.GeneratorConfig().validate()
+
+
+def test_default_stride_and_plan_decode_vs_reference(ref):
+    L = _capi.load()
+    R = ref.ref_lib()
+    for rows in [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 1 << 20]:
+        assert L.wallace_default_stride(rows) == R.ref_default_stride(rows)
+    rng = np.random.default_rng(0)
+    for n in (32, 1024, 4096, 16384):
+        for _ in range(200):
+            w0, w1 = (int(x) for x in rng.integers(0, 2**64, size=2, dtype=np.uint64))
+            o1, o2 = C.c_uint64(), C.c_uint64()
+            v1 = L.wallace_decode_pass_plan(n, w0, w1, C.byref(o1))
+            v2 = R.ref_decode_pass_plan(n, w0, w1, C.byref(o2))
+            assert (v1, o1.value) == (v2, o2.value)
+
+
+def _neumaier(v):
+    s = c = 0.0
+    for x in v:
+        t2 = x * x
+        t = s + t2
+        c += (s - t) + t2 if abs(s) >= abs(t2) else (t2 - t) + s
+        s = t
+    return s + c
+
+
+@pytest.mark.parametrize("n,seed", [(32, 3), (1024, 1), (4096, 1), (2048, 7)])
+def test_host_seeding_matches_reference_polar(ref, n, seed):
+    """generator.cpp:317-327 restated: Polar values from the reference library,
+    Neumaier and the k-scaling in Python doubles; the library must agree bit for bit."""
+    L = _capi.load()
+    R = ref.ref_lib()
+    pol = np.empty(n + 1)
+    R.ref_polar(seed, n + 1, pol.ctypes.data_as(C.POINTER(C.c_double)))
+    ss = _neumaier(pol[:n].tolist())
+    k = math.sqrt(n / ss)
+    want = np.array([x * k for x in pol[:n]])
+    cfg = pb.GeneratorConfig(pool_size=n, seed=seed)
+    raw = np.empty(n)
+    res, sq = C.c_double(), C.c_double()
+    s4 = (C.c_uint64 * 4)()
+    dr = C.c_uint64()
+    assert L.wallace_host_seed_pool(C.byref(cfg.to_c()), seed,
+                                    raw.ctypes.data_as(C.POINTER(C.c_double)), C.byref(res),
+                                    C.byref(sq), s4, C.byref(dr)) == 0
+    assert np.array_equal(raw.view(np.uint64), want.view(np.uint64))
+    assert res.value == pol[n]
+    assert sq.value == _neumaier(want.tolist())
+    # 16 warm-up passes take 32 words: draws after construction
+    g = ref.RefGen(ref.Cfg(pool_size=n, seed=seed))
+    assert dr.value + 32 == g.stats()["uniform_draws"]
+
+
+def test_unsupported_options_are_explicit():
+    for kw in (dict(transform_family=1), dict(mixing=1)):
+        cfg = pb.GeneratorConfig(**kw)
+        cfg.validate()  # valid in the reference

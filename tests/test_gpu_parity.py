@@ -1,0 +1,259 @@
+"""GPU parity: the sm_100a path (libwallace_b200.so, called through the C-ABI)
+against the pinned CPU oracle on the same seeds and parameters.
+
+f64: bit-exact vs the oracle's reference semantics (== the reference library,
+     tests/test_oracle_pin.py).
+f32: bit-exact vs the oracle's fp32 restatement.
+The cases replay the reference's hot-path tests (test_generator.cpp) on the
+device; the multi-pool cases check every pool slice of a batch.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1005_2314_b200 as pb
+from oracle.oracle import Cfg, OracleGen
+
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("oracle_built")]
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+
+
+def gcfg(**kw):
+    return pb.GeneratorConfig(**kw)
+
+
+def ocfg(**kw):
+    return Cfg(**kw)
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def assert_same(got, want, what=""):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.dtype == want.dtype and got.shape == want.shape, what
+    if not np.array_equal(bits(got), bits(want)):
+        bad = np.nonzero(bits(got) != bits(want))[0]
+        raise AssertionError(f"{what}: {bad.size} mismatches, first at {bad[:8]}: "
+                             f"got {got[bad[:4]]} want {want[bad[:4]]}")
+
+
+CONFIGS = [
+    dict(pool_size=32, discard_every=1),
+    dict(pool_size=64, discard_every=2, chi2_method=0),
+    dict(pool_size=128, discard_every=3, chi2_method=1),
+    dict(pool_size=256, discard_every=1, out_mean=5.0, out_sigma=2.0),
+    dict(pool_size=512, discard_every=2, disable_chi2=True),
+    dict(pool_size=1024, discard_every=1),
+    dict(pool_size=2048, discard_every=3),
+    dict(pool_size=4096, discard_every=2, disable_chi2=True),
+    dict(pool_size=4096, discard_every=2),
+    dict(pool_size=8192, discard_every=1, out_mean=-0.5, out_sigma=0.75),
+    dict(pool_size=16384, discard_every=1),
+    dict(pool_size=128, fixed_transform=True),
+]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kw", CONFIGS, ids=lambda k: "_".join(f"{a}{b}" for a, b in k.items()))
+def test_fill_matches_oracle(cuda, dtype, kw):
+    if dtype == "f64" and kw["pool_size"] > 8192:
+        pytest.skip("f64 on-chip limit")
+    n = kw["pool_size"]
+    seeds = [11, 12, 1013]
+    count = 3 * n + 5  # several emissions, misaligned pool-major stride
+    b = pb.PoolBatch(gcfg(**kw), n_pools=len(seeds), seeds=seeds, dtype=dtype)
+    out = b.fill(count).cpu().numpy()
+    for p, s in enumerate(seeds):
+        want = OracleGen(ocfg(seed=s, **kw), dtype).fill(count)
+        assert_same(out[p], want, f"pool {p} seed {s}")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_chunked_fill_and_api_sequence(cuda, dtype):
+    """fill(5), fill(5), ... carry the partial emission across calls
+    (generator.cpp:387-399); step_pass / next_pool / inject_pool interleave
+    (generator.cpp:333-343, 401-413)."""
+    kw = dict(pool_size=64, discard_every=2, out_mean=5.0, out_sigma=2.0)
+    seeds = [21, 22]
+    b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=seeds, dtype=dtype)
+    o = [OracleGen(ocfg(seed=s, **kw), dtype) for s in seeds]
+    for k in (5, 5, 200, 63, 1, 126, 127):
+        got = b.fill(k).cpu().numpy()
+        for p in range(2):
+            assert_same(got[p], o[p].fill(k), f"fill {k} pool {p}")
+    b.step_pass()
+    for g in o:
+        g.step_pass()
+    got = b.fill(70).cpu().numpy()  # drains the old emission first
+    for p in range(2):
+        assert_same(got[p], o[p].fill(70), "after step_pass")
+    vals, res, chi = b.next_pool()
+    vals = vals.cpu().numpy()
+    for p in range(2):
+        v, r, c = o[p].next_pool()
+        assert_same(vals[p], v, "next_pool values")
+        assert res[p] == r and chi[p] == c
+    inj = np.linspace(-2, 2, 64)
+    b.inject_pool(inj, pool=1)
+    o[1].inject_pool(inj)
+    got = b.fill(300).cpu().numpy()
+    for p in range(2):
+        assert_same(got[p], o[p].fill(300), f"after inject pool {p}")
+    for p in range(2):
+        assert_same(b.pool(p), o[p].pool(), "pool()")
+        info, st = b.info(p), o[p].stats()
+        for k in ("pass_count", "uniform_draws", "chi2_clamp_count", "sum_sq", "reserved_prev"):
+            assert info[k] == st[k], k
+        assert info["buffered"] == st["buffered"]
+
+
+def test_renormalisation_crossings(cuda):
+    """Config-1 shape: 1024 values per pass, renormalised every 256 passes
+    (generator.cpp:342, 345-351); 2^18 values cross the boundary once per
+    256 emissions."""
+    kw = dict(pool_size=1024, discard_every=1)
+    for dtype in ("f64", "f32"):
+        b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=[1, 2], dtype=dtype)
+        out = b.fill(1 << 18).cpu().numpy()
+        for p, s in enumerate([1, 2]):
+            g = OracleGen(ocfg(seed=s, **kw), dtype)
+            assert_same(out[p], g.fill(1 << 18), f"{dtype} seed {s}")
+            assert b.info(p)["sum_sq"] == g.stats()["sum_sq"]
+
+
+def test_renorm_on_emission_pass_and_midgroup(cuda):
+    """d=3 puts the 256-pass renormalisation both on and between emission
+    passes; disable_chi2 re-reads sum_sq after it."""
+    for kw in (dict(pool_size=128, discard_every=3), dict(pool_size=128, discard_every=3, disable_chi2=True),
+               dict(pool_size=64, discard_every=5, chi2_method=0)):
+        for dtype in ("f64", "f32"):
+            b = pb.PoolBatch(gcfg(**kw), n_pools=1, seeds=[9], dtype=dtype)
+            want = OracleGen(ocfg(seed=9, **kw), dtype).fill(40000)
+            assert_same(b.fill(40000).cpu().numpy()[0], want, f"{kw} {dtype}")
+
+
+def test_zero_pool_stays_zero(cuda):
+    """test_generator.cpp:93-101 on the device."""
+    b = pb.PoolBatch(gcfg(pool_size=64, seed=3), n_pools=1, dtype="f64")
+    b.inject_pool(np.zeros(64))
+    b.step_pass()
+    assert np.all(b.pool(0) == 0.0)
+
+
+def test_disable_chi2_scale_is_exactly_one(cuda):
+    """test_generator.cpp:218-231: values == raw, reserved == raw[n-1]."""
+    b = pb.PoolBatch(gcfg(pool_size=128, seed=5, disable_chi2=True), n_pools=1, dtype="f64")
+    vals, res, chi = b.next_pool()
+    raw = b.pool(0)
+    assert np.array_equal(vals.cpu().numpy()[0], raw[:127])
+    assert res[0] == raw[127]
+    assert chi[0] == b.info(0)["sum_sq"]
+
+
+def test_emission_scales_to_chi2_draw(cuda):
+    """test_generator.cpp:246-260: sum emitted^2 + reserved^2 == S."""
+    b = pb.PoolBatch(gcfg(pool_size=1024, seed=31), n_pools=4, dtype="f64")
+    for _ in range(50):
+        vals, res, chi = b.next_pool()
+        v = vals.cpu().numpy()
+        for p in range(4):
+            total = float(np.sum(v[p] ** 2)) + res[p] ** 2
+            assert abs(total - chi[p]) <= 1e-9 * 1024
+
+
+def test_mean_sigma_exact_affine(cuda):
+    """test_generator.cpp:233-244: sigma=2, mean=5 gives exactly 2x+5."""
+    a = pb.PoolBatch(gcfg(pool_size=256, seed=99), n_pools=2, dtype="f64").fill(10000).cpu().numpy()
+    b = pb.PoolBatch(gcfg(pool_size=256, seed=99, out_mean=5.0, out_sigma=2.0), n_pools=2,
+                     dtype="f64").fill(10000).cpu().numpy()
+    assert np.array_equal(2.0 * a + 5.0, b)
+
+
+def test_discard_policy_pass_counts(cuda):
+    """test_generator.cpp:312-335: pass_count == 16 + 3(i+1)."""
+    b = pb.PoolBatch(gcfg(pool_size=64, seed=9, discard_every=3), n_pools=1, dtype="f64")
+    assert b.pass_count() == 16
+    prev = b.uniform_draws()
+    for i in range(10):
+        b.next_pool()
+        assert b.pass_count() == 16 + 3 * (i + 1)
+        assert b.uniform_draws() - prev == 6  # >= 1 draw per pool (test_generator.cpp:337-351)
+        prev = b.uniform_draws()
+
+
+def test_fill_zero_raises(cuda):
+    b = pb.PoolBatch(gcfg(pool_size=64, seed=21), n_pools=1)
+    with pytest.raises(pb.InvalidParameterError):
+        b.fill(0)
+    with pytest.raises(pb.InvalidParameterError):
+        b.inject_pool(np.ones(63))
+
+
+def test_golden_fixtures_on_device(cuda):
+    """Every golden case (reference outputs, tests/golden/golden.json)
+    reproduced by the device path: f64 == reference, f32 == restatement."""
+    for case in GOLDEN["cases"]:
+        kw = dict(case["cfg"])
+        seed = kw.pop("seed")
+        for dtype in ("f64", "f32"):
+            b = pb.PoolBatch(gcfg(**kw), n_pools=1, seeds=[seed], dtype=dtype)
+            v = b.fill(case["count"]).cpu().numpy()[0]
+            h = hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest()
+            assert h == case[f"{dtype}_sha256"], (case["name"], dtype)
+
+
+def test_snapshot_replay_is_identical(cuda):
+    torch = cuda
+    b = pb.PoolBatch(gcfg(pool_size=4096, discard_every=2, disable_chi2=True), n_pools=64,
+                     seeds=list(range(1, 65)), dtype="f32")
+    b.snapshot()
+    o1 = torch.empty((64, 1 << 16), dtype=torch.float32, device="cuda")
+    o2 = torch.empty_like(o1)
+    b.fill_from_snapshot_into(o1)
+    b.fill_from_snapshot_into(o2)
+    assert torch.equal(o1, o2)
+    want = OracleGen(ocfg(pool_size=4096, discard_every=2, disable_chi2=True, seed=7), "f32").fill(1 << 16)
+    assert_same(o1[6].cpu().numpy(), want, "pool 6 after replay")
+
+
+def test_save_load_state_resumes(cuda):
+    kw = dict(pool_size=256, discard_every=2)
+    b = pb.PoolBatch(gcfg(**kw), n_pools=3, seeds=[1, 2, 3], dtype="f32")
+    b.fill(1001)
+    img = b.save_state()
+    x1 = b.fill(5000).cpu().numpy()
+    b.load_state(img)
+    x2 = b.fill(5000).cpu().numpy()
+    assert np.array_equal(x1, x2)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_consumer_matches_oracle(cuda, dtype):
+    """Config-5 consumer on a reduced batch: histogram exact, moment sums to
+    reduction rounding."""
+    from oracle.oracle import consume_pools
+    kw = dict(pool_size=1024, discard_every=1)
+    seeds = np.arange(1, 65, dtype=np.uint64)
+    count = 1 << 14
+    b = pb.PoolBatch(gcfg(**kw), n_pools=64, seeds=seeds, dtype=dtype)
+    sums, hist = b.consume(count)
+    osums, ohist = consume_pools(ocfg(**kw), dtype, seeds, count)
+    assert np.array_equal(hist, ohist)
+    assert int(hist.sum()) == 64 * count
+    np.testing.assert_allclose(sums, osums, rtol=1e-9, atol=1e-6)
+
+
+def test_boxmuller_comparator_statistics(cuda):
+    sums, hist = pb.boxmuller_consume(n_streams=256, count=1 << 14, seed_base=1)
+    n = 256 * (1 << 14)
+    assert int(hist.sum()) == n
+    rep = pb.moment_reports(sums, n)
+    assert all(r[4] for r in rep.values()), rep
