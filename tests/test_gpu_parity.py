@@ -248,7 +248,13 @@ def test_consumer_matches_oracle(cuda, dtype):
     osums, ohist = consume_pools(ocfg(**kw), dtype, seeds, count)
     assert np.array_equal(hist, ohist)
     assert int(hist.sum()) == 64 * count
-    np.testing.assert_allclose(sums, osums, rtol=1e-9, atol=1e-6)
+    # sums: per-element powers are formed in the handle's dtype (fp32 for
+    # f32), then accumulated in fp64; tolerance = that rounding, relative to
+    # the sum of |x|^k (E|x|^k = 0.80, 1, 1.60, 3 for N(0,1))
+    n = 64 * count
+    eps = 1e-6 if dtype == "f32" else 1e-12
+    tol = eps * n * np.array([0.80, 1.0, 1.60, 3.0])
+    assert np.all(np.abs(sums - osums) <= tol), (sums, osums)
 
 
 def test_boxmuller_comparator_statistics(cuda):
