@@ -199,7 +199,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.pools:
+        cfg["pools"] = args.pools
     n_pools, count, dtype = cfg["pools"], cfg["count"], cfg["dtype"]
     esize = 4 if dtype == "f32" else 8
     seeds = np.arange(1 + rank * n_pools, 1 + (rank + 1) * n_pools, dtype=np.uint64)
@@ -329,6 +331,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--pools", type=int, default=0, help="override pools per GPU (profiling only)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
