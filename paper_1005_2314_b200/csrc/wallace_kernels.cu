@@ -70,6 +70,11 @@ struct Geo {
   static constexpr int VEC = 16 / sizeof(T);  // elements per 128-bit store
   // the thread holding pool element N-1 (block ROWS-1, slot 3), group J-1
   static constexpr int OWNER = (NW - 1) * 32 + ((ROWS - 1) & 31);
+  // resident CTAs per SM we ask ptxas to fit in registers (smem allows ~6
+  // pools of 32 KiB ping-pong per SM for N=4096 fp32)
+  static constexpr int SMEM_PER_CTA = 2 * N * sizeof(T) + 2048;
+  static constexpr int MINB_RAW = (220 * 1024) / SMEM_PER_CTA;
+  static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW * THREADS > 2048 ? 2048 / THREADS : MINB_RAW);
 };
 
 // ---------------------------------------------------------------------------
@@ -250,65 +255,86 @@ struct Consumer {
 };
 
 // ---------------------------------------------------------------------------
-// the fast emission: values already in registers in pool order; 128-bit
-// aligned streaming stores, shifting by DELTA elements with warp shuffles
-// (the emission start e*(N-1) is misaligned in 3 of 4 emissions).
+// The fast emission (full emissions: all N-1 values): values are in
+// registers in pool order; 128-bit aligned streaming stores, shifted by DELTA
+// elements with warp shuffles (the emission start e*(N-1) is misaligned in
+// 3 of 4 emissions).
 //
-// Thread t owns blocks b_j = (warp*J + j)*32 + lane.  It stores the aligned
-// chunk of pool indices [4b+DELTA, 4b+DELTA+4): its own tail plus the first
-// DELTA values of block b+1 (lane+1, or lane 0 of group j+1 for lane 31).
-// The chunk that straddles two warps is written with scalar stores by both.
+// Thread t owns blocks b_j = (warp*J + j)*32 + lane.  The aligned chunk
+// [4b+DELTA, 4b+DELTA+4) holds b's tail and the first DELTA values of block
+// b+1, which lives in lane+1 — or, for lane 31, in lane 0 of group j+1.  So
+// lanes 0..30 store their group-j chunk as soon as group j is shuffled, and
+// lane 31 stores its group-(j-1) chunk when group j's shuffle delivers lane
+// 0's head.  Lane 31's last group and lane 0's first head straddle two warps
+// and use scalar stores.  Element N-1 is never emitted (generator.cpp:366).
 // ---------------------------------------------------------------------------
-template <typename T, int J, int VEC, int DELTA>
-__device__ __forceinline__ void emit_store(T (&Y)[J][4], T* gbase, uint32_t limit, int lane,
-                                           int warp, int rows) {
+template <typename T, int LOG2N, int DELTA, bool MZ>
+__device__ __forceinline__ void emit_full(const T (&X)[Geo<T, LOG2N>::J][4], T* gbase, T sc,
+                                          T mean, int lane, int warp) {
+  using G = Geo<T, LOG2N>;
+  constexpr int J = G::J, VEC = G::VEC;
   static_assert(DELTA < VEC, "shift");
-  T nb[J][DELTA > 0 ? DELTA : 1];
-  if constexpr (DELTA > 0) {
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-#pragma unroll
-      for (int t = 0; t < DELTA; ++t) {
-        const T prov = (lane == 0 && j + 1 < J) ? Y[j + 1 < J ? j + 1 : j][t] : Y[j][t];
-        nb[j][t] = __shfl_sync(0xffffffffu, prov, (lane + 1) & 31);
-      }
-    }
-  }
+  const bool l31 = lane == 31;
+  T prev[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const int b = (warp * J + j) * 32 + lane;
-    if (b >= rows) continue;
-    const uint32_t i0 = 4u * b + DELTA;
-    const bool edge = DELTA > 0 && lane == 31 && j == J - 1;  // neighbour in next warp
-    T c[4];
+    const uint32_t b = (warp * J + j) * 32 + lane;
+    T y[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int ni = DELTA + m - 4;  // index into the neighbour's head
-      c[m] = ni < 0 ? Y[j][ni < 0 ? DELTA + m : 0] : nb[j][ni < 0 ? 0 : ni];
-    }
-    if (!edge && i0 + 4 <= limit) {
+    for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[j][k], sc, T(0)) : add_rn(mul_rn(X[j][k], sc), mean);
+    if constexpr (DELTA == 0) {
+      if (b != G::ROWS - 1) {
 #pragma unroll
-      for (int v = 0; v < 4; v += VEC) stg_vec(gbase + i0 + v, c + v);
+        for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * b + v, y + v);
+      } else {
+        stg1(gbase + 4 * b + 0, y[0]);
+        stg1(gbase + 4 * b + 1, y[1]);
+        stg1(gbase + 4 * b + 2, y[2]);
+      }
     } else {
+      T sh[DELTA];
+#pragma unroll
+      for (int t = 0; t < DELTA; ++t) sh[t] = __shfl_sync(0xffffffffu, y[t], (lane + 1) & 31);
+      T c[4];
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const bool own = DELTA + m < 4;
-        if (i0 + m < limit && (own || !edge)) stg1(gbase + i0 + m, c[m]);
+        if (DELTA + m < 4) c[m] = l31 ? prev[(DELTA + m) & 3] : y[(DELTA + m) & 3];
+        else c[m] = sh[(DELTA + m - 4) & (DELTA > 0 ? 3 : 0)];
       }
-    }
-    if (DELTA > 0 && lane == 0 && j == 0) {
-      // head of the first block of this warp's range: the chunk it belongs to
-      // is owned by the previous warp's edge thread, which cannot see it
+      const uint32_t cb = l31 ? b - 32 : b;  // lane 31 completes its previous group
+      if (!(l31 && j == 0)) {
 #pragma unroll
-      for (int t = 0; t < DELTA; ++t)
-        if (4u * b + t < limit) stg1(gbase + 4 * b + t, Y[0][t]);
+        for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * cb + DELTA + v, c + v);
+      }
+      if (j == 0 && lane == 0) {  // head of this warp's first block
+#pragma unroll
+        for (int t = 0; t < DELTA; ++t) stg1(gbase + 4 * b + t, y[t]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) prev[k] = y[k];
+    }
+  }
+  if constexpr (DELTA > 0) {
+    if (l31) {  // last group of the warp: own tail only, the head is the next warp's
+      const uint32_t b = (warp * J + J - 1) * 32 + 31;
+#pragma unroll
+      for (int m = DELTA; m < 4; ++m)
+        if (4 * b + m < uint32_t(G::N - 1)) stg1(gbase + 4 * b + m, prev[m]);
     }
   }
 }
 
+template <typename T, int LOG2N, int DELTA>
+__device__ __forceinline__ void emit_full_mz(bool mz, const T (&X)[Geo<T, LOG2N>::J][4], T* gbase,
+                                             T sc, T mean, int lane, int warp) {
+  if (mz) emit_full<T, LOG2N, DELTA, true>(X, gbase, sc, mean, lane, warp);
+  else emit_full<T, LOG2N, DELTA, false>(X, gbase, sc, mean, lane, warp);
+}
+
 // ---------------------------------------------------------------------------
-// pool_kernel: one CTA per pool.  Pool ping-pongs between two shared-memory
-// buffers; one block barrier per pass.
+// pool_kernel: one CTA per pool.  The pool ping-pongs between two shared
+// buffers (one block barrier per pass); plans for the launch are staged in
+// shared memory; pool state persists in HBM across launches.
 //
 // One pass (generator.cpp:64-85): for b < ROWS, r = (off + b*STRIDE) mod ROWS,
 //   v_c = in[c*ROWS + r], a=v0+v1, bb=v0-v1, c=v2+v3, d=v2-v3,
@@ -317,16 +343,92 @@ __device__ __forceinline__ void emit_store(T (&Y)[J][4], T* gbase, uint32_t limi
 // so 32 consecutive b hit 32 distinct banks; out[4b..4b+3] is one 128-bit
 // shared store.  The row permutation src is warp-uniform per pass and is
 // applied through a 24-way uniform branch over compile-time register moves.
+// Shared addresses are byte offsets: gather = ((rb4 + off4) & MASK4) | cur,
+// one IADD3 + one LOP3 per 4-block (the buffers sit at power-of-two offsets).
 // ---------------------------------------------------------------------------
 template <typename T, int LOG2N>
-__global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS)
+struct Smem {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr uint32_t BUF = N * sizeof(T);  // bytes per pool buffer (power of two)
+};
+
+template <typename T, int LOG2N>
+__device__ __forceinline__ void run_pass(const T* pools, uint32_t cur_off, uint32_t nxt_off,
+                                         uint32_t plan, const uint32_t (&rb4)[Geo<T, LOG2N>::J],
+                                         int lane, int warp, T (&X)[Geo<T, LOG2N>::J][4]) {
+  using G = Geo<T, LOG2N>;
+  constexpr int J = G::J, ROWS = G::ROWS;
+  constexpr uint32_t MASK4 = (ROWS - 1) * sizeof(T);
+  const char* base = reinterpret_cast<const char*>(pools);
+  const uint32_t off4 = (plan & 0xffffu) * sizeof(T);
+  const uint32_t variant = plan >> 16;
+  const uint32_t perm = variant >> 4;
+  T hs[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+
+  // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
+  T z[J][4];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t b = (warp * J + j) * 32 + lane;
+    T v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    if (ROWS >= 32 || b < ROWS) {
+      const T* row = reinterpret_cast<const T*>(base + (((rb4[j] + off4) & MASK4) | cur_off));
+      v0 = row[0];
+      v1 = row[ROWS];
+      v2 = row[2 * ROWS];
+      v3 = row[3 * ROWS];
+    }
+    const T aa = add_rn(v0, v1);
+    const T bb = sub_rn(v0, v1);
+    const T cc = add_rn(v2, v3);
+    const T dd = sub_rn(v2, v3);
+    z[j][0] = sub_rn(aa, dd);
+    z[j][1] = add_rn(bb, cc);
+    z[j][2] = sub_rn(bb, cc);
+    z[j][3] = sub_rn(-aa, dd);
+  }
+  // signed row permutation: X[k] = (0.5*sign_k) * z[src_k]
+  switch (perm) {
+#define WB_PERM_CASE(P)                                     \
+  case P:                                                   \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {         \
+      X[j][0] = mul_rn(hs[0], z[j][PermAt<P, 0>::v]);       \
+      X[j][1] = mul_rn(hs[1], z[j][PermAt<P, 1>::v]);       \
+      X[j][2] = mul_rn(hs[2], z[j][PermAt<P, 2>::v]);       \
+      X[j][3] = mul_rn(hs[3], z[j][PermAt<P, 3>::v]);       \
+    }                                                       \
+    break;
+    WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
+    WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
+    WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
+    WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
+    WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22)
+    default: WB_PERM_CASE(23)
+#undef WB_PERM_CASE
+  }
+  char* nb = const_cast<char*>(base) + nxt_off;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t b = (warp * J + j) * 32 + lane;
+    if (ROWS >= 32 || b < ROWS)
+      sts4(reinterpret_cast<T*>(nb) + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
+  }
+}
+
+template <typename T, int LOG2N>
+__global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     pool_kernel(const FillArgs a) {
   using G = Geo<T, LOG2N>;
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* buf0 = reinterpret_cast<T*>(smem);
-  T* buf1 = buf0 + N;
-  uint32_t* s_plans = reinterpret_cast<uint32_t*>(buf1 + N);
+  constexpr uint32_t BUF = Smem<T, LOG2N>::BUF;
+  constexpr bool FAST = ROWS >= 32;
+  // pools at the start of dynamic shared memory: buffer 0 at 0, buffer 1 at
+  // BUF (a power of two above every gather offset), plans after them
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* const pools = reinterpret_cast<T*>(smem);
+  uint32_t* s_plans = reinterpret_cast<uint32_t*>(smem + 2 * BUF);
   __shared__ SState s;
   __shared__ uint32_t s_hist[258];
 
@@ -352,7 +454,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS)
     for (int i = tid; i < 258; i += THREADS) s_hist[i] = 0;
   {
     const float4* src = reinterpret_cast<const float4*>(static_cast<const T*>(a.pools_in) + pool * N);
-    float4* dst = reinterpret_cast<float4*>(buf0);
+    float4* dst = reinterpret_cast<float4*>(pools);
     constexpr int NV = N * sizeof(T) / 16;
     for (int i = tid; i < NV; i += THREADS) dst[i] = __ldcs(src + i);
   }
@@ -372,116 +474,59 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS)
     const T* lo = static_cast<const T*>(a.leftover) + pool * (N - 1);
     for (uint32_t i = tid; i < a.lead; i += THREADS) {
       const uint32_t idx = cursor0 + i;
-      const T v = mat ? lo[idx] : emit_value(buf0[idx], sc, mean_t, mean_zero);
+      const T v = mat ? lo[idx] : emit_value(pools[idx], sc, mean_t, mean_zero);
       if (a.mode == kModeConsume) cons.add_group(&v, 1);
       else stg1(out_pool + i, v);
     }
   }
 
-  // per-thread gather bases: rb_j = (b_j * STRIDE) mod ROWS
-  uint32_t rb[J];
+  // per-thread gather bases (bytes): rb4_j = ((b_j * STRIDE) mod ROWS) * sizeof(T)
+  uint32_t rb4[J];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const uint32_t b = (warp * J + j) * 32 + lane;
-    rb[j] = (b * G::STRIDE) & G::MASK;
+    rb4[j] = ((b * G::STRIDE) & G::MASK) * sizeof(T);
   }
 
-  T* cur = buf0;
-  T* nxt = buf1;
+  uint32_t cur_off = 0;
   for (uint32_t p = 0; p < a.n_passes; ++p) {
-    const uint32_t plan = s_plans[p];
-    const uint32_t off = plan & 0xffffu;
-    const uint32_t variant = plan >> 16;
-    const uint32_t perm = variant >> 4;
-    T hs[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
-
-    // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
-    T z[J][4];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const uint32_t b = (warp * J + j) * 32 + lane;
-      T v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-      if (ROWS >= 32 || b < ROWS) {
-        const uint32_t r = (rb[j] + off) & G::MASK;
-        v0 = cur[r];
-        v1 = cur[ROWS + r];
-        v2 = cur[2 * ROWS + r];
-        v3 = cur[3 * ROWS + r];
-      }
-      const T aa = add_rn(v0, v1);
-      const T bb = sub_rn(v0, v1);
-      const T cc = add_rn(v2, v3);
-      const T dd = sub_rn(v2, v3);
-      z[j][0] = sub_rn(aa, dd);
-      z[j][1] = add_rn(bb, cc);
-      z[j][2] = sub_rn(bb, cc);
-      z[j][3] = sub_rn(-aa, dd);
-    }
-    // signed row permutation: X[k] = (0.5*sign_k) * z[src_k]
+    const uint32_t nxt_off = cur_off ^ BUF;
     T X[J][4];
-    switch (perm) {
-#define WB_PERM_CASE(P)                                                      \
-  case P:                                                                    \
-    _Pragma("unroll") for (int j = 0; j < J; ++j) {                          \
-      X[j][0] = mul_rn(hs[0], z[j][PermAt<P, 0>::v]);                            \
-      X[j][1] = mul_rn(hs[1], z[j][PermAt<P, 1>::v]);                            \
-      X[j][2] = mul_rn(hs[2], z[j][PermAt<P, 2>::v]);                            \
-      X[j][3] = mul_rn(hs[3], z[j][PermAt<P, 3>::v]);                            \
-    }                                                                        \
-    break;
-      WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
-      WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
-      WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
-      WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
-      WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22)
-      default: WB_PERM_CASE(23)
-#undef WB_PERM_CASE
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const uint32_t b = (warp * J + j) * 32 + lane;
-      if (ROWS >= 32 || b < ROWS) sts4(nxt + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
-    }
+    run_pass<T, LOG2N>(pools, cur_off, nxt_off, s_plans[p], rb4, lane, warp, X);
 
     const bool emit_pass = a.mode != kModePasses && (p + 1) % a.d == 0;
     const uint32_t e = (p + 1) / a.d - 1;  // emission index when emit_pass
     const bool renorm_now = ((pass0 + p + 1) & 255u) == 0;
     const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
     T* const gbase = out_pool + a.lead + uint64_t(e) * (N - 1);
+    const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
 
-    if (emit_pass && !renorm_now) {
+    if (fast) {
       const int slot = e & 1;
       const T sc = from_double<T>(s.scale[slot]);
-      T Y[J][4];
-#pragma unroll
-      for (int j = 0; j < J; ++j)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) Y[j][k] = emit_value(X[j][k], sc, mean_t, mean_zero);
       if (a.mode == kModeFill) {
         const uint32_t delta =
             (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
             (G::VEC - 1);
         if constexpr (G::VEC == 4) {
           switch (delta) {
-            case 0: emit_store<T, J, 4, 0>(Y, gbase, limit, lane, warp, ROWS); break;
-            case 1: emit_store<T, J, 4, 1>(Y, gbase, limit, lane, warp, ROWS); break;
-            case 2: emit_store<T, J, 4, 2>(Y, gbase, limit, lane, warp, ROWS); break;
-            default: emit_store<T, J, 4, 3>(Y, gbase, limit, lane, warp, ROWS); break;
+            case 0: emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+            case 1: emit_full_mz<T, LOG2N, 1 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+            case 2: emit_full_mz<T, LOG2N, 2 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+            default: emit_full_mz<T, LOG2N, 3 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
           }
         } else {
-          if (delta == 0) emit_store<T, J, 2, 0>(Y, gbase, limit, lane, warp, ROWS);
-          else emit_store<T, J, 2, 1>(Y, gbase, limit, lane, warp, ROWS);
+          if (delta == 0) emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp);
+          else emit_full_mz<T, LOG2N, 1>(mean_zero, X, gbase, sc, mean_t, lane, warp);
         }
       } else {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
           const uint32_t b = (warp * J + j) * 32 + lane;
-          if (ROWS >= 32 || b < ROWS) {
-            const int n = (4 * b + 4 <= limit) ? 4 : (4 * b < limit ? int(limit - 4 * b) : 0);
-            if (n > 0) cons.add_group(Y[j], n);
-          }
+          T y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean_t, mean_zero);
+          cons.add_group(y, b == ROWS - 1 ? 3 : 4);
         }
       }
       if (tid == G::OWNER) {
@@ -490,36 +535,39 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS)
       }
     }
     __syncthreads();
-    T* t = cur;
-    cur = nxt;
-    nxt = t;
+    cur_off = nxt_off;
+    T* const cur = reinterpret_cast<T*>(smem + cur_off);
 
-    if (renorm_now) {
-      renormalize<T, N, THREADS>(cur, s, tid);
-      if (emit_pass) {
-        const int slot = e & 1;
+    if (renorm_now) renormalize<T, N, THREADS>(cur, s, tid);
+    if (emit_pass && !fast) {
+      // slow emission from shared memory: partial emissions, emissions right
+      // after a renormalisation (generator.cpp:342 precedes refill_'s S/r),
+      // and pools smaller than one warp of 4-blocks
+      const int slot = e & 1;
+      if (renorm_now) {
         if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
         __syncthreads();
-        const T sc = from_double<T>(s.scale[slot]);
-        for (uint32_t i = tid; i < limit; i += THREADS) {
-          const T v = emit_value(cur[i], sc, mean_t, mean_zero);
-          if (a.mode == kModeConsume) cons.add_group(&v, 1);
-          else stg1(gbase + i, v);
-        }
-        if (tid == 0) {
-          chain_close(s, slot, static_cast<double>(cur[N - 1]));
-          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
-        }
+      }
+      const T sc = from_double<T>(s.scale[slot]);
+      for (uint32_t i = tid; i < limit; i += THREADS) {
+        const T v = emit_value(cur[i], sc, mean_t, mean_zero);
+        if (a.mode == kModeConsume) cons.add_group(&v, 1);
+        else stg1(gbase + i, v);
+      }
+      if (tid == 0) {
+        chain_close(s, slot, static_cast<double>(cur[N - 1]));
+        if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+      }
+      __syncthreads();
+    } else if (renorm_now && a.mode != kModePasses) {
+      const uint32_t en = (p + 1) / a.d;  // next emission
+      if (en < a.n_emit) {
+        if (tid == 0) chain_rescale(s, en & 1, a.chi2, a.sigma);
         __syncthreads();
-      } else if (a.mode != kModePasses) {
-        const uint32_t en = (p + 1) / a.d;  // next emission
-        if (en < a.n_emit) {
-          if (tid == 0) chain_rescale(s, en & 1, a.chi2, a.sigma);
-          __syncthreads();
-        }
       }
     }
   }
+  T* const cur = reinterpret_cast<T*>(smem + cur_off);
 
   // ---- epilogue: pool and state back to HBM ---------------------------------
   {
@@ -742,6 +790,13 @@ cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream
   using G = Geo<T, LOG2N>;
   const size_t smem = 2 * size_t(G::N) * sizeof(T) + ((a.n_passes * 4 + 15) & ~size_t(15));
   auto fn = pool_kernel<T, LOG2N>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
