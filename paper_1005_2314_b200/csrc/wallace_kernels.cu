@@ -350,31 +350,37 @@ template <typename T, int LOG2N>
 struct Smem {
   static constexpr int N = 1 << LOG2N;
   static constexpr uint32_t BUF = N * sizeof(T);  // bytes per pool buffer (power of two)
+  // pools in static shared memory when they fit the 48 KiB static limit: the
+  // buffer base then folds into the LDS/STS immediate offsets
+  static constexpr bool STATIC = 2 * BUF <= 40 * 1024;
 };
 
+// One pass over the pool in shared memory (generator.cpp:64-85); leaves the
+// signed, permuted outputs of this thread's 4-blocks in X and stores them to
+// the next buffer.  sb = b0*STRIDE + off for this thread's first block.
 template <typename T, int LOG2N>
-__device__ __forceinline__ void run_pass(const T* pools, uint32_t cur_off, uint32_t nxt_off,
-                                         uint32_t plan, const uint32_t (&rb4)[Geo<T, LOG2N>::J],
-                                         int lane, int warp, T (&X)[Geo<T, LOG2N>::J][4]) {
+__device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
+                                         uint32_t plan, uint32_t b0, T (&X)[Geo<T, LOG2N>::J][4]) {
   using G = Geo<T, LOG2N>;
   constexpr int J = G::J, ROWS = G::ROWS;
   constexpr uint32_t MASK4 = (ROWS - 1) * sizeof(T);
-  const char* base = reinterpret_cast<const char*>(pools);
-  const uint32_t off4 = (plan & 0xffffu) * sizeof(T);
+  const uint32_t off = plan & 0xffffu;
   const uint32_t variant = plan >> 16;
   const uint32_t perm = variant >> 4;
   T hs[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+  // byte offset of row r_j = (off + b_j*STRIDE) mod ROWS, b_j = b0 + 32j
+  const uint32_t r0 = (b0 * G::STRIDE + off) * sizeof(T);
 
   // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
   T z[J][4];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const uint32_t b = (warp * J + j) * 32 + lane;
     T v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-    if (ROWS >= 32 || b < ROWS) {
-      const T* row = reinterpret_cast<const T*>(base + (((rb4[j] + off4) & MASK4) | cur_off));
+    if (ROWS >= 32 || b0 + 32 * j < ROWS) {
+      constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
+      const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) | cur_off));
       v0 = row[0];
       v1 = row[ROWS];
       v2 = row[2 * ROWS];
@@ -408,31 +414,50 @@ __device__ __forceinline__ void run_pass(const T* pools, uint32_t cur_off, uint3
     default: WB_PERM_CASE(23)
 #undef WB_PERM_CASE
   }
-  char* nb = const_cast<char*>(base) + nxt_off;
+  T* nb = reinterpret_cast<T*>(const_cast<char*>(base) + nxt_off);
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const uint32_t b = (warp * J + j) * 32 + lane;
-    if (ROWS >= 32 || b < ROWS)
-      sts4(reinterpret_cast<T*>(nb) + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
+    const uint32_t b = b0 + 32 * j;
+    if (ROWS >= 32 || b < ROWS) sts4(nb + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
   }
 }
 
+// Emission of the values already in registers (fast path) into the fused
+// consumer instead of memory.
 template <typename T, int LOG2N>
+__device__ __forceinline__ void consume_full(const T (&X)[Geo<T, LOG2N>::J][4], Consumer<T>& cons,
+                                             T sc, T mean, bool mz, uint32_t b0) {
+  using G = Geo<T, LOG2N>;
+#pragma unroll
+  for (int j = 0; j < G::J; ++j) {
+    const uint32_t b = b0 + 32 * j;
+    T y[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean, mz);
+    cons.add_group(y, b == G::ROWS - 1 ? 3 : 4);
+  }
+}
+
+template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     pool_kernel(const FillArgs a) {
   using G = Geo<T, LOG2N>;
+  using SM = Smem<T, LOG2N>;
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
-  constexpr uint32_t BUF = Smem<T, LOG2N>::BUF;
+  constexpr uint32_t BUF = SM::BUF;
   constexpr bool FAST = ROWS >= 32;
-  // pools at the start of dynamic shared memory: buffer 0 at 0, buffer 1 at
-  // BUF (a power of two above every gather offset), plans after them
-  extern __shared__ __align__(1024) unsigned char smem[];
-  T* const pools = reinterpret_cast<T*>(smem);
-  uint32_t* s_plans = reinterpret_cast<uint32_t*>(smem + 2 * BUF);
+  // buffer 0 at offset 0, buffer 1 at BUF (a power of two above every gather
+  // offset, so `| cur_off` selects the buffer); plans in dynamic smem
+  __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? 2 * BUF : 16];
+  extern __shared__ __align__(1024) unsigned char dsmem[];
+  unsigned char* const pbase = SM::STATIC ? s_pool : dsmem;
+  T* const pools = reinterpret_cast<T*>(pbase);
+  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : 2 * BUF));
   __shared__ SState s;
-  __shared__ uint32_t s_hist[258];
+  __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t b0 = warp * J * 32 + lane;  // first 4-block of this thread
   const uint64_t pool = blockIdx.x;
   const bool mean_zero = a.mean_is_zero != 0;
   const T mean_t = from_double<T>(a.mean);
@@ -448,9 +473,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     s.last_scale = st.scale;
     s.clamp = 0;
     s.flags = st.flags;
-    if (a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
+    if (MODE != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
   }
-  if (a.mode == kModeConsume)
+  if constexpr (MODE == kModeConsume)
     for (int i = tid; i < 258; i += THREADS) s_hist[i] = 0;
   {
     const float4* src = reinterpret_cast<const float4*>(static_cast<const T*>(a.pools_in) + pool * N);
@@ -468,106 +493,96 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   cons.hist = s_hist;
 
   // ---- drain the partially consumed emission --------------------------------
-  if (a.lead > 0) {
+  if (MODE != kModePasses && a.lead > 0) {
     const T sc = from_double<T>(s.cur_scale);
     const bool mat = (s.flags & kFlagLeftover) != 0;
     const T* lo = static_cast<const T*>(a.leftover) + pool * (N - 1);
     for (uint32_t i = tid; i < a.lead; i += THREADS) {
       const uint32_t idx = cursor0 + i;
       const T v = mat ? lo[idx] : emit_value(pools[idx], sc, mean_t, mean_zero);
-      if (a.mode == kModeConsume) cons.add_group(&v, 1);
+      if constexpr (MODE == kModeConsume) cons.add_group(&v, 1);
       else stg1(out_pool + i, v);
     }
   }
 
-  // per-thread gather bases (bytes): rb4_j = ((b_j * STRIDE) mod ROWS) * sizeof(T)
-  uint32_t rb4[J];
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const uint32_t b = (warp * J + j) * 32 + lane;
-    rb4[j] = ((b * G::STRIDE) & G::MASK) * sizeof(T);
-  }
-
+  const char* const cbase = reinterpret_cast<const char*>(pbase);
   uint32_t cur_off = 0;
-  for (uint32_t p = 0; p < a.n_passes; ++p) {
-    const uint32_t nxt_off = cur_off ^ BUF;
-    T X[J][4];
-    run_pass<T, LOG2N>(pools, cur_off, nxt_off, s_plans[p], rb4, lane, warp, X);
+  uint32_t pc = static_cast<uint32_t>(pass0 + 1) & 255u;  // pass count after the next pass, mod 256
+  uint32_t p = 0;                                          // plan index
 
-    const bool emit_pass = a.mode != kModePasses && (p + 1) % a.d == 0;
-    const uint32_t e = (p + 1) / a.d - 1;  // emission index when emit_pass
-    const bool renorm_now = ((pass0 + p + 1) & 255u) == 0;
-    const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
-    T* const gbase = out_pool + a.lead + uint64_t(e) * (N - 1);
-    const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
-
-    if (fast) {
-      const int slot = e & 1;
-      const T sc = from_double<T>(s.scale[slot]);
-      if (a.mode == kModeFill) {
-        const uint32_t delta =
-            (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
-            (G::VEC - 1);
-        if constexpr (G::VEC == 4) {
-          switch (delta) {
-            case 0: emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-            case 1: emit_full_mz<T, LOG2N, 1 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-            case 2: emit_full_mz<T, LOG2N, 2 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-            default: emit_full_mz<T, LOG2N, 3 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-          }
-        } else {
-          if (delta == 0) emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp);
-          else emit_full_mz<T, LOG2N, 1>(mean_zero, X, gbase, sc, mean_t, lane, warp);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const uint32_t b = (warp * J + j) * 32 + lane;
-          T y[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean_t, mean_zero);
-          cons.add_group(y, b == ROWS - 1 ? 3 : 4);
-        }
-      }
-      if (tid == G::OWNER) {
-        chain_close(s, slot, static_cast<double>(X[J - 1][3]));
-        if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
-      }
-    }
-    __syncthreads();
-    cur_off = nxt_off;
-    T* const cur = reinterpret_cast<T*>(smem + cur_off);
-
-    if (renorm_now) renormalize<T, N, THREADS>(cur, s, tid);
-    if (emit_pass && !fast) {
-      // slow emission from shared memory: partial emissions, emissions right
-      // after a renormalisation (generator.cpp:342 precedes refill_'s S/r),
-      // and pools smaller than one warp of 4-blocks
-      const int slot = e & 1;
-      if (renorm_now) {
-        if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
-        __syncthreads();
-      }
-      const T sc = from_double<T>(s.scale[slot]);
-      for (uint32_t i = tid; i < limit; i += THREADS) {
-        const T v = emit_value(cur[i], sc, mean_t, mean_zero);
-        if (a.mode == kModeConsume) cons.add_group(&v, 1);
-        else stg1(gbase + i, v);
-      }
-      if (tid == 0) {
-        chain_close(s, slot, static_cast<double>(cur[N - 1]));
-        if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
-      }
+  if constexpr (MODE == kModePasses) {
+    for (; p < a.n_passes; ++p) {
+      T X[J][4];
+      run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ BUF, s_plans[p], b0, X);
       __syncthreads();
-    } else if (renorm_now && a.mode != kModePasses) {
-      const uint32_t en = (p + 1) / a.d;  // next emission
-      if (en < a.n_emit) {
-        if (tid == 0) chain_rescale(s, en & 1, a.chi2, a.sigma);
+      cur_off ^= BUF;
+      if (pc == 0) renormalize<T, N, THREADS>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
+      pc = (pc + 1) & 255u;
+    }
+  } else {
+    T* gbase = out_pool + a.lead;  // element 0 of the current emission
+    for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
+      const int slot = e & 1;
+      const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
+      for (uint32_t q = 1; q <= a.d; ++q, ++p) {
+        T X[J][4];
+        run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ BUF, s_plans[p], b0, X);
+        const bool emit_pass = q == a.d;
+        const bool renorm_now = pc == 0;
+        const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
+        if (fast) {
+          const T sc = from_double<T>(s.scale[slot]);
+          if constexpr (MODE == kModeFill) {
+            const uint32_t delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) &
+                                                        (G::VEC - 1))) & (G::VEC - 1);
+            if constexpr (G::VEC == 4) {
+              switch (delta) {
+                case 0: emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+                case 1: emit_full_mz<T, LOG2N, 1 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+                case 2: emit_full_mz<T, LOG2N, 2 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+                default: emit_full_mz<T, LOG2N, 3 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+              }
+            } else {
+              if (delta == 0) emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp);
+              else emit_full_mz<T, LOG2N, 1>(mean_zero, X, gbase, sc, mean_t, lane, warp);
+            }
+          } else {
+            consume_full<T, LOG2N>(X, cons, sc, mean_t, mean_zero, b0);
+          }
+          if (tid == G::OWNER) {
+            chain_close(s, slot, static_cast<double>(X[J - 1][3]));
+            if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+          }
+        }
         __syncthreads();
+        cur_off ^= BUF;
+        T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+        if (renorm_now) {
+          renormalize<T, N, THREADS>(cur, s, tid);
+          // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
+          if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
+          __syncthreads();
+        }
+        if (emit_pass && !fast) {
+          // slow emission from shared memory: the partial last emission, an
+          // emission right after a renormalisation, pools below 128 values
+          const T sc = from_double<T>(s.scale[slot]);
+          for (uint32_t i = tid; i < limit; i += THREADS) {
+            const T v = emit_value(cur[i], sc, mean_t, mean_zero);
+            if constexpr (MODE == kModeConsume) cons.add_group(&v, 1);
+            else stg1(gbase + i, v);
+          }
+          if (tid == 0) {
+            chain_close(s, slot, static_cast<double>(cur[N - 1]));
+            if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+          }
+          __syncthreads();
+        }
+        pc = (pc + 1) & 255u;
       }
     }
   }
-  T* const cur = reinterpret_cast<T*>(smem + cur_off);
+  T* const cur = reinterpret_cast<T*>(pbase + cur_off);
 
   // ---- epilogue: pool and state back to HBM ---------------------------------
   {
@@ -576,7 +591,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     constexpr int NV = N * sizeof(T) / 16;
     for (int i = tid; i < NV; i += THREADS) dst[i] = src[i];
   }
-  if (a.mode == kModeConsume) {
+  if constexpr (MODE == kModeConsume) {
     // fixed-order block reduction of the moment sums
     __shared__ double s_red[4][32];
     double v[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
@@ -605,11 +620,11 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     so.scale = s.last_scale;
     so.r = s.last_r;
     so.last_chi2 = s.last_chi2;
-    if (a.n_emit > 0) {
+    if (MODE != kModePasses && a.n_emit > 0) {
       so.cursor = a.last_limit;
       flags &= ~kFlagLeftover;
     } else {
-      so.cursor = cursor0 + a.lead;
+      so.cursor = cursor0 + (MODE != kModePasses ? a.lead : 0);
     }
     so.flags = flags;
     so.seed = a.st_in[pool].seed;
@@ -785,24 +800,33 @@ __global__ void __launch_bounds__(128)
 // ---------------------------------------------------------------------------
 // host-callable launch table
 // ---------------------------------------------------------------------------
-template <typename T, int LOG2N>
-cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
-  using G = Geo<T, LOG2N>;
-  const size_t smem = 2 * size_t(G::N) * sizeof(T) + ((a.n_passes * 4 + 15) & ~size_t(15));
-  auto fn = pool_kernel<T, LOG2N>;
+template <typename T, int LOG2N, int MODE>
+cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
+  using SM = Smem<T, LOG2N>;
+  const size_t plans = (a.n_passes * 4 + 15) & ~size_t(15);
+  const size_t smem = (SM::STATIC ? 0 : 2 * size_t(SM::BUF)) + plans;
+  auto fn = pool_kernel<T, LOG2N, MODE>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(SM::STATIC ? 16 * 1024 : 2 * SM::BUF + 16 * 1024));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-  }
-  fn<<<dim3(unsigned(n_pools)), dim3(G::THREADS), smem, stream>>>(a);
+  fn<<<dim3(unsigned(n_pools)), dim3(Geo<T, LOG2N>::THREADS), smem, stream>>>(a);
   return cudaGetLastError();
+}
+
+template <typename T, int LOG2N>
+cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
+  switch (a.mode) {
+    case kModeFill: return launch_pool_mode<T, LOG2N, kModeFill>(a, n_pools, stream);
+    case kModePasses: return launch_pool_mode<T, LOG2N, kModePasses>(a, n_pools, stream);
+    default: return launch_pool_mode<T, LOG2N, kModeConsume>(a, n_pools, stream);
+  }
 }
 
 template <typename T>
