@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libwallace_b200.so")
+LIB_PATH = os.environ.get("WALLACE_B200_LIB") or os.path.join(PKG_DIR, "libwallace_b200.so")
 
 u64 = C.c_uint64
 i32 = C.c_int32

@@ -55,13 +55,39 @@ struct PermAt {
 };
 static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v == 0, "perm table");
 
+// Build-time knobs (defaults are the tuned choice; variants are built for
+// measurement by bench/tune scripts).
+#ifndef WB_INPLACE_F32
+#define WB_INPLACE_F32 0
+#endif
+#ifndef WB_INPLACE_F64
+#define WB_INPLACE_F64 0
+#endif
+#ifndef WB_REGS_INPLACE
+#define WB_REGS_INPLACE 56
+#endif
+// ABLATION builds only (timing experiments, wrong output): 1 = skip the
+// fast emission, 2 = skip its global stores, 3 = skip the scalar chain
+#ifndef WB_ABLATE
+#define WB_ABLATE 0
+#endif
+#ifndef WB_REGS_PP
+#define WB_REGS_PP 80
+#endif
+#ifndef WB_J_F32
+#define WB_J_F32 8
+#endif
+#ifndef WB_J_F64
+#define WB_J_F64 4
+#endif
+
 template <typename T, int LOG2N>
 struct Geo {
   static constexpr int N = 1 << LOG2N;
   static constexpr int ROWS = N / 4;
   // groups (4-blocks) per thread: enough independent gathers per thread to
   // hide LDS latency, few enough warps per pool for cheap barriers.
-  static constexpr int JWANT = sizeof(T) == 4 ? 8 : 4;
+  static constexpr int JWANT = sizeof(T) == 4 ? WB_J_F32 : WB_J_F64;
   static constexpr int J = (ROWS >= 32 * JWANT) ? JWANT : (ROWS >= 32 ? ROWS / 32 : 1);
   static constexpr int THREADS = (ROWS >= 32) ? ROWS / J : 32;
   static constexpr int NW = THREADS / 32;
@@ -70,11 +96,18 @@ struct Geo {
   static constexpr int VEC = 16 / sizeof(T);  // elements per 128-bit store
   // the thread holding pool element N-1 (block ROWS-1, slot 3), group J-1
   static constexpr int OWNER = (NW - 1) * 32 + ((ROWS - 1) & 31);
-  // resident CTAs per SM we ask ptxas to fit in registers (smem allows ~6
-  // pools of 32 KiB ping-pong per SM for N=4096 fp32)
-  static constexpr int SMEM_PER_CTA = 2 * N * sizeof(T) + 2048;
+  // in-place passes keep one pool buffer (two barriers per pass) and fit
+  // twice the pools per SM; ping-pong keeps two (one barrier per pass)
+  static constexpr bool INPLACE = sizeof(T) == 4 ? WB_INPLACE_F32 : WB_INPLACE_F64;
+  static constexpr int BUFS = INPLACE ? 1 : 2;
+  // resident CTAs per SM we ask ptxas to fit in registers: the smem limit
+  // (e.g. 6 ping-pong pools of N=4096 fp32) and a register budget
+  static constexpr int SMEM_PER_CTA = BUFS * N * sizeof(T) + 2048;
   static constexpr int MINB_RAW = (220 * 1024) / SMEM_PER_CTA;
-  static constexpr int MINB = MINB_RAW < 1 ? 1 : (MINB_RAW * THREADS > 2048 ? 2048 / THREADS : MINB_RAW);
+  static constexpr int MINB_SMEM = MINB_RAW < 1 ? 1 : (MINB_RAW * THREADS > 2048 ? 2048 / THREADS : MINB_RAW);
+  static constexpr int REG_BUDGET = INPLACE ? WB_REGS_INPLACE : WB_REGS_PP;
+  static constexpr int MINB_REGS = 65536 / (THREADS * REG_BUDGET) < 1 ? 1 : 65536 / (THREADS * REG_BUDGET);
+  static constexpr int MINB = MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS;
 };
 
 // ---------------------------------------------------------------------------
@@ -119,6 +152,9 @@ __device__ __forceinline__ void stg_vec(double* p, const double* v) {
 }
 template <typename T>
 __device__ __forceinline__ void stg1(T* p, T v) { __stcs(p, v); }
+#if WB_ABLATE == 2
+#define stg_vec(p, v) do { if (reinterpret_cast<uintptr_t>(p) == 1) stg_vec(p, v); } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // chi-squared draw and the per-emission scalar chain (chi2.cpp:27-59,
@@ -352,7 +388,8 @@ struct Smem {
   static constexpr uint32_t BUF = N * sizeof(T);  // bytes per pool buffer (power of two)
   // pools in static shared memory when they fit the 48 KiB static limit: the
   // buffer base then folds into the LDS/STS immediate offsets
-  static constexpr bool STATIC = 2 * BUF <= 40 * 1024;
+  static constexpr int BUFS = Geo<T, LOG2N>::BUFS;
+  static constexpr bool STATIC = BUFS * BUF <= 40 * 1024;
 };
 
 // One pass over the pool in shared memory (generator.cpp:64-85); leaves the
@@ -414,11 +451,31 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
     default: WB_PERM_CASE(23)
 #undef WB_PERM_CASE
   }
+  if constexpr (G::INPLACE) __syncthreads();  // every gather of this pass is done
   T* nb = reinterpret_cast<T*>(const_cast<char*>(base) + nxt_off);
+  if constexpr (sizeof(T) == 8) {
+    // a 4-double block is 32 bytes: two 128-bit stores at a 32-byte lane
+    // stride would hit each bank twice per 8-lane phase; lanes with bit 2 set
+    // store their halves in the opposite order, which makes both stores
+    // conflict-free (lanes l and l+4 then cover complementary banks)
+    const bool swz = (b0 >> 2) & 1;
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const uint32_t b = b0 + 32 * j;
-    if (ROWS >= 32 || b < ROWS) sts4(nb + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) {
+        double2* q = reinterpret_cast<double2*>(nb + 4 * b);
+        const double2 lo = make_double2(X[j][0], X[j][1]);
+        const double2 hi = make_double2(X[j][2], X[j][3]);
+        q[swz ? 1 : 0] = swz ? hi : lo;
+        q[swz ? 0 : 1] = swz ? lo : hi;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) sts4(nb + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
+    }
   }
 }
 
@@ -448,11 +505,12 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   constexpr bool FAST = ROWS >= 32;
   // buffer 0 at offset 0, buffer 1 at BUF (a power of two above every gather
   // offset, so `| cur_off` selects the buffer); plans in dynamic smem
-  __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? 2 * BUF : 16];
+  constexpr uint32_t FLIP = G::INPLACE ? 0u : BUF;  // cur_off ^ FLIP = next buffer
+  __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? SM::BUFS * BUF : 16];
   extern __shared__ __align__(1024) unsigned char dsmem[];
   unsigned char* const pbase = SM::STATIC ? s_pool : dsmem;
   T* const pools = reinterpret_cast<T*>(pbase);
-  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : 2 * BUF));
+  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::BUFS * BUF));
   __shared__ SState s;
   __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
 
@@ -513,9 +571,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   if constexpr (MODE == kModePasses) {
     for (; p < a.n_passes; ++p) {
       T X[J][4];
-      run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ BUF, s_plans[p], b0, X);
+      run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ FLIP, s_plans[p], b0, X);
       __syncthreads();
-      cur_off ^= BUF;
+      cur_off ^= FLIP;
       if (pc == 0) renormalize<T, N, THREADS>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
       pc = (pc + 1) & 255u;
     }
@@ -526,11 +584,11 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
       for (uint32_t q = 1; q <= a.d; ++q, ++p) {
         T X[J][4];
-        run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ BUF, s_plans[p], b0, X);
+        run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ FLIP, s_plans[p], b0, X);
         const bool emit_pass = q == a.d;
         const bool renorm_now = pc == 0;
         const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
-        if (fast) {
+        if (fast && WB_ABLATE != 1) {
           const T sc = from_double<T>(s.scale[slot]);
           if constexpr (MODE == kModeFill) {
             const uint32_t delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) &
@@ -549,13 +607,13 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           } else {
             consume_full<T, LOG2N>(X, cons, sc, mean_t, mean_zero, b0);
           }
-          if (tid == G::OWNER) {
+          if (tid == G::OWNER && WB_ABLATE != 3) {
             chain_close(s, slot, static_cast<double>(X[J - 1][3]));
             if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
           }
         }
         __syncthreads();
-        cur_off ^= BUF;
+        cur_off ^= FLIP;
         T* const cur = reinterpret_cast<T*>(pbase + cur_off);
         if (renorm_now) {
           renormalize<T, N, THREADS>(cur, s, tid);
@@ -804,7 +862,7 @@ template <typename T, int LOG2N, int MODE>
 cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
   using SM = Smem<T, LOG2N>;
   const size_t plans = (a.n_passes * 4 + 15) & ~size_t(15);
-  const size_t smem = (SM::STATIC ? 0 : 2 * size_t(SM::BUF)) + plans;
+  const size_t smem = (SM::STATIC ? 0 : SM::BUFS * size_t(SM::BUF)) + plans;
   auto fn = pool_kernel<T, LOG2N, MODE>;
   static bool configured = false;  // per instantiation
   if (!configured) {
@@ -812,7 +870,7 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
                                          cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(SM::STATIC ? 16 * 1024 : 2 * SM::BUF + 16 * 1024));
+                               int(SM::STATIC ? 16 * 1024 : SM::BUFS * SM::BUF + 16 * 1024));
     if (e != cudaSuccess) return e;
     configured = true;
   }
