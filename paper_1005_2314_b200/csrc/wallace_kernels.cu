@@ -71,6 +71,12 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_ABLATE
 #define WB_ABLATE 0
 #endif
+#ifndef WB_PREFETCH
+#define WB_PREFETCH 1
+#endif
+#ifndef WB_D2_STG64
+#define WB_D2_STG64 0
+#endif
 #ifndef WB_REGS_PP
 #define WB_REGS_PP 80
 #endif
@@ -78,7 +84,17 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #define WB_J_F32 8
 #endif
 #ifndef WB_J_F64
-#define WB_J_F64 4
+#define WB_J_F64 8
+#endif
+// 4-blocks per processing chunk (registers hold one chunk at a time)
+#ifndef WB_JC_F32
+#define WB_JC_F32 8
+#endif
+#ifndef WB_JC_F64
+#define WB_JC_F64 8
+#endif
+#ifndef WB_HS_LUT
+#define WB_HS_LUT 1
 #endif
 
 template <typename T, int LOG2N>
@@ -89,6 +105,9 @@ struct Geo {
   // hide LDS latency, few enough warps per pool for cheap barriers.
   static constexpr int JWANT = sizeof(T) == 4 ? WB_J_F32 : WB_J_F64;
   static constexpr int J = (ROWS >= 32 * JWANT) ? JWANT : (ROWS >= 32 ? ROWS / 32 : 1);
+  static constexpr int JCWANT = sizeof(T) == 4 ? WB_JC_F32 : WB_JC_F64;
+  static constexpr int JC = J < JCWANT ? J : JCWANT;
+  static_assert(J % JC == 0, "chunking");
   static constexpr int THREADS = (ROWS >= 32) ? ROWS / J : 32;
   static constexpr int NW = THREADS / 32;
   static constexpr uint32_t MASK = ROWS - 1;
@@ -305,20 +324,30 @@ struct Consumer {
 // and use scalar stores.  Element N-1 is never emitted (generator.cpp:366).
 // ---------------------------------------------------------------------------
 template <typename T, int LOG2N, int DELTA, bool MZ>
-__device__ __forceinline__ void emit_full(const T (&X)[Geo<T, LOG2N>::J][4], T* gbase, T sc,
-                                          T mean, int lane, int warp) {
+__device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], int c0, T (&prev)[4],
+                                           T* gbase, T sc, T mean, int lane, int warp) {
   using G = Geo<T, LOG2N>;
-  constexpr int J = G::J, VEC = G::VEC;
+  constexpr int J = G::J, JC = G::JC, VEC = G::VEC;
   static_assert(DELTA < VEC, "shift");
   const bool l31 = lane == 31;
-  T prev[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
+  for (int jj = 0; jj < JC; ++jj) {
+    const int j = c0 + jj;
     const uint32_t b = (warp * J + j) * 32 + lane;
     T y[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[j][k], sc, T(0)) : add_rn(mul_rn(X[j][k], sc), mean);
-    if constexpr (DELTA == 0) {
+    for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
+    if constexpr (WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
+      // global(4b) is 8-byte aligned: two float2 stores of the own block,
+      // no neighbour values needed
+      if (b != G::ROWS - 1) {
+        __stcs(reinterpret_cast<float2*>(gbase + 4 * b), make_float2(y[0], y[1]));
+        __stcs(reinterpret_cast<float2*>(gbase + 4 * b + 2), make_float2(y[2], y[3]));
+      } else {
+        __stcs(reinterpret_cast<float2*>(gbase + 4 * b), make_float2(y[0], y[1]));
+        stg1(gbase + 4 * b + 2, y[2]);
+      }
+    } else if constexpr (DELTA == 0) {
       if (b != G::ROWS - 1) {
 #pragma unroll
         for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * b + v, y + v);
@@ -350,8 +379,8 @@ __device__ __forceinline__ void emit_full(const T (&X)[Geo<T, LOG2N>::J][4], T* 
       for (int k = 0; k < 4; ++k) prev[k] = y[k];
     }
   }
-  if constexpr (DELTA > 0) {
-    if (l31) {  // last group of the warp: own tail only, the head is the next warp's
+  if constexpr (DELTA > 0 && !(WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2)) {
+    if (l31 && c0 + JC == J) {  // last group of the warp: own tail only, the head is the next warp's
       const uint32_t b = (warp * J + J - 1) * 32 + 31;
 #pragma unroll
       for (int m = DELTA; m < 4; ++m)
@@ -361,10 +390,10 @@ __device__ __forceinline__ void emit_full(const T (&X)[Geo<T, LOG2N>::J][4], T* 
 }
 
 template <typename T, int LOG2N, int DELTA>
-__device__ __forceinline__ void emit_full_mz(bool mz, const T (&X)[Geo<T, LOG2N>::J][4], T* gbase,
-                                             T sc, T mean, int lane, int warp) {
-  if (mz) emit_full<T, LOG2N, DELTA, true>(X, gbase, sc, mean, lane, warp);
-  else emit_full<T, LOG2N, DELTA, false>(X, gbase, sc, mean, lane, warp);
+__device__ __forceinline__ void emit_chunk_mz(bool mz, const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
+                                              T (&prev)[4], T* gbase, T sc, T mean, int lane, int warp) {
+  if (mz) emit_chunk<T, LOG2N, DELTA, true>(X, c0, prev, gbase, sc, mean, lane, warp);
+  else emit_chunk<T, LOG2N, DELTA, false>(X, c0, prev, gbase, sc, mean, lane, warp);
 }
 
 // ---------------------------------------------------------------------------
@@ -395,18 +424,28 @@ struct Smem {
 // One pass over the pool in shared memory (generator.cpp:64-85); leaves the
 // signed, permuted outputs of this thread's 4-blocks in X and stores them to
 // the next buffer.  sb = b0*STRIDE + off for this thread's first block.
-template <typename T, int LOG2N>
+template <typename T, int LOG2N, int J>
 __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
-                                         uint32_t plan, uint32_t b0, T (&X)[Geo<T, LOG2N>::J][4]) {
+                                         uint32_t plan, uint32_t b0, T (&X)[J][4],
+                                         const float* hs_lut) {
   using G = Geo<T, LOG2N>;
-  constexpr int J = G::J, ROWS = G::ROWS;
+  constexpr int ROWS = G::ROWS;
   constexpr uint32_t MASK4 = (ROWS - 1) * sizeof(T);
   const uint32_t off = plan & 0xffffu;
   const uint32_t variant = plan >> 16;
   const uint32_t perm = variant >> 4;
   T hs[4];
+  if constexpr (WB_HS_LUT && sizeof(T) == 4) {
+    // the four +-1/2 row factors of this variant's sign mask, one 128-bit load
+    const float4 h = reinterpret_cast<const float4*>(hs_lut)[variant & 15u];
+    hs[0] = h.x;
+    hs[1] = h.y;
+    hs[2] = h.z;
+    hs[3] = h.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+    for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+  }
   // byte offset of row r_j = (off + b_j*STRIDE) mod ROWS, b_j = b0 + 32j
   const uint32_t r0 = (b0 * G::STRIDE + off) * sizeof(T);
 
@@ -447,8 +486,8 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
     WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
     WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
     WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
-    WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22)
-    default: WB_PERM_CASE(23)
+    WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22) WB_PERM_CASE(23)
+    default: __builtin_unreachable();  // perm = variant >> 4 < 24 (variant = w0 % 384)
 #undef WB_PERM_CASE
   }
   if constexpr (G::INPLACE) __syncthreads();  // every gather of this pass is done
@@ -482,12 +521,12 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
 // Emission of the values already in registers (fast path) into the fused
 // consumer instead of memory.
 template <typename T, int LOG2N>
-__device__ __forceinline__ void consume_full(const T (&X)[Geo<T, LOG2N>::J][4], Consumer<T>& cons,
-                                             T sc, T mean, bool mz, uint32_t b0) {
+__device__ __forceinline__ void consume_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], Consumer<T>& cons,
+                                              T sc, T mean, bool mz, uint32_t b0c) {
   using G = Geo<T, LOG2N>;
 #pragma unroll
-  for (int j = 0; j < G::J; ++j) {
-    const uint32_t b = b0 + 32 * j;
+  for (int j = 0; j < G::JC; ++j) {
+    const uint32_t b = b0c + 32 * j;
     T y[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean, mz);
@@ -513,6 +552,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::BUFS * BUF));
   __shared__ SState s;
   __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
+  __shared__ __align__(16) float s_hs[64];  // sign mask -> (0.5*sign_k)_k (transforms.cpp:88)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t b0 = warp * J * 32 + lane;  // first 4-block of this thread
@@ -535,6 +575,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   }
   if constexpr (MODE == kModeConsume)
     for (int i = tid; i < 258; i += THREADS) s_hist[i] = 0;
+  for (int i = tid; i < 64; i += THREADS) s_hs[i] = ((i >> 2) >> (i & 3)) & 1 ? -0.5f : 0.5f;
   {
     const float4* src = reinterpret_cast<const float4*>(static_cast<const T*>(a.pools_in) + pool * N);
     float4* dst = reinterpret_cast<float4*>(pools);
@@ -570,47 +611,67 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
 
   if constexpr (MODE == kModePasses) {
     for (; p < a.n_passes; ++p) {
-      T X[J][4];
-      run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ FLIP, s_plans[p], b0, X);
+      const uint32_t plan_p = s_plans[p];
+      for (int c0 = 0; c0 < J; c0 += G::JC) {
+        T X[G::JC][4];
+        run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+      }
       __syncthreads();
       cur_off ^= FLIP;
       if (pc == 0) renormalize<T, N, THREADS>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
       pc = (pc + 1) & 255u;
     }
   } else {
+    uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
     T* gbase = out_pool + a.lead;  // element 0 of the current emission
     for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
       const int slot = e & 1;
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
       for (uint32_t q = 1; q <= a.d; ++q, ++p) {
-        T X[J][4];
-        run_pass<T, LOG2N>(cbase, cur_off, cur_off ^ FLIP, s_plans[p], b0, X);
         const bool emit_pass = q == a.d;
         const bool renorm_now = pc == 0;
         const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
-        if (fast && WB_ABLATE != 1) {
-          const T sc = from_double<T>(s.scale[slot]);
-          if constexpr (MODE == kModeFill) {
-            const uint32_t delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) &
-                                                        (G::VEC - 1))) & (G::VEC - 1);
-            if constexpr (G::VEC == 4) {
-              switch (delta) {
-                case 0: emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-                case 1: emit_full_mz<T, LOG2N, 1 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-                case 2: emit_full_mz<T, LOG2N, 2 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
-                default: emit_full_mz<T, LOG2N, 3 % G::VEC>(mean_zero, X, gbase, sc, mean_t, lane, warp); break;
+        // the emission scale is final before this pass (published behind at
+        // least one barrier); load it up front so its latency hides
+        const double scd = WB_PREFETCH ? s.scale[slot] : 0.0;
+        if (!WB_PREFETCH) plan = s_plans[p];
+        const uint32_t plan_p = plan;
+        if (WB_PREFETCH) plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
+        const bool do_emit = fast && WB_ABLATE != 1;
+        T sc = T(0);
+        uint32_t delta = 0;
+        if (do_emit) {
+          sc = from_double<T>(WB_PREFETCH ? scd : s.scale[slot]);
+          delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
+                  (G::VEC - 1);
+        }
+        T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
+        T x_last = T(0);
+        for (int c0 = 0; c0 < J; c0 += G::JC) {
+          T X[G::JC][4];
+          run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+          if (do_emit) {
+            if constexpr (MODE == kModeFill) {
+              if constexpr (G::VEC == 4) {
+                switch (delta) {
+                  case 0: emit_chunk_mz<T, LOG2N, 0>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
+                  case 1: emit_chunk_mz<T, LOG2N, 1 % G::VEC>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
+                  case 2: emit_chunk_mz<T, LOG2N, 2 % G::VEC>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
+                  default: emit_chunk_mz<T, LOG2N, 3 % G::VEC>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
+                }
+              } else {
+                if (delta == 0) emit_chunk_mz<T, LOG2N, 0>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
+                else emit_chunk_mz<T, LOG2N, 1>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
               }
             } else {
-              if (delta == 0) emit_full_mz<T, LOG2N, 0>(mean_zero, X, gbase, sc, mean_t, lane, warp);
-              else emit_full_mz<T, LOG2N, 1>(mean_zero, X, gbase, sc, mean_t, lane, warp);
+              consume_chunk<T, LOG2N>(X, cons, sc, mean_t, mean_zero, b0 + 32 * c0);
             }
-          } else {
-            consume_full<T, LOG2N>(X, cons, sc, mean_t, mean_zero, b0);
           }
-          if (tid == G::OWNER && WB_ABLATE != 3) {
-            chain_close(s, slot, static_cast<double>(X[J - 1][3]));
-            if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
-          }
+          x_last = X[G::JC - 1][3];
+        }
+        if (do_emit && tid == G::OWNER && WB_ABLATE != 3) {
+          chain_close(s, slot, static_cast<double>(x_last));
+          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
         }
         __syncthreads();
         cur_off ^= FLIP;
