@@ -109,6 +109,11 @@ wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t cou
 wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* reserved,
                                  double* chi2_draw);
 
+/* Same as wallace_next_pool but the values land in HOST memory
+ * (n_pools * (pool_size - 1) elements of the handle's dtype). */
+wallace_status wallace_next_pool_host(wallace_handle* h, void* host_values, double* reserved,
+                                      double* chi2_draw);
+
 /* Generator::step_pass() (generator.cpp:333-343), n_passes times. */
 wallace_status wallace_step_pass(wallace_handle* h, uint64_t n_passes);
 

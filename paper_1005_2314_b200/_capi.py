@@ -63,6 +63,7 @@ SYMBOLS = [
     ("wallace_fill", i32, [vp, vp, u64]),
     ("wallace_fill_host", i32, [vp, vp, u64]),
     ("wallace_next_pool", i32, [vp, vp, P(f64), P(f64)]),
+    ("wallace_next_pool_host", i32, [vp, vp, P(f64), P(f64)]),
     ("wallace_step_pass", i32, [vp, u64]),
     ("wallace_inject_pool", i32, [vp, u64, P(f64), u64]),
     ("wallace_get_pool", i32, [vp, u64, P(f64), u64]),

@@ -712,6 +712,26 @@ wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* re
   return st;
 }
 
+wallace_status wallace_next_pool_host(wallace_handle* h, void* host_values, double* reserved,
+                                      double* chi2_draw) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  const uint64_t bytes = h->n_pools * (h->N - 1) * h->esize;
+  if (h->stage_bytes < bytes) {
+    cudaFree(h->d_stage);
+    h->d_stage = nullptr;
+    h->stage_bytes = 0;
+    WB_CUDA(cudaMalloc(&h->d_stage, bytes));
+    h->stage_bytes = bytes;
+  }
+  wallace_status st = wallace_next_pool(h, h->d_stage, reserved, chi2_draw);
+  if (st) return st;
+  if (host_values) {
+    WB_CUDA(cudaMemcpyAsync(host_values, h->d_stage, bytes, cudaMemcpyDeviceToHost, h->stream));
+    WB_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return WALLACE_OK;
+}
+
 wallace_status wallace_step_pass(wallace_handle* h, uint64_t n_passes) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   wallace_status st = materialize(h);

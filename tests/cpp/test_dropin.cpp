@@ -1,0 +1,328 @@
+// Drop-in test: the reference's hot-path test cases
+// (/root/reference/proj/tests/test_generator.cpp) replayed against
+// wallace_b200::Generator (include/wallace_b200.hpp -> C-ABI -> sm_100a),
+// plus bit-for-bit stream comparison with the UNMODIFIED reference library
+// (oracle/_ref/libmaxent_ref.so, extern "C" shim in oracle/ref_shim.cpp).
+// Needs a GPU.  Exit code 0 = all checks passed.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "wallace_b200.hpp"
+
+// ---- the reference library, through the test shim (oracle/ref_shim.cpp) ----
+extern "C" {
+void* ref_create(uint64_t pool_size, int chi2_method, uint64_t discard_every, double mean,
+                 double sigma, uint64_t seed, int fixed, int disable_chi2);
+void ref_destroy(void* g);
+int ref_fill(void* g, double* out, uint64_t count);
+double ref_next_normal(void* g);
+int ref_next_pool(void* g, double* values, double* reserved, double* chi2);
+void ref_step_pass(void* g);
+int ref_inject_pool(void* g, const double* v, uint64_t n);
+void ref_get_pool(void* g, double* raw);
+void ref_get_stats(void* g, uint64_t* pass_count, uint64_t* draws, uint64_t* clamp,
+                   double* sum_sq, double* reserved_prev);
+double ref_chi2_sample(double x, uint64_t nu, int method, int* clamped);
+}
+
+namespace wb = wallace_b200;
+
+static int g_checks = 0, g_fail = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    ++g_checks;                                                              \
+    if (!(cond)) {                                                           \
+      ++g_fail;                                                              \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);   \
+    }                                                                        \
+  } while (0)
+#define CHECK_THROWS_AS(expr, type)                                          \
+  do {                                                                       \
+    bool caught_ = false;                                                    \
+    try {                                                                    \
+      (void)(expr);                                                          \
+    } catch (const type&) {                                                  \
+      caught_ = true;                                                        \
+    } catch (...) {                                                          \
+    }                                                                        \
+    CHECK(caught_ && #type);                                                 \
+  } while (0)
+#define CHECK_THROWS_WITH(expr, type, needle)                                \
+  do {                                                                       \
+    bool ok_ = false;                                                        \
+    try {                                                                    \
+      (void)(expr);                                                          \
+    } catch (const type& e_) {                                               \
+      ok_ = std::string(e_.what()).find(needle) != std::string::npos;        \
+    } catch (...) {                                                          \
+    }                                                                        \
+    CHECK(ok_ && needle);                                                    \
+  } while (0)
+
+struct Ref {
+  void* g;
+  explicit Ref(const wb::GeneratorConfig& c)
+      : g(ref_create(c.pool_size, static_cast<int>(c.chi2_method), c.discard_every, c.out_mean,
+                     c.out_sigma, c.seed, c.diag.fixed_transform, c.diag.disable_chi2)) {}
+  ~Ref() { ref_destroy(g); }
+  std::vector<double> fill(size_t n) {
+    std::vector<double> v(n);
+    ref_fill(g, v.data(), n);
+    return v;
+  }
+};
+
+static bool same_bits(const std::vector<double>& a, const std::vector<double>& b) {
+  return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * 8) == 0;
+}
+
+static double pool_sum_sq(const std::vector<double>& v) {
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return s;
+}
+
+static wb::GeneratorConfig cfg_of(size_t n, uint64_t seed) {
+  wb::GeneratorConfig c;
+  c.pool_size = n;
+  c.seed = seed;
+  return c;
+}
+
+int main() {
+  // test_generator.cpp:42-72 config validation names the offending field
+  {
+    wb::GeneratorConfig cfg;
+    cfg.pool_size = 48;
+    CHECK_THROWS_WITH(cfg.validate(), wb::ConfigError, "pool_size");
+    cfg.pool_size = 16;
+    CHECK_THROWS_AS(cfg.validate(), wb::ConfigError);
+    cfg.pool_size = 1024;
+    cfg.discard_every = 0;
+    CHECK_THROWS_WITH(cfg.validate(), wb::ConfigError, "discard_every");
+    cfg.discard_every = 1;
+    cfg.out_sigma = 0.0;
+    CHECK_THROWS_WITH(cfg.validate(), wb::ConfigError, "out_sigma");
+    cfg.out_sigma = 1.0;
+    cfg.out_mean = std::numeric_limits<double>::infinity();
+    CHECK_THROWS_WITH(cfg.validate(), wb::ConfigError, "out_mean");
+    cfg.out_mean = 0.0;
+    cfg.validate();
+    CHECK_THROWS_AS(wb::Generator(cfg_of(48, 0)), wb::ConfigError);
+    wb::GeneratorConfig rot = cfg_of(128, 1);
+    rot.transform_family = wb::TransformFamily::rotation;
+    CHECK_THROWS_AS(wb::Generator(rot), wb::UnsupportedError);
+  }
+  // :74-82 identical config gives a bit-identical stream (and == reference)
+  {
+    wb::Generator a(cfg_of(128, 42)), b(cfg_of(128, 42));
+    Ref r(cfg_of(128, 42));
+    bool same = true, ref_same = true;
+    for (int i = 0; i < 10000; ++i) {
+      const double x = a.next_normal();
+      same = same && x == b.next_normal();
+      ref_same = ref_same && x == ref_next_normal(r.g);
+    }
+    CHECK(same);
+    CHECK(ref_same);
+  }
+  // :84-91 construction normalizes the pool and warms up
+  {
+    wb::Generator gen(cfg_of(1024, 7));
+    CHECK(gen.pass_count() == 16);
+    CHECK(std::abs(pool_sum_sq(gen.pool().raw) - 1024.0) <= 1e-12 * 1024.0);
+    CHECK(std::abs(gen.pool().sum_sq - 1024.0) <= 1e-12 * 1024.0);
+  }
+  // :93-101 a pool of zeros stays zero under any pass
+  {
+    wb::Generator gen(cfg_of(64, 3));
+    gen.inject_pool(std::vector<double>(64, 0.0));
+    gen.step_pass();
+    bool zero = true;
+    for (double v : gen.pool().raw) zero = zero && v == 0.0;
+    CHECK(zero);
+  }
+  // :143-154 conservation through the 256-pass renormalization
+  {
+    wb::Generator gen(cfg_of(256, 17));
+    bool ok = true;
+    for (int p = 0; p < 300; ++p) {
+      gen.step_pass();
+      const auto& pool = gen.pool();
+      const double actual = pool_sum_sq(pool.raw);
+      ok = ok && std::abs(actual - pool.sum_sq) <= 1e-9 * 256.0 &&
+           std::abs(actual - 256.0) <= 1e-6 * 256.0;
+    }
+    CHECK(ok);
+  }
+  // :218-231 chi-squared scaling disabled reproduces the raw pool
+  {
+    wb::GeneratorConfig cfg = cfg_of(128, 5);
+    cfg.diag.disable_chi2 = true;
+    wb::Generator gen(cfg);
+    const auto po = gen.next_pool();
+    CHECK(po.values.size() == 127);
+    const auto raw = gen.pool().raw;
+    bool eq = true;
+    for (size_t i = 0; i < po.values.size(); ++i) eq = eq && po.values[i] == raw[i];
+    CHECK(eq);
+    CHECK(po.reserved == raw[127]);
+    CHECK(po.chi2_draw == gen.pool().sum_sq);
+  }
+  // :233-244 mean and sigma are an exact affine map of the unit stream
+  {
+    wb::GeneratorConfig unit = cfg_of(256, 99), scaled = cfg_of(256, 99);
+    scaled.out_mean = 5.0;
+    scaled.out_sigma = 2.0;
+    wb::Generator a(unit), b(scaled);
+    bool ok = true;
+    for (int i = 0; i < 10000; ++i) ok = ok && 2.0 * a.next_normal() + 5.0 == b.next_normal();
+    CHECK(ok);
+  }
+  // :246-260 emission scales to the chi-squared draw
+  {
+    wb::Generator gen(cfg_of(1024, 31));
+    bool ok = true;
+    for (int rep = 0; rep < 50; ++rep) {
+      const auto po = gen.next_pool();
+      std::vector<double> vals(po.values.begin(), po.values.end());
+      const double total = pool_sum_sq(vals) + po.reserved * po.reserved;
+      ok = ok && std::abs(total - po.chi2_draw) <= 1e-9 * 1024.0;
+      const auto pool = gen.pool();
+      const double r = std::sqrt(po.chi2_draw / pool.sum_sq);
+      ok = ok && po.reserved == pool.raw[1023] * r;
+    }
+    CHECK(ok);
+  }
+  // :280-291 reserved variate is sourced from the previous pool
+  {
+    wb::Generator gen(cfg_of(64, 77));
+    const auto p0 = gen.next_pool();
+    int clamped = 0;
+    const double expect_s = ref_chi2_sample(p0.reserved, 64, 2, &clamped);
+    const auto p1 = gen.next_pool();
+    CHECK(p1.chi2_draw == expect_s);
+  }
+  // :293-310 fill is equivalent to repeated next_normal; fill(0) throws
+  {
+    wb::Generator a(cfg_of(64, 21)), b(cfg_of(64, 21));
+    const auto first = a.fill(5);
+    const auto second = a.fill(5);
+    bool ok = true;
+    for (int i = 0; i < 5; ++i) ok = ok && first[i] == b.next_normal();
+    for (int i = 0; i < 5; ++i) ok = ok && second[i] == b.next_normal();
+    CHECK(ok);
+    CHECK_THROWS_AS(a.fill(0), wb::InvalidParameterError);
+    wb::Generator c(cfg_of(64, 21));
+    const auto before = c.pass_count();
+    c.fill(3 * 64);
+    CHECK(c.pass_count() - before >= 3);
+  }
+  // :312-335 discard policy emits every k-th pool
+  {
+    wb::GeneratorConfig third = cfg_of(64, 9);
+    third.discard_every = 3;
+    wb::Generator b(third);
+    bool ok = true;
+    for (int i = 0; i < 10; ++i) {
+      b.next_pool();
+      ok = ok && b.pass_count() == uint64_t(16 + 3 * (i + 1));
+    }
+    CHECK(ok);
+  }
+  // :337-351 at least one uniform draw per pool
+  {
+    for (size_t discard : {size_t(1), size_t(3)}) {
+      wb::GeneratorConfig cfg = cfg_of(64, 2);
+      cfg.discard_every = discard;
+      wb::Generator gen(cfg);
+      uint64_t prev = gen.uniform_draws();
+      bool ok = true;
+      for (int i = 0; i < 20; ++i) {
+        gen.next_pool();
+        const uint64_t d = gen.uniform_draws();
+        ok = ok && d - prev >= discard;
+        prev = d;
+      }
+      CHECK(ok);
+    }
+  }
+  // :353-358 inject_pool validates the size
+  {
+    wb::Generator gen(cfg_of(64, 2));
+    CHECK_THROWS_AS(gen.inject_pool(std::vector<double>(63, 1.0)), wb::InvalidParameterError);
+  }
+  // :360-376 stream moments are sane at a million draws
+  {
+    wb::Generator gen(cfg_of(1024, 4242));
+    const auto v = gen.fill(1000000);
+    double sum = 0.0, sum2 = 0.0;
+    for (double z : v) {
+      sum += z;
+      sum2 += z * z;
+    }
+    const double nn = 1e6, mean = sum / nn, var = sum2 / nn - mean * mean;
+    CHECK(std::abs(mean) <= 5.0 / std::sqrt(nn));
+    CHECK(std::abs(var - 1.0) <= 5.0 * std::sqrt(2.0 / nn));
+  }
+  // bit-for-bit against the reference library on every BASELINE shape, and
+  // through an interleaved API sequence
+  {
+    struct Case {
+      size_t n, d;
+      int chi2;
+      bool dis;
+      uint64_t seed;
+      size_t count;
+    };
+    const Case cases[] = {{4096, 2, 2, true, 1, 1 << 18},  {4096, 2, 2, false, 1, 1 << 18},
+                          {2048, 3, 2, false, 7, 1 << 17}, {1024, 1, 2, false, 1, 1 << 20},
+                          {64, 1, 0, false, 5, 100000},     {128, 3, 1, false, 9, 50000}};
+    for (const auto& k : cases) {
+      wb::GeneratorConfig c = cfg_of(k.n, k.seed);
+      c.discard_every = k.d;
+      c.chi2_method = static_cast<wb::Chi2Method>(k.chi2);
+      c.diag.disable_chi2 = k.dis;
+      wb::Generator g(c);
+      Ref r(c);
+      CHECK(same_bits(g.fill(k.count), r.fill(k.count)));
+    }
+    wb::GeneratorConfig c = cfg_of(64, 21);
+    c.out_mean = 5.0;
+    c.out_sigma = 2.0;
+    c.discard_every = 2;
+    wb::Generator g(c);
+    Ref r(c);
+    bool ok = true;
+    for (size_t k : {5, 5, 200, 63, 1}) ok = ok && same_bits(g.fill(k), r.fill(k));
+    g.step_pass();
+    ref_step_pass(r.g);
+    for (int i = 0; i < 100; ++i) ok = ok && g.next_normal() == ref_next_normal(r.g);
+    const auto po = g.next_pool();
+    std::vector<double> rv(63);
+    double rres, rchi;
+    ref_next_pool(r.g, rv.data(), &rres, &rchi);
+    ok = ok && std::memcmp(po.values.data(), rv.data(), 63 * 8) == 0 && po.reserved == rres &&
+         po.chi2_draw == rchi;
+    std::vector<double> inj(64);
+    for (int i = 0; i < 64; ++i) inj[i] = -2.0 + 4.0 * i / 63.0;
+    g.inject_pool(inj);
+    ref_inject_pool(r.g, inj.data(), 64);
+    ok = ok && same_bits(g.fill(300), r.fill(300));
+    std::vector<double> rp(64);
+    ref_get_pool(r.g, rp.data());
+    ok = ok && same_bits(g.pool().raw, rp);
+    uint64_t pc, dr, cl;
+    double ss, rpv;
+    ref_get_stats(r.g, &pc, &dr, &cl, &ss, &rpv);
+    ok = ok && g.pass_count() == pc && g.uniform_draws() == dr && g.chi2_clamp_count() == cl &&
+         g.pool().sum_sq == ss && g.pool().reserved_prev == rpv;
+    CHECK(ok);
+  }
+  std::printf("%d checks, %d failed\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
