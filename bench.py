@@ -216,7 +216,7 @@ def run_ours(args):
 
     def step():
         if consume:
-            batch.consume(count)  # synchronous; replays from the live state
+            batch.consume_from_snapshot(count)  # synchronous; replays the seeded job
         else:
             batch.fill_from_snapshot_into(out)
 

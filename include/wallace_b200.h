@@ -150,6 +150,10 @@ wallace_status wallace_fill_from_snapshot(wallace_handle* h, void* dev_out,
 wallace_status wallace_consume(wallace_handle* h, uint64_t count_per_pool, double sums[4],
                                uint64_t hist[258]);
 
+/* wallace_consume starting from the device snapshot (see wallace_snapshot). */
+wallace_status wallace_consume_from_snapshot(wallace_handle* h, uint64_t count_per_pool,
+                                             double sums[4], uint64_t hist[258]);
+
 /* Box-Muller comparator (baselines.cpp:68-92): stream p consumes the
  * uniform stream UniformState(seeds[p] or seed_base+p) exactly as
  * boxmuller_next does (u1 == 0 -> 2^-53, cached twin), evaluated on the

@@ -243,6 +243,14 @@ class PoolBatch:
                                       hist.ctypes.data_as(C.POINTER(C.c_uint64))))
         return sums, hist
 
+    def consume_from_snapshot(self, count: int):
+        sums = np.zeros(4, dtype=np.float64)
+        hist = np.zeros(258, dtype=np.uint64)
+        _check(self.L.wallace_consume_from_snapshot(
+            self.h, count, sums.ctypes.data_as(C.POINTER(C.c_double)),
+            hist.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return sums, hist
+
     def set_stream(self, stream) -> None:
         self._stream = _stream_handle(stream)
         _check(self.L.wallace_set_stream(self.h, self._stream))

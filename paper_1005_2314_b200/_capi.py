@@ -74,6 +74,7 @@ SYMBOLS = [
     ("wallace_snapshot", i32, [vp]),
     ("wallace_fill_from_snapshot", i32, [vp, vp, u64]),
     ("wallace_consume", i32, [vp, u64, P(f64), P(u64)]),
+    ("wallace_consume_from_snapshot", i32, [vp, u64, P(f64), P(u64)]),
     ("wallace_boxmuller_consume", i32, [P(u64), u64, u64, u64, vp, P(f64), P(u64)]),
     ("wallace_profile_begin", i32, [vp]),
     ("wallace_profile_end", i32, [vp, P(f64), P(u64), P(f64), P(u64)]),

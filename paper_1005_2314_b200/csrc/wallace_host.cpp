@@ -883,8 +883,10 @@ static wallace_status finish_consumer(cudaStream_t stream, const double* part_su
   return WALLACE_OK;
 }
 
-wallace_status wallace_consume(wallace_handle* h, uint64_t count, double sums[4], uint64_t hist[258]) {
+static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sums[4],
+                                   uint64_t hist[258], bool from_snapshot) {
   if (!h || !sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "handle/sums/hist must not be NULL");
+  if (from_snapshot && !h->has_snapshot) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (h->part_cap < h->n_pools) {
     cudaFree(h->d_part_sums);
@@ -904,13 +906,24 @@ wallace_status wallace_consume(wallace_handle* h, uint64_t count, double sums[4]
   const uint64_t d = h->cfg.discard_every;
   const uint64_t per_launch_emit = std::max<uint64_t>(1, h->plan_cap / std::max<uint64_t>(1, d));
   uint64_t done = 0;
+  if (from_snapshot) {
+    if (h->d_snap_leftover && h->snap_cursor < h->N - 1)
+      WB_CUDA(cudaMemcpyAsync(h->d_leftover, h->d_snap_leftover, h->n_pools * (h->N - 1) * h->esize,
+                              cudaMemcpyDeviceToDevice, h->stream));
+    h->cursor = h->snap_cursor;
+    h->pass_count = h->snap_pass_count;
+  }
+  bool first = true;
   while (done < count) {
     // values a single launch produces: the lead plus per_launch_emit emissions
     const uint64_t lead = (h->cursor < n1) ? (n1 - h->cursor) : 0;
     const uint64_t cap = lead + per_launch_emit * n1;
     const uint64_t c = std::min(cap, count - done);
-    wallace_status st = run_emit(h, nullptr, c, wb::kModeConsume, h->d_state, h->d_pools);
+    const bool snap = from_snapshot && first;
+    wallace_status st = run_emit(h, nullptr, c, wb::kModeConsume, snap ? h->d_snap_state : h->d_state,
+                                 snap ? h->d_snap_pools : h->d_pools);
     if (st) return st;
+    first = false;
     double s4[4];
     uint64_t h258[258];
     st = finish_consumer(h->stream, h->d_part_sums, h->d_part_hist, h->n_pools, s4, h258);
@@ -922,6 +935,15 @@ wallace_status wallace_consume(wallace_handle* h, uint64_t count, double sums[4]
   for (int k = 0; k < 4; ++k) sums[k] = tot[k];
   for (int b = 0; b < 258; ++b) hist[b] = th[b];
   return WALLACE_OK;
+}
+
+wallace_status wallace_consume(wallace_handle* h, uint64_t count, double sums[4], uint64_t hist[258]) {
+  return consume_impl(h, count, sums, hist, false);
+}
+
+wallace_status wallace_consume_from_snapshot(wallace_handle* h, uint64_t count, double sums[4],
+                                             uint64_t hist[258]) {
+  return consume_impl(h, count, sums, hist, true);
 }
 
 wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_base, uint64_t n_streams,
