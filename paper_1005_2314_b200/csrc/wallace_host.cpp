@@ -8,6 +8,7 @@
 // the reference uses (bit parity of the seeded pool); the 16 warm-up passes
 // then run on the device.  Seeding is spread over host threads, one pool at a
 // time per thread.
+#include <cuda.h>  // CUtensorMap / cuTensorMapEncodeTiled signature
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -180,6 +181,42 @@ int ilog2(uint64_t v) {
   int l = 0;
   while ((1ull << l) < v) ++l;
   return l;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library links cudart statically and never links libcuda directly).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D map of a pool-major output [n_pools][count], box 256 x 1, for the
+// bulk-store emission path.  False when the layout does not allow it
+// (alignment, stride, coordinate range); the kernel then emits from registers.
+bool make_output_map(CUtensorMap* map, void* out, uint64_t count, uint64_t n_pools, size_t esize) {
+  if (!out || (reinterpret_cast<uintptr_t>(out) & 15) || (count * esize) % 16 || count >= (1ull << 31) ||
+      n_pools >= (1ull << 31) || count < 256)
+    return false;
+  const EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {count, n_pools};
+  const cuuint64_t strides[1] = {count * esize};
+  const cuuint32_t box[2] = {256, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out,
+            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 constexpr uint64_t kPlanBudgetBytes = 128ull << 20;
@@ -378,8 +415,13 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
   const uint64_t d = h->cfg.discard_every;
   uint64_t produced = 0;
   bool first = true;
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  const bool tma_ok = mode == wb::kModeFill && make_output_map(&tmap, out, count, h->n_pools, h->esize);
   while (produced < count) {
     wb::FillArgs a = base_args(h);
+    a.tma_ok = tma_ok ? 1 : 0;
+    a.tmap = tmap;
     a.mode = mode;
     a.out = out;
     a.out_stride = count;

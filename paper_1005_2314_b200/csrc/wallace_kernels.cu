@@ -13,6 +13,7 @@
 // compiled with -fmad=false, so no multiply-add is contracted — the
 // reference pins -ffp-contract=off for the same reason
 // (/root/reference/proj/CMakeLists.txt:10-14).
+#include <cuda.h>  // CUtensorMap (the map itself is encoded on the host)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -76,6 +77,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #endif
 #ifndef WB_D2_STG64
 #define WB_D2_STG64 0
+#endif
+// 1: bulk (TMA) emission when the emission is the pool itself (scale 1, mean +0)
+#ifndef WB_TMA
+#define WB_TMA 0
 #endif
 #ifndef WB_REGS_PP
 #define WB_REGS_PP 80
@@ -215,6 +220,7 @@ struct SState {
   uint32_t clamp;
   uint32_t flags;
   int32_t renorm_ok;
+  uint32_t zero_seen;  // an exact zero was emitted by bulk stores (patch needed)
 };
 
 // S, r, scale of the emission in `slot` from the current reserved value.
@@ -325,7 +331,8 @@ struct Consumer {
 // ---------------------------------------------------------------------------
 template <typename T, int LOG2N, int DELTA, bool MZ>
 __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], int c0, T (&prev)[4],
-                                           T* gbase, T sc, T mean, int lane, int warp) {
+                                           T* gbase, T sc, T mean, int lane, int warp,
+                                           int jfirst = 0) {
   using G = Geo<T, LOG2N>;
   constexpr int J = G::J, JC = G::JC, VEC = G::VEC;
   static_assert(DELTA < VEC, "shift");
@@ -333,6 +340,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
 #pragma unroll
   for (int jj = 0; jj < JC; ++jj) {
     const int j = c0 + jj;
+    if (j < jfirst) continue;  // groups before jfirst are emitted by bulk stores
     const uint32_t b = (warp * J + j) * 32 + lane;
     T y[4];
 #pragma unroll
@@ -367,11 +375,11 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         else c[m] = sh[(DELTA + m - 4) & (DELTA > 0 ? 3 : 0)];
       }
       const uint32_t cb = l31 ? b - 32 : b;  // lane 31 completes its previous group
-      if (!(l31 && j == 0)) {
+      if (!(l31 && j == jfirst)) {
 #pragma unroll
         for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * cb + DELTA + v, c + v);
       }
-      if (j == 0 && lane == 0) {  // head of this warp's first block
+      if (j == jfirst && lane == 0) {  // head of this warp's first block
 #pragma unroll
         for (int t = 0; t < DELTA; ++t) stg1(gbase + 4 * b + t, y[t]);
       }
@@ -391,9 +399,62 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
 
 template <typename T, int LOG2N, int DELTA>
 __device__ __forceinline__ void emit_chunk_mz(bool mz, const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
-                                              T (&prev)[4], T* gbase, T sc, T mean, int lane, int warp) {
-  if (mz) emit_chunk<T, LOG2N, DELTA, true>(X, c0, prev, gbase, sc, mean, lane, warp);
-  else emit_chunk<T, LOG2N, DELTA, false>(X, c0, prev, gbase, sc, mean, lane, warp);
+                                              T (&prev)[4], T* gbase, T sc, T mean, int lane, int warp,
+                                              int jfirst = 0) {
+  if (mz) emit_chunk<T, LOG2N, DELTA, true>(X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+  else emit_chunk<T, LOG2N, DELTA, false>(X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+}
+
+// Register emission of one chunk for any shift: dispatch on delta.
+template <typename T, int LOG2N>
+__device__ __forceinline__ void emit_chunk_any(uint32_t delta, bool mz,
+                                               const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
+                                               T (&prev)[4], T* gbase, T sc, T mean, int lane,
+                                               int warp, int jfirst = 0) {
+  using G = Geo<T, LOG2N>;
+  if constexpr (G::VEC == 4) {
+    switch (delta) {
+      case 0: emit_chunk_mz<T, LOG2N, 0>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+      case 1: emit_chunk_mz<T, LOG2N, 1 % G::VEC>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+      case 2: emit_chunk_mz<T, LOG2N, 2 % G::VEC>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+      default: emit_chunk_mz<T, LOG2N, 3 % G::VEC>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+    }
+  } else {
+    if (delta == 0) emit_chunk_mz<T, LOG2N, 0>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+    else emit_chunk_mz<T, LOG2N, 1>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bulk (TMA) emission.  When an emission's scale is exactly 1 and the mean
+// is +0 (e.g. disable_chi2 with sigma 1 — BASELINE config 2), its values are
+// the pool itself, already in shared memory in pool order: out[i] = x[i]*1+0
+// = x[i] bit for bit, except that the reference's "+0" turns an exact -0 into
+// +0.  The emission is then issued as 2-D tensor stores of BOX elements from
+// the pool buffer (TMA takes arbitrary element coordinates, so the output's
+// misalignment costs nothing); the last (N-1) mod BOX + ... values, the
+// groups past the last full box, go through the register path; an exact zero
+// anywhere in the emission (probability ~1e-8 per value) triggers a patch
+// pass that rewrites -0 as +0 after the bulk stores have completed.
+// ---------------------------------------------------------------------------
+constexpr int kTmaBox = 256;  // elements per tensor-store box (TMA box dim limit)
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -536,7 +597,7 @@ __device__ __forceinline__ void consume_chunk(const T (&X)[Geo<T, LOG2N>::JC][4]
 
 template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
-    pool_kernel(const FillArgs a) {
+    pool_kernel(const __grid_constant__ FillArgs a) {
   using G = Geo<T, LOG2N>;
   using SM = Smem<T, LOG2N>;
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
@@ -570,6 +631,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     s.last_r = st.r;
     s.last_scale = st.scale;
     s.clamp = 0;
+    s.zero_seen = 0;
     s.flags = st.flags;
     if (MODE != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
   }
@@ -623,6 +685,15 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     }
   } else {
     uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
+    // bulk-store geometry (see "Bulk (TMA) emission"): boxes cover pool
+    // elements [0, TMA_ELEMS); 4-blocks from TAIL_B on go through registers
+    constexpr int TMA_ELEMS = ((N - 1) / kTmaBox) * kTmaBox;
+    constexpr int TAIL_B = TMA_ELEMS / 4;
+    constexpr bool TMA_GEOM = MODE == kModeFill && FAST && TMA_ELEMS > 0 && TAIL_B % 32 == 0;
+    // groups of the last warp at or past TAIL_B (the tail is in the last warp)
+    constexpr int TAIL_J = TMA_GEOM ? (TAIL_B - (G::NW - 1) * J * 32) / 32 : 0;
+    static_assert(!TMA_GEOM || (TAIL_J >= 0 && TAIL_J < J), "tail must sit in the last warp");
+    bool bulk_pending = false;
     T* gbase = out_pool + a.lead;  // element 0 of the current emission
     for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
       const int slot = e & 1;
@@ -637,7 +708,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         if (!WB_PREFETCH) plan = s_plans[p];
         const uint32_t plan_p = plan;
         if (WB_PREFETCH) plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
-        const bool do_emit = fast && WB_ABLATE != 1;
+        const bool do_emit = fast && WB_ABLATE != 1 && WB_ABLATE != 4;
         T sc = T(0);
         uint32_t delta = 0;
         if (do_emit) {
@@ -645,6 +716,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
                   (G::VEC - 1);
         }
+        // the pool itself is the emission: bulk stores from shared memory
+        const bool bulk = TMA_GEOM && WB_TMA && do_emit && a.tma_ok && mean_zero && sc == T(1);
+        bool zero_seen = false;
         T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
         T x_last = T(0);
         for (int c0 = 0; c0 < J; c0 += G::JC) {
@@ -652,16 +726,15 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
           if (do_emit) {
             if constexpr (MODE == kModeFill) {
-              if constexpr (G::VEC == 4) {
-                switch (delta) {
-                  case 0: emit_chunk_mz<T, LOG2N, 0>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
-                  case 1: emit_chunk_mz<T, LOG2N, 1 % G::VEC>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
-                  case 2: emit_chunk_mz<T, LOG2N, 2 % G::VEC>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
-                  default: emit_chunk_mz<T, LOG2N, 3 % G::VEC>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp); break;
-                }
+              if (bulk) {
+#pragma unroll
+                for (int jj = 0; jj < G::JC; ++jj)
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) zero_seen |= X[jj][k] == T(0);
+                if (warp == G::NW - 1 && c0 + G::JC > TAIL_J)
+                  emit_chunk_any<T, LOG2N>(delta, true, X, c0, prev, gbase, sc, mean_t, lane, warp, TAIL_J);
               } else {
-                if (delta == 0) emit_chunk_mz<T, LOG2N, 0>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
-                else emit_chunk_mz<T, LOG2N, 1>(mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
+                emit_chunk_any<T, LOG2N>(delta, mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
               }
             } else {
               consume_chunk<T, LOG2N>(X, cons, sc, mean_t, mean_zero, b0 + 32 * c0);
@@ -669,13 +742,61 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           }
           x_last = X[G::JC - 1][3];
         }
+        if (bulk) {
+          fence_proxy_async_smem();  // this thread's pool stores -> visible to the bulk copies
+          if (zero_seen) s.zero_seen = 1;
+        }
         if (do_emit && tid == G::OWNER && WB_ABLATE != 3) {
           chain_close(s, slot, static_cast<double>(x_last));
           if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
         }
+        // the bulk copies of the previous emission must have read their
+        // source before this barrier releases the buffer for overwriting
+        if (bulk_pending && tid == 0) bulk_wait_read();
+        bulk_pending = false;
+#if WB_ABLATE == 4
+        // timing-only: the previous bulk store must have read its source
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
         __syncthreads();
         cur_off ^= FLIP;
         T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+        if (bulk) {
+          if (tid == 0) {
+            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
+            const int x0 = static_cast<int>(a.out_offset + a.lead + uint64_t(e) * (N - 1));
+#pragma unroll 1
+            for (int k = 0; k < TMA_ELEMS / kTmaBox; ++k)
+              tma_store_2d(&a.tmap, src + k * kTmaBox * sizeof(T), x0 + k * kTmaBox, static_cast<int>(pool));
+            bulk_commit();
+          }
+          bulk_pending = true;
+          if (s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk stores landed
+            if (tid == 0) {
+              bulk_wait_all();
+              fence_proxy_async_global();
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < uint32_t(TMA_ELEMS); i += THREADS)
+              if (cur[i] == T(0) && signbit(cur[i])) stg1(gbase + i, T(0));
+            __syncthreads();
+            if (tid == 0) s.zero_seen = 0;
+            __syncthreads();
+          }
+        }
+#if WB_ABLATE == 4
+        // timing-only: emission as one bulk (TMA) store of the pool buffer to an
+        // aligned-down address (wrong output; measures the store-path cost)
+        if (fast && tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const unsigned long long dst = reinterpret_cast<unsigned long long>(gbase) & ~15ull;
+          const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                       "r"(uint32_t((N - 1) * sizeof(T)) & ~15u)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+#endif
         if (renorm_now) {
           renormalize<T, N, THREADS>(cur, s, tid);
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
@@ -700,7 +821,12 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         pc = (pc + 1) & 255u;
       }
     }
+    if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
   }
+#if WB_ABLATE == 4
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncthreads();
+#endif
   T* const cur = reinterpret_cast<T*>(pbase + cur_off);
 
   // ---- epilogue: pool and state back to HBM ---------------------------------

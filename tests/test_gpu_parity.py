@@ -263,3 +263,28 @@ def test_boxmuller_comparator_statistics(cuda):
     assert int(hist.sum()) == n
     rep = pb.moment_reports(sums, n)
     assert all(r[4] for r in rep.values()), rep
+
+
+@pytest.mark.parametrize("n", [512, 4096, 16384])
+def test_unit_scale_emission_with_exact_zeros(cuda, n):
+    """Scale-1/mean-0 emissions (disable_chi2, sigma 1): a sparse injected pool
+    makes exact zeros of both signs; the reference emits them as +0 (x*1 + 0),
+    so the device output must have no -0 and match bit for bit."""
+    kw = dict(pool_size=n, discard_every=2, disable_chi2=True)
+    inj = np.zeros(n)
+    inj[::97] = 1.0
+    inj[5::131] = -0.5
+    for dtype in ("f32", "f64"):
+        if dtype == "f64" and n > 8192:
+            continue
+        b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=[3, 4], dtype=dtype)
+        o = [OracleGen(ocfg(seed=s, **kw), dtype) for s in (3, 4)]
+        b.inject_pool(inj, pool=0)
+        o[0].inject_pool(inj)
+        count = 6 * (n - 1) + 16
+        got = b.fill(count).cpu().numpy()
+        for p in range(2):
+            want = o[p].fill(count)
+            assert_same(got[p], want, f"{dtype} n={n} pool {p}")
+        assert np.any(got[0] == 0)
+        assert not np.any(np.signbit(got[0][got[0] == 0]))
