@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "wallace_common.h"
 
@@ -82,6 +83,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_TMA
 #define WB_TMA 0
 #endif
+// 1: emission stores at one base register + immediate group offsets
+#ifndef WB_EMIT_IMM
+#define WB_EMIT_IMM 0
+#endif
 #ifndef WB_REGS_PP
 #define WB_REGS_PP 80
 #endif
@@ -134,6 +139,15 @@ struct Geo {
   static constexpr int MINB = MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS;
 };
 
+// compile-time loop: f(std::integral_constant<int, i>) for i in [0, N)
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // explicit-rounding arithmetic
 // ---------------------------------------------------------------------------
@@ -176,6 +190,19 @@ __device__ __forceinline__ void stg_vec(double* p, const double* v) {
 }
 template <typename T>
 __device__ __forceinline__ void stg1(T* p, T v) { __stcs(p, v); }
+// streaming 128-bit store at base + OFF bytes (OFF an immediate: one base
+// register serves every group of a chunk)
+template <int OFF>
+__device__ __forceinline__ void stg_vec_at(uint64_t base, const float* v) {
+  // no "memory" clobber: nothing in the kernel reads the output, and a
+  // clobber would pin the scheduler (all stores bunched at the end)
+  asm("st.global.cs.v4.f32 [%0+%1], {%2, %3, %4, %5};" ::"l"(base), "n"(OFF), "f"(v[0]), "f"(v[1]),
+      "f"(v[2]), "f"(v[3]));
+}
+template <int OFF>
+__device__ __forceinline__ void stg_vec_at(uint64_t base, const double* v) {
+  asm("st.global.cs.v2.f64 [%0+%1], {%2, %3};" ::"l"(base), "n"(OFF), "d"(v[0]), "d"(v[1]));
+}
 #if WB_ABLATE == 2
 #define stg_vec(p, v) do { if (reinterpret_cast<uintptr_t>(p) == 1) stg_vec(p, v); } while (0)
 #endif
@@ -337,11 +364,27 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
   constexpr int J = G::J, JC = G::JC, VEC = G::VEC;
   static_assert(DELTA < VEC, "shift");
   const bool l31 = lane == 31;
+  const uint32_t b0 = warp * J * 32 + lane;  // this thread's block in group 0
+  // Every lane's chunk of group j starts at cbase + 128 j elements: lanes
+  // 0..30 store their own group-j chunk, lane 31 its group-(j-1) chunk, so
+  // its base is one group (128 elements) lower.  The group offsets are then
+  // immediates of the store instructions.
+  const uint64_t cbase = reinterpret_cast<uint64_t>(gbase) +
+                         sizeof(T) * (4ull * (b0 + 32u * c0) + DELTA) -
+                         ((DELTA > 0 && l31) ? 128u * sizeof(T) : 0u);
+  auto store_group = [&](auto jjc, const T* c) {
+    constexpr int JJ = decltype(jjc)::value;
+#pragma unroll
+    for (int v = 0; v < 4; v += VEC) {
+      if (v == 0) stg_vec_at<JJ * 128 * int(sizeof(T))>(cbase, c);
+      else stg_vec_at<JJ * 128 * int(sizeof(T)) + 16>(cbase, c + 2);
+    }
+  };
 #pragma unroll
   for (int jj = 0; jj < JC; ++jj) {
     const int j = c0 + jj;
-    if (j < jfirst) continue;  // groups before jfirst are emitted by bulk stores
-    const uint32_t b = (warp * J + j) * 32 + lane;
+    if (j < jfirst) continue;  // groups before jfirst are emitted elsewhere
+    const uint32_t b = b0 + 32 * j;
     T y[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
@@ -357,8 +400,14 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       }
     } else if constexpr (DELTA == 0) {
       if (b != G::ROWS - 1) {
+        if constexpr (WB_EMIT_IMM) {
+          static_for<JC>([&](auto jjc) {
+            if (decltype(jjc)::value == jj) store_group(jjc, y);
+          });
+        } else {
 #pragma unroll
-        for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * b + v, y + v);
+          for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * b + v, y + v);
+        }
       } else {
         stg1(gbase + 4 * b + 0, y[0]);
         stg1(gbase + 4 * b + 1, y[1]);
@@ -374,10 +423,16 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         if (DELTA + m < 4) c[m] = l31 ? prev[(DELTA + m) & 3] : y[(DELTA + m) & 3];
         else c[m] = sh[(DELTA + m - 4) & (DELTA > 0 ? 3 : 0)];
       }
-      const uint32_t cb = l31 ? b - 32 : b;  // lane 31 completes its previous group
       if (!(l31 && j == jfirst)) {
+        if constexpr (WB_EMIT_IMM) {
+          static_for<JC>([&](auto jjc) {
+            if (decltype(jjc)::value == jj) store_group(jjc, c);
+          });
+        } else {
+          const uint32_t cb = l31 ? b - 32 : b;
 #pragma unroll
-        for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * cb + DELTA + v, c + v);
+          for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * cb + DELTA + v, c + v);
+        }
       }
       if (j == jfirst && lane == 0) {  // head of this warp's first block
 #pragma unroll
