@@ -172,6 +172,12 @@ wallace_status wallace_profile_end(wallace_handle* h, double* pool_kernel_ms,
                                    uint64_t* pool_launches, double* plan_kernel_ms,
                                    uint64_t* plan_launches);
 
+/* Kernel shape: 0 auto (latency kernel for <= 148 pools), 1 throughput
+ * kernel (a few warps per pool, many pools per SM), 2 latency kernel (one
+ * 4-block per thread, up to 1024 threads per pool).  Results are identical;
+ * exposed for tests and tuning. */
+wallace_status wallace_set_kernel_mode(wallace_handle* h, int32_t mode);
+
 /* Rebind the handle to another stream. */
 wallace_status wallace_set_stream(wallace_handle* h, void* stream);
 

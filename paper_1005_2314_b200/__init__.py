@@ -251,6 +251,10 @@ class PoolBatch:
             hist.ctypes.data_as(C.POINTER(C.c_uint64))))
         return sums, hist
 
+    def set_kernel_mode(self, mode: str) -> None:
+        """'auto', 'throughput' or 'latency' (identical results)."""
+        _check(self.L.wallace_set_kernel_mode(self.h, {"auto": 0, "throughput": 1, "latency": 2}[mode]))
+
     def set_stream(self, stream) -> None:
         self._stream = _stream_handle(stream)
         _check(self.L.wallace_set_stream(self.h, self._stream))

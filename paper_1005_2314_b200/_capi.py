@@ -78,6 +78,7 @@ SYMBOLS = [
     ("wallace_boxmuller_consume", i32, [P(u64), u64, u64, u64, vp, P(f64), P(u64)]),
     ("wallace_profile_begin", i32, [vp]),
     ("wallace_profile_end", i32, [vp, P(f64), P(u64), P(f64), P(u64)]),
+    ("wallace_set_kernel_mode", i32, [vp, i32]),
     ("wallace_set_stream", i32, [vp, vp]),
     ("wallace_kernel_launches", u64, []),
     ("wallace_last_error", C.c_char_p, []),

@@ -238,7 +238,12 @@ struct wallace_handle {
 
   void* d_pools = nullptr;
   PoolState* d_state = nullptr;
-  uint32_t* d_plans = nullptr;
+  uint32_t* d_plans = nullptr;   // two plan buffers of n_pools * plan_cap words
+  // plan generation runs one launch ahead on a side stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_planned[2] = {nullptr, nullptr}, ev_pooled[2] = {nullptr, nullptr};
+  int key = 0;        // kernel key: log2(N) (+16 for the latency kernel)
+  int kmode = 0;      // 0 auto, 1 throughput, 2 latency
   void* d_leftover = nullptr;
   void* d_snap_pools = nullptr;
   PoolState* d_snap_state = nullptr;
@@ -301,14 +306,25 @@ wallace_status check_supported(const wallace_config* c, int dtype) {
   return WALLACE_OK;
 }
 
+// Few pools cannot fill the GPU with the throughput kernel (a few warps per
+// pool): give each pool a CTA of up to 1024 threads instead.
+constexpr uint64_t kLatencyMaxPools = 148;
+
+void select_kernel(wallace_handle* h) {
+  const int lim = h->dtype == WALLACE_F32 ? 14 : 13;
+  const bool lat_ok = h->log2n >= 8 && h->log2n <= lim;
+  bool lat = false;
+  if (h->kmode == 2) lat = lat_ok;
+  else if (h->kmode == 0) lat = lat_ok && h->n_pools <= kLatencyMaxPools;
+  h->key = h->log2n + (lat ? 16 : 0);
+}
+
 wb::FillArgs base_args(wallace_handle* h) {
   wb::FillArgs a{};
   a.pools_in = h->d_pools;
   a.pools_out = h->d_pools;
   a.st_in = h->d_state;
   a.st_out = h->d_state;
-  a.plans = h->d_plans;
-  a.plan_stride = h->plan_cap;
   a.d = static_cast<uint32_t>(std::min<uint64_t>(h->cfg.discard_every, 0xffffffffu));
   a.mean = h->cfg.out_mean;
   a.sigma = h->cfg.out_sigma;
@@ -333,58 +349,81 @@ cudaEvent_t take_event(wallace_handle* h) {
 // Brackets one launch with events when profiling is on.
 template <class F>
 cudaError_t timed(wallace_handle* h, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& log,
-                  F&& launch) {
+                  cudaStream_t stream, F&& launch) {
   if (!h->profiling) return launch();
   cudaEvent_t a = take_event(h), b = take_event(h);
-  cudaEventRecord(a, h->stream);
+  cudaEventRecord(a, stream);
   const cudaError_t e = launch();
-  cudaEventRecord(b, h->stream);
+  cudaEventRecord(b, stream);
   log.emplace_back(a, b);
   return e;
 }
 
-wallace_status run_plans(wallace_handle* h, uint32_t n_passes, const PoolState* st_in) {
-  if (n_passes == 0) return WALLACE_OK;
-  wb::PlanArgs p{};
-  p.st_in = st_in;
-  p.st_out = h->d_state;
-  p.plans = h->d_plans;
-  p.plan_stride = h->plan_cap;
-  p.n_passes = n_passes;
-  p.n_pools = static_cast<uint32_t>(h->n_pools);
-  p.rows_mask = static_cast<uint32_t>(h->N / 4 - 1);
-  p.fixed_transform = h->cfg.fixed_transform;
-  WB_CUDA(timed(h, h->ev_plan, [&] { return wb::launch_plan_kernel(p, h->stream); }));
-  ++g_launches;
-  return WALLACE_OK;
-}
+// One pool-kernel launch and the plans it consumes.
+struct Launch {
+  wb::FillArgs a;
+};
 
-wallace_status run_pool(wallace_handle* h, const wb::FillArgs& a) {
-  WB_CUDA(timed(h, h->ev_pool,
-                [&] { return wb::launch_pool_kernel(h->dtype, h->log2n, a, h->n_pools, h->stream); }));
-  ++g_launches;
+// Issues a sequence of launches.  Plans for launch k+1 are generated on the
+// side stream while launch k runs (double-buffered plan words); the xoshiro
+// stream itself is advanced only by the plan kernels, in order.
+wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
+  if (ls.empty()) return WALLACE_OK;
+  const size_t plan_words = h->n_pools * size_t(h->plan_cap);
+  WB_CUDA(cudaEventRecord(h->ev_start, h->stream));
+  WB_CUDA(cudaStreamWaitEvent(h->side, h->ev_start, 0));
+  auto plans = [&](size_t k) -> wallace_status {
+    wb::FillArgs& a = ls[k].a;
+    a.plans = h->d_plans + (k & 1) * plan_words;
+    a.plan_stride = h->plan_cap;
+    if (a.n_passes == 0) return WALLACE_OK;
+    // the buffer is free once launch k-2 finished
+    if (k >= 2) WB_CUDA(cudaStreamWaitEvent(h->side, h->ev_pooled[k & 1], 0));
+    wb::PlanArgs p{};
+    p.st_in = a.st_in;
+    p.st_out = h->d_state;
+    p.plans = const_cast<uint32_t*>(a.plans);
+    p.plan_stride = h->plan_cap;
+    p.n_passes = a.n_passes;
+    p.n_pools = static_cast<uint32_t>(h->n_pools);
+    p.rows_mask = static_cast<uint32_t>(h->N / 4 - 1);
+    p.fixed_transform = h->cfg.fixed_transform;
+    WB_CUDA(timed(h, h->ev_plan, h->side, [&] { return wb::launch_plan_kernel(p, h->side); }));
+    ++g_launches;
+    WB_CUDA(cudaEventRecord(h->ev_planned[k & 1], h->side));
+    return WALLACE_OK;
+  };
+  wallace_status st = plans(0);
+  if (st) return st;
+  for (size_t k = 0; k < ls.size(); ++k) {
+    if (k + 1 < ls.size() && (st = plans(k + 1))) return st;
+    const wb::FillArgs& a = ls[k].a;
+    if (a.n_passes > 0) WB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_planned[k & 1], 0));
+    WB_CUDA(timed(h, h->ev_pool, h->stream,
+                  [&] { return wb::launch_pool_kernel(h->dtype, h->key, a, h->n_pools, h->stream); }));
+    ++g_launches;
+    WB_CUDA(cudaEventRecord(h->ev_pooled[k & 1], h->stream));
+  }
   return WALLACE_OK;
 }
 
 // Run n passes without emission (warm-up, step_pass), in launches of at most
 // plan_cap passes.
 wallace_status run_passes(wallace_handle* h, uint64_t n) {
+  std::vector<Launch> ls;
   while (n > 0) {
     const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(n, h->plan_cap));
-    wallace_status st = run_plans(h, k, h->d_state);
-    if (st) return st;
-    wb::FillArgs a = base_args(h);
-    a.mode = wb::kModePasses;
-    a.n_passes = k;
-    a.n_emit = 0;
-    a.lead = 0;
-    a.last_limit = 0;
-    st = run_pool(h, a);
-    if (st) return st;
+    Launch l{base_args(h)};
+    l.a.mode = wb::kModePasses;
+    l.a.n_passes = k;
+    l.a.n_emit = 0;
+    l.a.lead = 0;
+    l.a.last_limit = 0;
+    ls.push_back(l);
     h->pass_count += k;
     n -= k;
   }
-  return WALLACE_OK;
+  return issue(h, ls);
 }
 
 wallace_status ensure_leftover(wallace_handle* h) {
@@ -418,6 +457,7 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
   const bool tma_ok = mode == wb::kModeFill && make_output_map(&tmap, out, count, h->n_pools, h->esize);
+  std::vector<Launch> ls;
   while (produced < count) {
     wb::FillArgs a = base_args(h);
     a.tma_ok = tma_ok ? 1 : 0;
@@ -447,7 +487,9 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
         // per launch)
         wallace_status st = WALLACE_OK;
         if (!first || (st_first == h->d_state && pools_first == h->d_pools)) {
-          st = run_passes(h, d - 1);
+          st = issue(h, ls);
+          ls.clear();
+          if (!st) st = run_passes(h, d - 1);
         } else {
           return fail(WALLACE_ERR_UNSUPPORTED, "discard_every too large for snapshot replay");
         }
@@ -463,21 +505,22 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     a.n_emit = static_cast<uint32_t>(e);
     a.n_passes = static_cast<uint32_t>(passes);
     a.last_limit = static_cast<uint32_t>(last_limit);
-    wallace_status st = run_plans(h, a.n_passes, a.st_in);
-    if (st) return st;
-    st = run_pool(h, a);
-    if (st) return st;
-    if (mode == wb::kModeConsume) {
-      // consumer partials are per launch; fold them into the running totals
-      // by launching the fixed-order reduction per launch (rare: one launch
-      // per fill unless the fill is larger than plan_cap passes)
+    if (a.d != h->cfg.discard_every) {
+      // the huge-discard path ran d-1 passes eagerly: keep launch order
+      std::vector<Launch> one{Launch{a}};
+      wallace_status st = issue(h, ls);
+      if (!st) st = issue(h, one);
+      if (st) return st;
+      ls.clear();
+    } else {
+      ls.push_back(Launch{a});
     }
     h->pass_count += passes;
     h->cursor = e > 0 ? static_cast<uint32_t>(last_limit) : h->cursor + static_cast<uint32_t>(lead);
     produced += lead + (e == 0 ? 0 : (e == e_total ? remaining : e * n1));
     first = false;
   }
-  return WALLACE_OK;
+  return issue(h, ls);
 }
 
 }  // namespace
@@ -587,7 +630,14 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
   } while (0)
   WB_CUDA_C(cudaMalloc(&h->d_pools, pools.size()));
   WB_CUDA_C(cudaMalloc(&h->d_state, n_pools * sizeof(PoolState)));
-  WB_CUDA_C(cudaMalloc(&h->d_plans, n_pools * h->plan_cap * sizeof(uint32_t)));
+  WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * sizeof(uint32_t)));
+  WB_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_planned[i], cudaEventDisableTiming));
+    WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_pooled[i], cudaEventDisableTiming));
+  }
+  select_kernel(h);
   WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,
                             h->stream));
   WB_CUDA_C(cudaMemcpyAsync(h->d_state, states.data(), n_pools * sizeof(PoolState),
@@ -605,6 +655,12 @@ wallace_status wallace_destroy(wallace_handle* h) {
   cudaFree(h->d_pools);
   cudaFree(h->d_state);
   cudaFree(h->d_plans);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_planned[i]) cudaEventDestroy(h->ev_planned[i]);
+    if (h->ev_pooled[i]) cudaEventDestroy(h->ev_pooled[i]);
+  }
   cudaFree(h->d_leftover);
   cudaFree(h->d_snap_pools);
   cudaFree(h->d_snap_state);
@@ -630,6 +686,7 @@ wallace_status wallace_profile_end(wallace_handle* h, double* pool_ms, uint64_t*
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   h->profiling = false;
   WB_CUDA(cudaStreamSynchronize(h->stream));
+  WB_CUDA(cudaStreamSynchronize(h->side));
   auto sum = [&](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& log, double* ms, uint64_t* n) {
     double acc = 0.0;
     for (auto& [a, b] : log) {
@@ -644,6 +701,14 @@ wallace_status wallace_profile_end(wallace_handle* h, double* pool_ms, uint64_t*
   };
   sum(h->ev_pool, pool_ms, pool_n);
   sum(h->ev_plan, plan_ms, plan_n);
+  return WALLACE_OK;
+}
+
+wallace_status wallace_set_kernel_mode(wallace_handle* h, int32_t mode) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (mode < 0 || mode > 2) return fail(WALLACE_ERR_INVALID_PARAM, "kernel mode must be 0, 1 or 2");
+  h->kmode = mode;
+  select_kernel(h);
   return WALLACE_OK;
 }
 

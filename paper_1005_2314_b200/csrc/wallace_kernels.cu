@@ -87,6 +87,11 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_EMIT_IMM
 #define WB_EMIT_IMM 0
 #endif
+// 1: latency kernel runs the per-emission chain in a dedicated warp (measured
+// slower for one pool: the chain latency, not its placement, is the limit)
+#ifndef WB_CHAINW
+#define WB_CHAINW 0
+#endif
 #ifndef WB_REGS_PP
 #define WB_REGS_PP 80
 #endif
@@ -107,19 +112,30 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #define WB_HS_LUT 1
 #endif
 
+// Kernel geometry.  The template key is log2(N) for the throughput kernel
+// (many pools: few warps per pool, 8 4-blocks per thread) and log2(N) + 16
+// for the latency kernel (few pools: one 4-block per thread, up to 1024
+// threads per pool, so one pass is a short critical path).
 template <typename T, int LOG2N>
 struct Geo {
-  static constexpr int N = 1 << LOG2N;
+  static constexpr bool LAT = LOG2N >= 16;
+  static constexpr int N = 1 << (LOG2N & 15);
   static constexpr int ROWS = N / 4;
   // groups (4-blocks) per thread: enough independent gathers per thread to
   // hide LDS latency, few enough warps per pool for cheap barriers.
-  static constexpr int JWANT = sizeof(T) == 4 ? WB_J_F32 : WB_J_F64;
+  static constexpr int JWANT = LAT ? (ROWS > (WB_CHAINW ? 512 : 1024) ? ROWS / (WB_CHAINW ? 512 : 1024) : 1)
+                                   : (sizeof(T) == 4 ? WB_J_F32 : WB_J_F64);
   static constexpr int J = (ROWS >= 32 * JWANT) ? JWANT : (ROWS >= 32 ? ROWS / 32 : 1);
-  static constexpr int JCWANT = sizeof(T) == 4 ? WB_JC_F32 : WB_JC_F64;
+  static constexpr int JCWANT = LAT ? J : (sizeof(T) == 4 ? WB_JC_F32 : WB_JC_F64);
   static constexpr int JC = J < JCWANT ? J : JCWANT;
   static_assert(J % JC == 0, "chunking");
-  static constexpr int THREADS = (ROWS >= 32) ? ROWS / J : 32;
-  static constexpr int NW = THREADS / 32;
+  static constexpr int CT = (ROWS >= 32) ? ROWS / J : 32;  // compute threads (4-block owners)
+  static constexpr int NW = CT / 32;                       // compute warps
+  // the latency kernel adds a chain warp: the per-emission fp64 chain (chi2,
+  // division, sqrt: ~30 dependent ops) then overlaps the next pass instead of
+  // sitting on every pass's critical path
+  static constexpr bool CHAINW = LAT && WB_CHAINW;
+  static constexpr int THREADS = CT + (CHAINW ? 32 : 0);
   static constexpr uint32_t MASK = ROWS - 1;
   static constexpr uint32_t STRIDE = default_stride_c(ROWS) % ROWS;
   static constexpr int VEC = 16 / sizeof(T);  // elements per 128-bit store
@@ -136,7 +152,7 @@ struct Geo {
   static constexpr int MINB_SMEM = MINB_RAW < 1 ? 1 : (MINB_RAW * THREADS > 2048 ? 2048 / THREADS : MINB_RAW);
   static constexpr int REG_BUDGET = INPLACE ? WB_REGS_INPLACE : WB_REGS_PP;
   static constexpr int MINB_REGS = 65536 / (THREADS * REG_BUDGET) < 1 ? 1 : 65536 / (THREADS * REG_BUDGET);
-  static constexpr int MINB = MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS;
+  static constexpr int MINB = LAT ? 1 : (MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS);
 };
 
 // compile-time loop: f(std::integral_constant<int, i>) for i in [0, N)
@@ -248,6 +264,7 @@ struct SState {
   uint32_t flags;
   int32_t renorm_ok;
   uint32_t zero_seen;  // an exact zero was emitted by bulk stores (patch needed)
+  uint32_t ready;      // chain-warp kernels: S/r/scale of every emission <= ready published
 };
 
 // S, r, scale of the emission in `slot` from the current reserved value.
@@ -271,6 +288,21 @@ __device__ __forceinline__ void chain_close(SState& s, int slot, double x_last) 
   s.last_chi2 = s.S[slot];
   s.last_r = s.r[slot];
   s.last_scale = s.scale[slot];
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p)))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
 }
 
 // generator.cpp:20-34 recompute_sum_sq — sequential Neumaier, one thread.
@@ -529,7 +561,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // ---------------------------------------------------------------------------
 template <typename T, int LOG2N>
 struct Smem {
-  static constexpr int N = 1 << LOG2N;
+  static constexpr int N = Geo<T, LOG2N>::N;
   static constexpr uint32_t BUF = N * sizeof(T);  // bytes per pool buffer (power of two)
   // pools in static shared memory when they fit the 48 KiB static limit: the
   // buffer base then folds into the LDS/STS immediate offsets
@@ -672,6 +704,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t b0 = warp * J * 32 + lane;  // first 4-block of this thread
+  const bool compute = !G::CHAINW || tid < G::CT;  // owns 4-blocks (else: chain warp)
   const uint64_t pool = blockIdx.x;
   const bool mean_zero = a.mean_is_zero != 0;
   const T mean_t = from_double<T>(a.mean);
@@ -687,6 +720,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     s.last_scale = st.scale;
     s.clamp = 0;
     s.zero_seen = 0;
+    s.ready = 0;
     s.flags = st.flags;
     if (MODE != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
   }
@@ -729,9 +763,11 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   if constexpr (MODE == kModePasses) {
     for (; p < a.n_passes; ++p) {
       const uint32_t plan_p = s_plans[p];
-      for (int c0 = 0; c0 < J; c0 += G::JC) {
-        T X[G::JC][4];
-        run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+      if (compute) {
+        for (int c0 = 0; c0 < J; c0 += G::JC) {
+          T X[G::JC][4];
+          run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+        }
       }
       __syncthreads();
       cur_off ^= FLIP;
@@ -744,7 +780,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     // elements [0, TMA_ELEMS); 4-blocks from TAIL_B on go through registers
     constexpr int TMA_ELEMS = ((N - 1) / kTmaBox) * kTmaBox;
     constexpr int TAIL_B = TMA_ELEMS / 4;
-    constexpr bool TMA_GEOM = MODE == kModeFill && FAST && TMA_ELEMS > 0 && TAIL_B % 32 == 0;
+    constexpr bool TMA_GEOM = MODE == kModeFill && FAST && !G::LAT && TMA_ELEMS > 0 && TAIL_B % 32 == 0;
     // groups of the last warp at or past TAIL_B (the tail is in the last warp)
     constexpr int TAIL_J = TMA_GEOM ? (TAIL_B - (G::NW - 1) * J * 32) / 32 : 0;
     static_assert(!TMA_GEOM || (TAIL_J >= 0 && TAIL_J < J), "tail must sit in the last warp");
@@ -776,7 +812,15 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         bool zero_seen = false;
         T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
         T x_last = T(0);
-        for (int c0 = 0; c0 < J; c0 += G::JC) {
+        if (G::CHAINW && do_emit && compute) {
+          // S/r/scale of emission e come from the chain warp: one lane per
+          // warp polls (acquire), __syncwarp orders the other lanes' reads
+          if (lane == 0)
+            while (ld_acquire_cta(&s.ready) < e) __nanosleep(32);
+          __syncwarp();
+          sc = from_double<T>(*static_cast<volatile double*>(&s.scale[slot]));
+        }
+        for (int c0 = 0; c0 < J && compute; c0 += G::JC) {
           T X[G::JC][4];
           run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
           if (do_emit) {
@@ -801,7 +845,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           fence_proxy_async_smem();  // this thread's pool stores -> visible to the bulk copies
           if (zero_seen) s.zero_seen = 1;
         }
-        if (do_emit && tid == G::OWNER && WB_ABLATE != 3) {
+        if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3) {
           chain_close(s, slot, static_cast<double>(x_last));
           if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
         }
@@ -816,6 +860,13 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         __syncthreads();
         cur_off ^= FLIP;
         T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+        if (G::CHAINW && fast && tid == G::CT) {
+          // generator.cpp:373-375 for emission e, then S/r/scale of e+1; the
+          // compute warps pick them up at emission e+1 (acquire on s.ready)
+          chain_close(s, slot, static_cast<double>(cur[N - 1]));
+          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+          st_release_cta(&s.ready, e + 1);
+        }
         if (bulk) {
           if (tid == 0) {
             const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
@@ -853,6 +904,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         }
 #endif
         if (renorm_now) {
+          if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
           renormalize<T, N, THREADS>(cur, s, tid);
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
           if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
@@ -870,6 +922,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           if (tid == 0) {
             chain_close(s, slot, static_cast<double>(cur[N - 1]));
             if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+            s.ready = e + 1;
           }
           __syncthreads();
         }
@@ -877,6 +930,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       }
     }
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
+    if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
   }
 #if WB_ABLATE == 4
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1132,6 +1186,16 @@ cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream
 template <typename T>
 cudaError_t launch_pool_dispatch(int log2n, const FillArgs& a, uint64_t n_pools, cudaStream_t s) {
   switch (log2n) {
+    // latency kernels (key log2(N) + 16)
+    case 16 + 8: return launch_pool<T, 16 + 8>(a, n_pools, s);
+    case 16 + 9: return launch_pool<T, 16 + 9>(a, n_pools, s);
+    case 16 + 10: return launch_pool<T, 16 + 10>(a, n_pools, s);
+    case 16 + 11: return launch_pool<T, 16 + 11>(a, n_pools, s);
+    case 16 + 12: return launch_pool<T, 16 + 12>(a, n_pools, s);
+    case 16 + 13: return launch_pool<T, 16 + 13>(a, n_pools, s);
+    case 16 + 14:
+      if constexpr (sizeof(T) == 4) return launch_pool<T, 16 + 14>(a, n_pools, s);
+      else return cudaErrorInvalidValue;
     case 5: return launch_pool<T, 5>(a, n_pools, s);
     case 6: return launch_pool<T, 6>(a, n_pools, s);
     case 7: return launch_pool<T, 7>(a, n_pools, s);

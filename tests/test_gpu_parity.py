@@ -61,29 +61,33 @@ CONFIGS = [
 ]
 
 
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("kw", CONFIGS, ids=lambda k: "_".join(f"{a}{b}" for a, b in k.items()))
-def test_fill_matches_oracle(cuda, dtype, kw):
+def test_fill_matches_oracle(cuda, dtype, kw, kernel):
     if dtype == "f64" and kw["pool_size"] > 8192:
         pytest.skip("f64 on-chip limit")
     n = kw["pool_size"]
     seeds = [11, 12, 1013]
     count = 3 * n + 5  # several emissions, misaligned pool-major stride
     b = pb.PoolBatch(gcfg(**kw), n_pools=len(seeds), seeds=seeds, dtype=dtype)
+    b.set_kernel_mode(kernel)
     out = b.fill(count).cpu().numpy()
     for p, s in enumerate(seeds):
         want = OracleGen(ocfg(seed=s, **kw), dtype).fill(count)
         assert_same(out[p], want, f"pool {p} seed {s}")
 
 
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_chunked_fill_and_api_sequence(cuda, dtype):
+def test_chunked_fill_and_api_sequence(cuda, dtype, kernel):
     """fill(5), fill(5), ... carry the partial emission across calls
     (generator.cpp:387-399); step_pass / next_pool / inject_pool interleave
     (generator.cpp:333-343, 401-413)."""
     kw = dict(pool_size=64, discard_every=2, out_mean=5.0, out_sigma=2.0)
     seeds = [21, 22]
     b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=seeds, dtype=dtype)
+    b.set_kernel_mode(kernel)
     o = [OracleGen(ocfg(seed=s, **kw), dtype) for s in seeds]
     for k in (5, 5, 200, 63, 1, 126, 127):
         got = b.fill(k).cpu().numpy()
@@ -115,13 +119,15 @@ def test_chunked_fill_and_api_sequence(cuda, dtype):
         assert info["buffered"] == st["buffered"]
 
 
-def test_renormalisation_crossings(cuda):
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
+def test_renormalisation_crossings(cuda, kernel):
     """Config-1 shape: 1024 values per pass, renormalised every 256 passes
     (generator.cpp:342, 345-351); 2^18 values cross the boundary once per
     256 emissions."""
     kw = dict(pool_size=1024, discard_every=1)
     for dtype in ("f64", "f32"):
         b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=[1, 2], dtype=dtype)
+        b.set_kernel_mode(kernel)
         out = b.fill(1 << 18).cpu().numpy()
         for p, s in enumerate([1, 2]):
             g = OracleGen(ocfg(seed=s, **kw), dtype)
