@@ -306,30 +306,63 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
 }
 
 // generator.cpp:20-34 recompute_sum_sq — sequential Neumaier, one thread.
-template <typename T>
+// SELECT: branch-free form — the reference's two branches are the same
+// expression with the operands ordered by magnitude, (big - t) + small, so
+// only the running sum's 8-cycle DADD dependency is on the critical path
+// (used by the latency kernel, where the renormalisation is on the critical
+// path; the throughput kernel keeps the compact form for register pressure).
+template <bool SELECT>
+__device__ __forceinline__ void neumaier_add(double& sum, double& comp, double x) {
+  const double term = __dmul_rn(x, x);
+  const double t = __dadd_rn(sum, term);
+  if constexpr (SELECT) {
+    const bool sum_big = fabs(sum) >= fabs(term);
+    const double big = sum_big ? sum : term;
+    const double small = sum_big ? term : sum;
+    comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(big, t), small));
+  } else if (fabs(sum) >= fabs(term)) {
+    comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(sum, t), term));
+  } else {
+    comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(term, t), sum));
+  }
+  sum = t;
+}
+template <typename T, bool VECTOR_LOADS>
 __device__ double neumaier_sq(const T* v, int n) {
   double sum = 0.0, comp = 0.0;
-#pragma unroll 8
-  for (int i = 0; i < n; ++i) {
-    const double x = static_cast<double>(v[i]);
-    const double term = __dmul_rn(x, x);
-    const double t = __dadd_rn(sum, term);
-    if (fabs(sum) >= fabs(term)) {
-      comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(sum, t), term));
-    } else {
-      comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(term, t), sum));
+  if constexpr (VECTOR_LOADS && sizeof(T) == 4) {
+    const float4* q = reinterpret_cast<const float4*>(v);
+#pragma unroll 4
+    for (int i = 0; i < n / 4; ++i) {
+      const float4 f = q[i];
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.x);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.y);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.z);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.w);
     }
-    sum = t;
+  } else if constexpr (VECTOR_LOADS) {
+    const double2* q = reinterpret_cast<const double2*>(v);
+#pragma unroll 4
+    for (int i = 0; i < n / 2; ++i) {
+      const double2 f = q[i];
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.x);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.y);
+    }
+  } else {
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) neumaier_add<false>(sum, comp, static_cast<double>(v[i]));
   }
   return __dadd_rn(sum, comp);
 }
 
 // generator.cpp:345-351 renormalize_.  Contains block barriers: call from
 // all threads.
-template <typename T, int N, int THREADS>
-__device__ void renormalize(T* cur, SState& s, int tid) {
+// LAT: the latency kernel (one pool per SM, the renormalisation is on the
+// critical path: vector loads, out of line); otherwise inline scalar loads
+template <typename T, int N, int THREADS, bool LAT>
+__device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
   if (tid == 0) {
-    const double ss = neumaier_sq(cur, N);
+    const double ss = neumaier_sq<T, LAT>(cur, N);
     s.renorm_ok = ss > 0.0;
     s.renorm_k = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
   }
@@ -339,7 +372,7 @@ __device__ void renormalize(T* cur, SState& s, int tid) {
     for (int i = tid; i < N; i += THREADS)
       cur[i] = from_double<T>(__dmul_rn(static_cast<double>(cur[i]), k));
     __syncthreads();
-    if (tid == 0) s.sum_sq = neumaier_sq(cur, N);
+    if (tid == 0) s.sum_sq = neumaier_sq<T, LAT>(cur, N);
   }
   __syncthreads();
 }
@@ -771,7 +804,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       }
       __syncthreads();
       cur_off ^= FLIP;
-      if (pc == 0) renormalize<T, N, THREADS>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
+      if (pc == 0) renormalize<T, N, THREADS, G::LAT>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
       pc = (pc + 1) & 255u;
     }
   } else {
@@ -905,7 +938,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
 #endif
         if (renorm_now) {
           if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
-          renormalize<T, N, THREADS>(cur, s, tid);
+          renormalize<T, N, THREADS, G::LAT>(cur, s, tid);
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
           if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
           __syncthreads();
