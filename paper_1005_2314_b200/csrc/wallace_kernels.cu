@@ -92,6 +92,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_CHAINW
 #define WB_CHAINW 0
 #endif
+// ABLATION builds only: consumer without histogram (1) / moments (2) / both (3)
+#ifndef WB_CONS_ABLATE
+#define WB_CONS_ABLATE 0
+#endif
 #ifndef WB_REGS_PP
 #define WB_REGS_PP 80
 #endif
@@ -382,28 +386,37 @@ __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
 // ---------------------------------------------------------------------------
 template <typename T>
 struct Consumer {
-  double s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+  double s1 = 0, s2 = 0, s3 = 0, s4 = 0;  // per-thread totals (fp64)
+  T a1 = 0, a2 = 0, a3 = 0, a4 = 0;       // per-emission partials (T)
   uint32_t* hist;  // shared, 258 bins (under, 256, over)
-  __device__ __forceinline__ void add_group(const T* y, int n) {
-    T a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < n) {
-        const T x = y[k];
-        const T x2 = mul_rn(x, x);
-        a1 = add_rn(a1, x);
-        a2 = add_rn(a2, x2);
-        a3 = add_rn(a3, mul_rn(x2, x));
-        a4 = add_rn(a4, mul_rn(x2, x2));
-        const T t = mul_rn(add_rn(x, T(8)), T(16));
-        const int bin = t < T(0) ? -1 : (t >= T(256) ? 256 : static_cast<int>(t));
-        atomicAdd(&hist[bin + 1], 1u);
-      }
+  __device__ __forceinline__ void add(T x) {
+    if (WB_CONS_ABLATE != 2 && WB_CONS_ABLATE != 3) {
+      const T x2 = mul_rn(x, x);
+      a1 = add_rn(a1, x);
+      a2 = add_rn(a2, x2);
+      a3 = fma_rn(x2, x, a3);
+      a4 = fma_rn(x2, x2, a4);
     }
+    if (WB_CONS_ABLATE != 1 && WB_CONS_ABLATE != 3) {
+      // bin = floor((x + 8) * 16) in T, clamped to [-1, 256] (under / over)
+      const T t = mul_rn(add_rn(x, T(8)), T(16));
+      int bin = sizeof(T) == 4 ? __float2int_rd(static_cast<float>(t)) : __double2int_rd(static_cast<double>(t));
+      bin = max(-1, min(bin, 256));
+      atomicAdd(&hist[bin + 1], 1u);
+    }
+  }
+  __device__ __forceinline__ void add_group(const T* y, int n) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < n) add(y[k]);
+  }
+  // fold the per-emission partials into the fp64 totals
+  __device__ __forceinline__ void flush() {
     s1 += static_cast<double>(a1);
     s2 += static_cast<double>(a2);
     s3 += static_cast<double>(a3);
     s4 += static_cast<double>(a4);
+    a1 = a2 = a3 = a4 = T(0);
   }
 };
 
@@ -701,12 +714,12 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
 
 // Emission of the values already in registers (fast path) into the fused
 // consumer instead of memory.
-template <typename T, int LOG2N>
-__device__ __forceinline__ void consume_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], Consumer<T>& cons,
-                                              T sc, T mean, bool mz, uint32_t b0c) {
+template <typename T, int LOG2N, int JCL>
+__device__ __forceinline__ void consume_chunk(const T (&X)[JCL][4], Consumer<T>& cons, T sc, T mean,
+                                              bool mz, uint32_t b0c) {
   using G = Geo<T, LOG2N>;
 #pragma unroll
-  for (int j = 0; j < G::JC; ++j) {
+  for (int j = 0; j < JCL; ++j) {
     const uint32_t b = b0c + 32 * j;
     T y[4];
 #pragma unroll
@@ -783,9 +796,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     for (uint32_t i = tid; i < a.lead; i += THREADS) {
       const uint32_t idx = cursor0 + i;
       const T v = mat ? lo[idx] : emit_value(pools[idx], sc, mean_t, mean_zero);
-      if constexpr (MODE == kModeConsume) cons.add_group(&v, 1);
+      if constexpr (MODE == kModeConsume) cons.add(v);
       else stg1(out_pool + i, v);
     }
+    if constexpr (MODE == kModeConsume) cons.flush();
   }
 
   const char* const cbase = reinterpret_cast<const char*>(pbase);
@@ -853,9 +867,13 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           __syncwarp();
           sc = from_double<T>(*static_cast<volatile double*>(&s.scale[slot]));
         }
-        for (int c0 = 0; c0 < J && compute; c0 += G::JC) {
-          T X[G::JC][4];
-          run_pass<T, LOG2N, G::JC>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+        // chunk of 4-blocks held in registers at a time (half chunks for the
+        // consumer remove its spills but cost a second permutation dispatch
+        // per pass: measured slower)
+        constexpr int JCL = G::JC;
+        for (int c0 = 0; c0 < J && compute; c0 += JCL) {
+          T X[JCL][4];
+          run_pass<T, LOG2N, JCL>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
           if (do_emit) {
             if constexpr (MODE == kModeFill) {
               if (bulk) {
@@ -869,11 +887,13 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
                 emit_chunk_any<T, LOG2N>(delta, mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
               }
             } else {
-              consume_chunk<T, LOG2N>(X, cons, sc, mean_t, mean_zero, b0 + 32 * c0);
+              consume_chunk<T, LOG2N, JCL>(X, cons, sc, mean_t, mean_zero, b0 + 32 * c0);
             }
           }
-          x_last = X[G::JC - 1][3];
+          x_last = X[JCL - 1][3];
         }
+        if constexpr (MODE == kModeConsume)
+          if (do_emit) cons.flush();
         if (bulk) {
           fence_proxy_async_smem();  // this thread's pool stores -> visible to the bulk copies
           if (zero_seen) s.zero_seen = 1;
@@ -949,9 +969,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           const T sc = from_double<T>(s.scale[slot]);
           for (uint32_t i = tid; i < limit; i += THREADS) {
             const T v = emit_value(cur[i], sc, mean_t, mean_zero);
-            if constexpr (MODE == kModeConsume) cons.add_group(&v, 1);
+            if constexpr (MODE == kModeConsume) cons.add(v);
             else stg1(gbase + i, v);
           }
+          if constexpr (MODE == kModeConsume) cons.flush();
           if (tid == 0) {
             chain_close(s, slot, static_cast<double>(cur[N - 1]));
             if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
@@ -1166,7 +1187,9 @@ __global__ void __launch_bounds__(128)
       sincospif(2.0f * static_cast<float>(u[1]), &sn, &cs);
       const float z[2] = {r * cs, r * sn};
       cons.add_group(z, (i + 1 < count) ? 2 : 1);
+      if ((i & 127) == 126) cons.flush();  // fp32 partials over <= 128 values
     }
+    cons.flush();
   }
   double v[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
 #pragma unroll

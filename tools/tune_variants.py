@@ -22,8 +22,10 @@ for lib in libs:
                             "--no-e2e", "--no-cpu"], cwd=ROOT, env=env, capture_output=True, text=True)
         try:
             d = json.loads(r.stdout.strip().splitlines()[-1])
+            frac = (d.get("roofline") or {}).get("frac")
             print(f"{name:24s} cfg{c} parity={'ok' if ok else 'FAIL'} ms={d['ms_per_step']:.3f} "
-                  f"frac={d['roofline']['frac']:.3f} sm_mhz={d['clocks']['sm_mhz']}", flush=True)
+                  f"frac={frac if frac is None else round(frac, 3)} sm_mhz={d['clocks']['sm_mhz']}",
+                  flush=True)
         except Exception:  # noqa: BLE001
             print(f"{name:24s} cfg{c} parity={'ok' if ok else 'FAIL'} bench failed: {r.stderr[-300:]}",
                   flush=True)
