@@ -269,6 +269,16 @@ def run_ours(args):
 
     # end to end through the C-ABI into pinned host memory
     e2e = None
+    if rank == 0 and consume and not args.no_e2e:
+        # the consumer's result (4 sums + 258 counts) is its only output
+        e2e_steps = max(1, min(args.e2e_steps, args.steps))
+        t1 = time.perf_counter()
+        for _ in range(e2e_steps):
+            batch.consume_from_snapshot(count)
+        dt = (time.perf_counter() - t1) / e2e_steps
+        e2e = {"value": variates_rank / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": 4 * 8 + 258 * 8,
+               "api": "wallace_consume_from_snapshot (C-ABI), wall clock", "s_per_step": dt}
     if rank == 0 and not consume and not args.no_e2e:
         try:
             host = torch.empty((n_pools, count), dtype=batch.torch_dtype, pin_memory=True)
@@ -285,6 +295,36 @@ def run_ours(args):
             del host
         except Exception as ex:  # noqa: BLE001
             e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+
+    comparator = None
+    if consume and rank == 0:
+        # BASELINE config 5: the same statistics from a Box-Muller kernel fed
+        # by the same per-pool uniform streams (baselines.cpp:80-92)
+        import math
+        sums, hist = batch.consume_from_snapshot(count)
+        n = n_pools * count
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        bsums, bhist = pb.boxmuller_consume(n_streams=n_pools, count=count, seeds=seeds)
+        bm_s = time.perf_counter() - t1
+
+        def zs(sm):
+            return {k: round(v[3], 3) for k, v in pb.moment_reports(sm, n).items()}
+
+        def hist_z(h):
+            edges = np.arange(257) / 16.0 - 8.0
+            cdf = np.array([0.5 * math.erfc(-e / math.sqrt(2)) for e in edges])
+            expect = n * np.diff(cdf)
+            ok = expect > 50
+            chi2 = float(np.sum((h[1:257][ok].astype(np.float64) - expect[ok]) ** 2 / expect[ok]))
+            dof = int(ok.sum()) - 1
+            return round((chi2 - dof) / math.sqrt(2 * dof), 3)
+
+        comparator = {"wallace": {"variates_per_s": value, "moment_z": zs(sums), "hist_chi2_z": hist_z(hist)},
+                      "boxmuller": {"variates_per_s": n / bm_s, "moment_z": zs(bsums),
+                                    "hist_chi2_z": hist_z(bhist),
+                                    "note": "fp32 transcendentals, same UniformState(seed) streams, "
+                                            "wall clock incl. launch and 2 KB D2H"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -311,6 +351,7 @@ def run_ours(args):
                        "l2": "output per step (16 GiB for cfg2) >> 126 MB L2; no flush needed",
                        "step": "replay of the seeded job from the device snapshot"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            **({"comparator": comparator} if comparator else {}),
             "clocks": clk.summary(), "gpu_launches": launches,
             "init_s": init_s,
         }
