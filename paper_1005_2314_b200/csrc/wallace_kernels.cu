@@ -80,6 +80,7 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #define WB_D2_STG64 0
 #endif
 // 1: bulk (TMA) emission when the emission is the pool itself (scale 1, mean +0)
+// and starts 16-byte aligned
 #ifndef WB_TMA
 #define WB_TMA 0
 #endif
@@ -855,7 +856,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
                   (G::VEC - 1);
         }
         // the pool itself is the emission: bulk stores from shared memory
-        const bool bulk = TMA_GEOM && WB_TMA && do_emit && a.tma_ok && mean_zero && sc == T(1);
+        // (tensor stores need 16-byte-aligned coordinates: only emissions that
+        // start aligned, delta == 0, go out this way)
+        const bool bulk = TMA_GEOM && WB_TMA && do_emit && a.tma_ok && mean_zero && sc == T(1) && delta == 0;
         bool zero_seen = false;
         T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
         T x_last = T(0);
