@@ -261,11 +261,24 @@ def run_ours(args):
     if not consume:
         achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
         tr = ncu_traffic(args.config)
+        # The path only writes HBM, so also time a store-only pass over the same
+        # output buffer on this box (torch's vectorised fill; tools/probes/
+        # store_peak.cu measured 6816 GB/s for 128-bit streaming stores).
+        fills = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out.fill_(0.5)
+            b.record(stream)
+            b.synchronize()
+            fills.append(a.elapsed_time(b))
+        store_gbs = out.numel() * out.element_size() / (min(fills) / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
                     "kernel": "pool_kernel", "kernel_ms": per_launch_ms,
                     "kernel_share_of_step": pool_ms.value / max(1e-9, pool_ms.value + plan_ms.value),
-                    "algorithmic_bytes_per_launch": alg_bytes}
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "store_only_peak": store_gbs, "frac_of_store_only_peak": achieved / store_gbs}
 
     # end to end through the C-ABI into pinned host memory
     e2e = None

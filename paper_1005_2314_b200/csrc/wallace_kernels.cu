@@ -79,6 +79,17 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_D2_STG64
 #define WB_D2_STG64 0
 #endif
+// 1: fp32 emissions shifted by 3 store [4b-1, 4b+3) (one shuffle per block)
+// instead of [4b+3, 4b+7) (three shuffles)
+#ifndef WB_D3_DOWN
+#define WB_D3_DOWN 1
+#endif
+// packed f32x2 ops for fp32 (measured slower on cfg2: 3.754-3.778 vs 3.731 ms,
+// FFMA2 latency lengthens each pass): bit 0 the butterfly and row factors, bit 1 the
+// mean-zero emission scaling
+#ifndef WB_PACKED
+#define WB_PACKED 0
+#endif
 // 1: bulk (TMA) emission when the emission is the pool itself (scale 1, mean +0)
 // and starts 16-byte aligned
 #ifndef WB_TMA
@@ -183,6 +194,52 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 template <typename T> __device__ __forceinline__ T from_double(double x);
 template <> __device__ __forceinline__ float from_double<float>(double x) { return __double2float_rn(x); }
 template <> __device__ __forceinline__ double from_double<double>(double x) { return x; }
+
+// Packed fp32 pairs (sm_100 FADD2/FMUL2/FFMA2): two independently rounded
+// lanes per instruction.  fma(x, +-1, y) is exactly the sum y +- x (the
+// product is exact), including the sign of a zero result, so the butterfly
+// below is bit-identical to the scalar add_rn/sub_rn form.  ptxas folds the
+// lane broadcasts, swaps and per-lane negations of pk2() into operand
+// modifiers.
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2_rn(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2_rn(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Second butterfly stage for output pair (S0, S1) of a permutation, times
+// the two row factors h = (h0, h1):
+//   z0 = a - d = fma(d, -1, a)     z1 = b + c = fma(c, 1, b)
+//   z2 = b - c = fma(c, -1, b)     z3 = (-a) - d = fma(d, -1, -a)
+// (transforms.hpp:89-103 op order).  The pair {z0, z3} shares a, so it uses
+// z0 = fma(a, 1, -d), z3 = fma(a, -1, -d): one broadcast per operand.
+template <int S0, int S1>
+__device__ __forceinline__ void wallace_pair(float a, float b, float c, float d, uint64_t h, float& o0,
+                                             float& o1) {
+  uint64_t z;
+  if constexpr ((S0 == 0 && S1 == 3) || (S0 == 3 && S1 == 0)) {
+    z = fma2_rn(pk2(a, a), pk2(S0 == 0 ? 1.f : -1.f, S1 == 0 ? 1.f : -1.f), pk2(-d, -d));
+  } else {
+    auto m = [&](int s) { return (s == 1 || s == 2) ? c : d; };
+    auto k = [](int s) { return s == 1 ? 1.f : -1.f; };
+    auto ad = [&](int s) { return s == 0 ? a : s == 3 ? -a : b; };
+    z = fma2_rn(pk2(m(S0), m(S1)), pk2(k(S0), k(S1)), pk2(ad(S0), ad(S1)));
+  }
+  upk2(mul2_rn(z, h), o0, o1);
+}
 
 // out = x * scale + mean with two roundings (generator.cpp:366-368).  When
 // mean is +0.0, fma(x, scale, +0) rounds x*scale once and adds +0 exactly,
@@ -465,8 +522,17 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
     if (j < jfirst) continue;  // groups before jfirst are emitted elsewhere
     const uint32_t b = b0 + 32 * j;
     T y[4];
+    if constexpr ((WB_PACKED & 2) && MZ && sizeof(T) == 4) {
+      // (only the mean-zero form: ptxas contracts a packed mul.rn + add.rn
+      // pair into one FFMA2 despite the explicit rounding modifiers)
+      const uint64_t s2 = pk2(sc, sc);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
+      for (int h = 0; h < 4; h += 2)
+        upk2(fma2_rn(pk2(X[jj][h], X[jj][h + 1]), s2, pk2(0.f, 0.f)), y[h], y[h + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
+    }
     if constexpr (WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
       // global(4b) is 8-byte aligned: two float2 stores of the own block,
       // no neighbour values needed
@@ -477,6 +543,23 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         __stcs(reinterpret_cast<float2*>(gbase + 4 * b), make_float2(y[0], y[1]));
         stg1(gbase + 4 * b + 2, y[2]);
       }
+    } else if constexpr (WB_D3_DOWN && VEC == 4 && DELTA == 3) {
+      // shift the other way: the aligned chunk [4b-1, 4b+3) is the previous
+      // block's last value (lane-1, or for lane 0 lane 31 of group j-1, kept
+      // in prev[0]) and this block's first three -- one shuffle, and the
+      // pool's last element X[N-1] = y[3] of block ROWS-1 falls outside
+      const T s = __shfl_sync(0xffffffffu, y[3], (lane + 31) & 31);
+      if (lane == 0 && j == jfirst) {  // head of this warp: the value before is the previous warp's
+        stg1(gbase + 4 * b + 0, y[0]);
+        stg1(gbase + 4 * b + 1, y[1]);
+        stg1(gbase + 4 * b + 2, y[2]);
+      } else {
+        const T c[4] = {lane == 0 ? prev[0] : s, y[0], y[1], y[2]};
+        stg_vec(gbase + 4 * b - 1, c);
+      }
+      if (lane == 31 && j == J - 1 && 4 * b + 3 < uint32_t(G::N - 1))
+        stg1(gbase + 4 * b + 3, y[3]);  // tail of this warp: the next warp's head is scalar
+      prev[0] = s;
     } else if constexpr (DELTA == 0) {
       if (b != G::ROWS - 1) {
         if constexpr (WB_EMIT_IMM) {
@@ -521,7 +604,8 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       for (int k = 0; k < 4; ++k) prev[k] = y[k];
     }
   }
-  if constexpr (DELTA > 0 && !(WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2)) {
+  if constexpr (DELTA > 0 && !(WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) &&
+                !(WB_D3_DOWN && VEC == 4 && DELTA == 3)) {
     if (l31 && c0 + JC == J) {  // last group of the warp: own tail only, the head is the next warp's
       const uint32_t b = (warp * J + J - 1) * 32 + 31;
 #pragma unroll
@@ -643,6 +727,56 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
   }
   // byte offset of row r_j = (off + b_j*STRIDE) mod ROWS, b_j = b0 + 32j
   const uint32_t r0 = (b0 * G::STRIDE + off) * sizeof(T);
+
+  if constexpr ((WB_PACKED & 1) && sizeof(T) == 4) {
+    // gather + first butterfly stage as two packed ops per 4-block:
+    // (a, b) = (v0 + v1, v0 - v1), (c, d) = (v2 + v3, v2 - v3)
+    float ab[J][2], cd[J][2];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      float v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+      if (ROWS >= 32 || b0 + 32 * j < ROWS) {
+        constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
+        const float* row = reinterpret_cast<const float*>(base + (((r0 + j * step) & MASK4) | cur_off));
+        v0 = row[0];
+        v1 = row[ROWS];
+        v2 = row[2 * ROWS];
+        v3 = row[3 * ROWS];
+      }
+      const uint64_t pm = pk2(1.f, -1.f);
+      upk2(fma2_rn(pk2(v1, v1), pm, pk2(v0, v0)), ab[j][0], ab[j][1]);
+      upk2(fma2_rn(pk2(v3, v3), pm, pk2(v2, v2)), cd[j][0], cd[j][1]);
+    }
+    const uint64_t h01 = pk2(float(hs[0]), float(hs[1]));
+    const uint64_t h23 = pk2(float(hs[2]), float(hs[3]));
+    float (&Xf)[J][4] = reinterpret_cast<float (&)[J][4]>(X);
+    switch (perm) {
+#define WB_PERM_CASE(P)                                                                              \
+  case P:                                                                                            \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {                                                  \
+      wallace_pair<PermAt<P, 0>::v, PermAt<P, 1>::v>(ab[j][0], ab[j][1], cd[j][0], cd[j][1], h01,    \
+                                                      Xf[j][0], Xf[j][1]);                           \
+      wallace_pair<PermAt<P, 2>::v, PermAt<P, 3>::v>(ab[j][0], ab[j][1], cd[j][0], cd[j][1], h23,    \
+                                                      Xf[j][2], Xf[j][3]);                           \
+    }                                                                                                \
+    break;
+      WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
+      WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
+      WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
+      WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
+      WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22) WB_PERM_CASE(23)
+      default: __builtin_unreachable();
+#undef WB_PERM_CASE
+    }
+    if constexpr (G::INPLACE) __syncthreads();
+    float* nb = reinterpret_cast<float*>(const_cast<char*>(base) + nxt_off);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) sts4(nb + 4 * b, Xf[j][0], Xf[j][1], Xf[j][2], Xf[j][3]);
+    }
+    return;
+  }
 
   // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
   T z[J][4];
