@@ -56,9 +56,12 @@ class Cfg:
     seed: int = 0
     fixed_transform: bool = False
     disable_chi2: bool = False
+    transform_family: int = 0  # 0 wallace4, 1 rotation
+    mixing: int = 0  # 0 stride_transpose, 1 affine
 
     def wo(self) -> WoConfig:
-        return WoConfig(self.pool_size, 0, 0, self.chi2_method, int(self.fixed_transform),
+        return WoConfig(self.pool_size, self.transform_family, self.mixing, self.chi2_method,
+                        int(self.fixed_transform),
                         int(self.disable_chi2), 0, self.discard_every, self.out_mean,
                         self.out_sigma, self.seed)
 
@@ -95,6 +98,12 @@ def oracle_lib():
         L.wo_default_stride.argtypes = [u64]
         L.wo_default_stride.restype = u64
         L.wo_wallace_variant.argtypes = [C.c_int, P(C.c_int), P(f64)]
+        L.wo_default_multipliers.argtypes = [u64, P(u64), P(u64)]
+        L.wo_default_multipliers.restype = None
+        L.wo_rotation_t.argtypes = [C.c_int]
+        L.wo_rotation_t.restype = f64
+        L.wo_rotation_from_t.argtypes = [f64, P(f64), P(f64)]
+        L.wo_rotation_from_t.restype = None
         L.wo_compute_a.argtypes = [u64]
         L.wo_compute_a.restype = f64
         L.wo_chi2_sample.argtypes = [f64, u64, f64, C.c_int, P(C.c_int)]
@@ -116,6 +125,13 @@ def ref_lib():
         L = C.CDLL(REF_SO)
         L.ref_create.argtypes = [u64, C.c_int, u64, f64, f64, u64, C.c_int, C.c_int]
         L.ref_create.restype = vp
+        L.ref_create_ex.argtypes = [u64, C.c_int, u64, f64, f64, u64, C.c_int, C.c_int, C.c_int,
+                                    C.c_int]
+        L.ref_create_ex.restype = vp
+        L.ref_rotation_table.argtypes = [P(f64), P(f64), P(f64)]
+        L.ref_rotation_table.restype = None
+        L.ref_default_multipliers.argtypes = [u64, P(u64), P(u64)]
+        L.ref_default_multipliers.restype = None
         L.ref_last_error.restype = C.c_char_p
         L.ref_destroy.argtypes = [vp]
         L.ref_fill.argtypes = [vp, P(f64), u64]
@@ -209,9 +225,9 @@ class RefGen:
     def __init__(self, cfg: Cfg):
         self.L = ref_lib()
         self.cfg = cfg
-        h = self.L.ref_create(cfg.pool_size, cfg.chi2_method, cfg.discard_every, cfg.out_mean,
-                              cfg.out_sigma, cfg.seed, int(cfg.fixed_transform),
-                              int(cfg.disable_chi2))
+        h = self.L.ref_create_ex(cfg.pool_size, cfg.chi2_method, cfg.discard_every, cfg.out_mean,
+                                 cfg.out_sigma, cfg.seed, int(cfg.fixed_transform),
+                                 int(cfg.disable_chi2), cfg.transform_family, cfg.mixing)
         if not h:
             raise ValueError(self.L.ref_last_error().decode())
         self.h = h

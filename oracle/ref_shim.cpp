@@ -28,9 +28,12 @@ thread_local std::string g_err;
 maxent::GeneratorConfig to_cfg(uint64_t pool_size, int chi2_method,
                                uint64_t discard_every, double mean,
                                double sigma, uint64_t seed, int fixed,
-                               int disable_chi2) {
+                               int disable_chi2, int family = 0,
+                               int mixing = 0) {
   maxent::GeneratorConfig c;
   c.pool_size = pool_size;
+  c.transform_family = static_cast<maxent::TransformFamily>(family);
+  c.mixing = static_cast<maxent::MixingScheme>(mixing);
   c.chi2_method = static_cast<maxent::Chi2Method>(chi2_method);
   c.discard_every = discard_every;
   c.out_mean = mean;
@@ -57,6 +60,35 @@ void* ref_create(uint64_t pool_size, int chi2_method, uint64_t discard_every,
     g_err = e.what();
     return nullptr;
   }
+}
+
+void* ref_create_ex(uint64_t pool_size, int chi2_method, uint64_t discard_every,
+                    double mean, double sigma, uint64_t seed, int fixed,
+                    int disable_chi2, int family, int mixing) {
+  try {
+    return new maxent::Generator(to_cfg(pool_size, chi2_method, discard_every,
+                                        mean, sigma, seed, fixed, disable_chi2,
+                                        family, mixing));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_rotation_table(double* t16, double* c16, double* s16) {
+  const auto tab = maxent::rotation_t_table();
+  for (size_t k = 0; k < tab.size() && k < 16; ++k) {
+    const auto rc = maxent::rotation_from_t(tab[k]);
+    t16[k] = rc.t;
+    c16[k] = rc.c;
+    s16[k] = rc.s;
+  }
+}
+
+void ref_default_multipliers(uint64_t n, uint64_t* alpha, uint64_t* beta) {
+  const auto ab = maxent::default_multipliers(n);
+  *alpha = ab.first;
+  *beta = ab.second;
 }
 
 void ref_destroy(void* g) { delete static_cast<maxent::Generator*>(g); }

@@ -18,6 +18,9 @@ struct wo_gen {
   void* raw;
   void* scratch;
   void* out;
+  void* tmp; /* rotation: the sweep-0 result */
+  uint64_t alpha, beta; /* affine multipliers (generator.cpp:286-294) */
+  double rot_c[16], rot_s[16]; /* rotation_from_t of the 16 table entries */
   uint64_t out_len;
   uint64_t cursor;
   uint64_t u[4];
@@ -177,6 +180,38 @@ double wo_chi2_sample(double x, uint64_t nu_i, double a, int method, int* clampe
   return s;
 }
 
+/* generator.cpp:286-294 default_multipliers */
+void wo_default_multipliers(uint64_t n, uint64_t* alpha, uint64_t* beta) {
+  uint64_t a = (uint64_t)llround(0.382 * (double)n) | 1;
+  uint64_t b = (uint64_t)llround(0.618 * (double)n) | 1;
+  if (a == b) b += 2;
+  *alpha = a;
+  *beta = b;
+}
+
+/* transforms.cpp:39-50: half-angle tangents of 16 angles evenly spaced over
+ * the window where cos and sin both lie in [0.05, 0.95] -- the midpoints of
+ * 16 equal slices of [acos(0.95), asin(0.95)] (bit-identical to the
+ * reference's table; pinned by tests/test_oracle_pin.py). */
+double wo_rotation_t(int k) {
+  const double lo = acos(0.95), hi = asin(0.95);
+  return tan((lo + (k + 0.5) * (hi - lo) / 16) / 2);
+}
+
+/* transforms.cpp:52-70 rotation_from_t (t finite) */
+void wo_rotation_from_t(double t, double* c, double* s) {
+  if (fabs(t) <= 1.0) {
+    const double den = 1.0 + t * t;
+    *c = (1.0 - t * t) / den;
+    *s = (2.0 * t) / den;
+  } else {
+    const double u = 1.0 / t;
+    const double den = 1.0 + u * u;
+    *c = (u * u - 1.0) / den;
+    *s = (2.0 * u) / den;
+  }
+}
+
 #define T double
 #define SFX _f64
 #include "oracle_gen.inc"
@@ -195,7 +230,7 @@ static int validate(const wo_config* c) {
   if (c->discard_every < 1) return -2;
   if (!isfinite(c->out_sigma) || c->out_sigma <= 0.0) return -3;
   if (!isfinite(c->out_mean)) return -4;
-  if (c->transform_family != 0 || c->mixing != 0) return -5;
+  if (c->transform_family < 0 || c->transform_family > 1 || c->mixing < 0 || c->mixing > 1) return -5;
   return 0;
 }
 
@@ -210,6 +245,9 @@ int wo_create(const wo_config* cfg, int dtype, wo_gen** out) {
   g->raw = malloc(cfg->pool_size * es);
   g->scratch = malloc(cfg->pool_size * es);
   g->out = malloc(cfg->pool_size * es);
+  g->tmp = malloc(cfg->pool_size * es);
+  wo_default_multipliers(cfg->pool_size, &g->alpha, &g->beta);
+  for (int k = 0; k < 16; ++k) wo_rotation_from_t(wo_rotation_t(k), &g->rot_c[k], &g->rot_s[k]);
   g->out_len = 0;
   g->cursor = 0;
   if (dtype) init_f64(g);
@@ -223,6 +261,7 @@ void wo_destroy(wo_gen* g) {
   free(g->raw);
   free(g->scratch);
   free(g->out);
+  free(g->tmp);
   free(g);
 }
 

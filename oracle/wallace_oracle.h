@@ -30,8 +30,8 @@ extern "C" {
 /* Mirrors maxent::GeneratorConfig (generator.hpp:21-45). */
 typedef struct wo_config {
   uint64_t pool_size;
-  int32_t transform_family; /* 0 = wallace4 (only family restated) */
-  int32_t mixing;           /* 0 = stride_transpose (only map restated) */
+  int32_t transform_family; /* 0 = wallace4, 1 = rotation */
+  int32_t mixing;           /* 0 = stride_transpose, 1 = affine */
   int32_t chi2_method;      /* 0 sqrt_shift, 1 wilson_hilferty, 2 cubic_a */
   int32_t fixed_transform;  /* diag.fixed_transform */
   int32_t disable_chi2;     /* diag.disable_chi2 */
@@ -54,6 +54,10 @@ double wo_uniform_next(uint64_t s[4]);
 uint64_t wo_default_stride(uint64_t rows);
 /* transforms.cpp:76-97: source_row[4] and row_sign[4] of a variant */
 void wo_wallace_variant(int id, int source_row[4], double row_sign[4]);
+/* generator.cpp:286-294; transforms.cpp:39-70 */
+void wo_default_multipliers(uint64_t n, uint64_t* alpha, uint64_t* beta);
+double wo_rotation_t(int k);
+void wo_rotation_from_t(double t, double* c, double* s);
 /* chi2.cpp:11-17, 27-59 */
 double wo_compute_a(uint64_t nu);
 double wo_chi2_sample(double x, uint64_t nu, double a, int method, int* clamped);

@@ -169,3 +169,77 @@ def test_oracle_f32_restatement_tracks_reference(ref):
         a = RefGen(c).fill(cnt)
         f = OracleGen(c, "f32").fill(cnt).astype(np.float64)
         assert np.max(np.abs(f - a)) <= 1e-4
+
+
+# ---- rotation family and affine mixing (generator.cpp:86-172) -------------------
+def test_rotation_table_and_multipliers_vs_reference(ref):
+    """The oracle computes the 16 half-angle tangents from their construction
+    (transforms.cpp:39-50) and default_multipliers (generator.cpp:286-294);
+    both must equal the reference's values bit for bit."""
+    import ctypes as C
+    L, R = oracle_lib(), ref.ref_lib()
+    t, c, s = (C.c_double * 16)(), (C.c_double * 16)(), (C.c_double * 16)()
+    R.ref_rotation_table(t, c, s)
+    for k in range(16):
+        assert L.wo_rotation_t(k) == t[k], k
+        oc, os_ = C.c_double(), C.c_double()
+        L.wo_rotation_from_t(t[k], C.byref(oc), C.byref(os_))
+        assert (oc.value, os_.value) == (c[k], s[k]), k
+    for n in [32, 64, 128, 256, 1024, 2048, 4096, 8192, 16384, 1 << 20]:
+        a1, b1, a2, b2 = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        R.ref_default_multipliers(n, C.byref(a1), C.byref(b1))
+        L.wo_default_multipliers(n, C.byref(a2), C.byref(b2))
+        assert (a1.value, b1.value) == (a2.value, b2.value), n
+
+
+FAMILY_CASES = [
+    # (family, mixing, pool_size, discard_every, chi2_method, disable_chi2, seed, count)
+    (0, 1, 1024, 1, 2, False, 3, 300000),   # wallace4 + affine, crosses a renormalisation
+    (0, 1, 4096, 2, 2, True, 1, 1 << 17),
+    (0, 1, 32, 2, 1, False, 8, 20000),
+    (1, 0, 1024, 1, 2, False, 1, 300000),   # rotation + stride_transpose
+    (1, 0, 2048, 3, 2, False, 7, 1 << 16),
+    (1, 0, 64, 1, 0, False, 5, 50000),
+    (1, 1, 1024, 2, 2, False, 11, 200000),  # rotation + affine
+    (1, 1, 4096, 1, 2, True, 2, 1 << 16),
+    (1, 1, 32, 3, 2, False, 4, 20000),
+]
+
+
+@pytest.mark.parametrize("case", FAMILY_CASES)
+def test_oracle_families_bit_exact_vs_reference(ref, case):
+    fam, mix, n, d, chi, dis, seed, cnt = case
+    c = Cfg(pool_size=n, discard_every=d, chi2_method=chi, disable_chi2=dis, seed=seed,
+            transform_family=fam, mixing=mix)
+    r, o = RefGen(c), OracleGen(c, "f64")
+    assert np.array_equal(r.fill(cnt).view(np.uint64), o.fill(cnt).view(np.uint64))
+    sr, so = r.stats(), o.stats()
+    for k in ("pass_count", "uniform_draws", "chi2_clamp_count", "sum_sq", "reserved_prev"):
+        assert sr[k] == so[k], k
+    assert np.array_equal(r.pool(), o.pool())
+
+
+@pytest.mark.parametrize("fam,mix", [(0, 1), (1, 0), (1, 1)])
+def test_oracle_families_fixed_transform_and_api(ref, fam, mix):
+    cf = Cfg(pool_size=128, seed=4, fixed_transform=True, transform_family=fam, mixing=mix)
+    assert np.array_equal(RefGen(cf).fill(5000), OracleGen(cf, "f64").fill(5000))
+    c = Cfg(pool_size=64, seed=21, out_mean=5.0, out_sigma=2.0, discard_every=2,
+            transform_family=fam, mixing=mix)
+    r, o = RefGen(c), OracleGen(c, "f64")
+    assert np.array_equal(r.fill(77), o.fill(77))
+    r.step_pass(); o.step_pass()
+    vr, rr, cr = r.next_pool()
+    vo, ro, co = o.next_pool()
+    assert np.array_equal(vr, vo) and rr == ro and cr == co
+    inj = np.linspace(-2, 2, 64)
+    r.inject_pool(inj); o.inject_pool(inj)
+    assert np.array_equal(r.fill(300), o.fill(300))
+
+
+@pytest.mark.parametrize("fam,mix", [(0, 1), (1, 0), (1, 1)])
+def test_oracle_families_f32_restatement_tracks_reference(ref, fam, mix):
+    """DESIGN.md §3 tolerance for the fp32 restatement, rotation/affine too."""
+    c = Cfg(pool_size=1024, discard_every=1, seed=1, transform_family=fam, mixing=mix)
+    a = RefGen(c).fill(1 << 19)
+    f = OracleGen(c, "f32").fill(1 << 19).astype(np.float64)
+    assert np.max(np.abs(f - a)) <= 1e-4
