@@ -46,9 +46,9 @@ typedef enum wallace_chi2_method {
   WALLACE_CHI2_CUBIC_A = 2
 } wallace_chi2_method;
 
-/* maxent::GeneratorConfig (generator.hpp:21-45).  transform_family 0 is
- * wallace4 and mixing 0 is stride_transpose; the rotation family and affine
- * mixing return WALLACE_ERR_UNSUPPORTED. */
+/* maxent::GeneratorConfig (generator.hpp:21-45).  transform_family: 0
+ * wallace4, 1 rotation (generator.cpp:113-172); mixing: 0 stride_transpose,
+ * 1 affine (generator.cpp:86-110).  All four combinations run on the B200. */
 typedef struct wallace_config {
   uint64_t pool_size;       /* power of two in [32, 2^31]; on-chip limit 2^14 (f32) / 2^13 (f64) */
   int32_t transform_family; /* TransformFamily */
@@ -201,6 +201,21 @@ wallace_status wallace_host_seed_pool(const wallace_config* cfg, uint64_t seed, 
 uint64_t wallace_default_stride(uint64_t rows);
 int32_t wallace_decode_pass_plan(uint64_t pool_size, uint64_t transform_word,
                                  uint64_t offset_word, uint64_t* offset0);
+
+/* maxent::PassPlan (generator.hpp:50-55) and decode_pass_plan(cfg, w0, w1)
+ * (generator.cpp:238-257) for every family/mixing combination. */
+typedef struct wallace_pass_plan {
+  int32_t wallace_variant;
+  int32_t t_index[2];
+  int32_t negate[2];
+  int32_t reserved_;
+  uint64_t offset[2];
+} wallace_pass_plan;
+wallace_status wallace_decode_pass_plan_ex(const wallace_config* cfg, uint64_t transform_word,
+                                           uint64_t offset_word, wallace_pass_plan* out);
+/* rotation_t_table() and rotation_from_t (transforms.cpp:39-70): t, c = cos,
+ * s = sin of the 16 table entries (any pointer may be NULL). */
+void wallace_rotation_table(double t[16], double c[16], double s[16]);
 
 #ifdef __cplusplus
 }

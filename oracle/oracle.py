@@ -132,6 +132,9 @@ def ref_lib():
         L.ref_rotation_table.restype = None
         L.ref_default_multipliers.argtypes = [u64, P(u64), P(u64)]
         L.ref_default_multipliers.restype = None
+        L.ref_decode_pass_plan_ex.argtypes = [u64, C.c_int, C.c_int, u64, u64, P(C.c_int32),
+                                              P(u64)]
+        L.ref_decode_pass_plan_ex.restype = None
         L.ref_last_error.restype = C.c_char_p
         L.ref_destroy.argtypes = [vp]
         L.ref_fill.argtypes = [vp, P(f64), u64]

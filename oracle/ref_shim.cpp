@@ -179,6 +179,23 @@ int ref_decode_pass_plan(uint64_t pool_size, uint64_t w0, uint64_t w1,
   return plan.wallace_variant;
 }
 
+// decode_pass_plan for any family/mixing: ints = {variant, t0, t1, neg0, neg1}
+void ref_decode_pass_plan_ex(uint64_t pool_size, int family, int mixing, uint64_t w0,
+                             uint64_t w1, int32_t* ints, uint64_t* offsets) {
+  maxent::GeneratorConfig c;
+  c.pool_size = pool_size;
+  c.transform_family = static_cast<maxent::TransformFamily>(family);
+  c.mixing = static_cast<maxent::MixingScheme>(mixing);
+  const auto plan = maxent::decode_pass_plan(c, w0, w1);
+  ints[0] = plan.wallace_variant;
+  ints[1] = plan.t_index[0];
+  ints[2] = plan.t_index[1];
+  ints[3] = plan.negate[0] ? 1 : 0;
+  ints[4] = plan.negate[1] ? 1 : 0;
+  offsets[0] = plan.offset[0];
+  offsets[1] = plan.offset[1];
+}
+
 void ref_polar(uint64_t seed, uint64_t n, double* out) {
   maxent::BaselineState s(seed);
   for (uint64_t i = 0; i < n; ++i) out[i] = maxent::polar_next(s);

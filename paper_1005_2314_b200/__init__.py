@@ -68,8 +68,8 @@ class GeneratorConfig:
     """maxent::GeneratorConfig (generator.hpp:21-45)."""
 
     pool_size: int = 1024
-    transform_family: int = 0  # 0 wallace4, 1 rotation (unsupported here)
-    mixing: int = 0            # 0 stride_transpose, 1 affine (unsupported here)
+    transform_family: int = 0  # 0 wallace4, 1 rotation
+    mixing: int = 0            # 0 stride_transpose, 1 affine
     chi2_method: int = 2       # 0 sqrt_shift, 1 wilson_hilferty, 2 cubic_a
     discard_every: int = 1
     out_mean: float = 0.0

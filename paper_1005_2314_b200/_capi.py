@@ -43,6 +43,17 @@ class wallace_config(C.Structure):
     ]
 
 
+class wallace_pass_plan(C.Structure):
+    """maxent::PassPlan (generator.hpp:50-55)."""
+    _fields_ = [
+        ("wallace_variant", i32),
+        ("t_index", i32 * 2),
+        ("negate", i32 * 2),
+        ("reserved_", i32),
+        ("offset", u64 * 2),
+    ]
+
+
 class wallace_pool_info(C.Structure):
     _fields_ = [
         ("pass_count", u64),
@@ -86,6 +97,8 @@ SYMBOLS = [
     ("wallace_host_seed_pool", i32, [P(wallace_config), u64, P(f64), P(f64), P(f64), P(u64), P(u64)]),
     ("wallace_default_stride", u64, [u64]),
     ("wallace_decode_pass_plan", i32, [u64, u64, u64, P(u64)]),
+    ("wallace_decode_pass_plan_ex", i32, [P(wallace_config), u64, u64, P(wallace_pass_plan)]),
+    ("wallace_rotation_table", None, [P(C.c_double), P(C.c_double), P(C.c_double)]),
 ]
 
 _lib = None

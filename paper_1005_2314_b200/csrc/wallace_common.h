@@ -66,7 +66,8 @@ struct FillArgs {
   void* pools_out;
   const PoolState* st_in;
   PoolState* st_out;
-  const uint32_t* plans;  // [n_pools][plan_stride]: offset | variant << 16
+  const uint32_t* plans;  // [n_pools][plan_stride] words: wallace4 offset | variant << 16;
+                          // rotation two per pass, offset | t << 16 | negate << 20
   uint32_t plan_stride;
   uint32_t n_passes;      // passes in this launch
   uint32_t d;             // discard_every
@@ -83,6 +84,12 @@ struct FillArgs {
   double mean;
   double sigma;
   Chi2Consts chi2;
+  // pass type (pass_type_of: 2*family + mixing) and, for the rotation
+  // family, the 16 table coefficients c, s (transforms.cpp:39-70)
+  int32_t pass_type;
+  int32_t pad_pt;
+  double rot_c[16];
+  double rot_s[16];
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]
@@ -97,8 +104,9 @@ struct PlanArgs {
   uint32_t plan_stride;
   uint32_t n_passes;
   uint32_t n_pools;
-  uint32_t rows_mask;
+  uint32_t off_mask;       // rows-1 (stride_transpose) or N-1 (affine)
   int32_t fixed_transform;
+  int32_t rotation;        // family: two plan words per pass
 };
 
 }  // namespace wb

@@ -30,6 +30,7 @@ namespace wb {
 cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t n_pools,
                                cudaStream_t s);
 int pool_kernel_threads(int dtype, int log2n);
+void affine_multipliers(int log2n, uint32_t* alpha, uint32_t* beta);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
 cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void* leftover,
                                uint64_t n_pools, uint32_t N, double mean, cudaStream_t s);
@@ -235,10 +236,13 @@ struct wallace_handle {
   cudaStream_t stream = nullptr;
   wb::Chi2Consts chi2{};
   uint32_t plan_cap = 0;  // passes per launch
+  int pass_type = 0;      // 2*family + mixing (wb::pass_type_of)
+  uint32_t plan_words = 1;  // plan words per pass (rotation: 2)
+  double rot_c[16] = {}, rot_s[16] = {};  // rotation_from_t of the table
 
   void* d_pools = nullptr;
   PoolState* d_state = nullptr;
-  uint32_t* d_plans = nullptr;   // two plan buffers of n_pools * plan_cap words
+  uint32_t* d_plans = nullptr;   // two plan buffers of n_pools * plan_cap * plan_words words
   // plan generation runs one launch ahead on a side stream
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_planned[2] = {nullptr, nullptr}, ev_pooled[2] = {nullptr, nullptr};
@@ -272,6 +276,40 @@ struct wallace_handle {
 
 namespace {
 
+// transforms.cpp:39-50: half-angle tangents of 16 angles, the midpoints of 16
+// equal slices of the window where cos and sin both lie in [0.05, 0.95]
+// (bit-identical to the reference table; tests/test_capi_host.py pins it)
+double rotation_t(int k) {
+  const double lo = std::acos(0.95), hi = std::asin(0.95);
+  return std::tan((lo + (k + 0.5) * (hi - lo) / 16) / 2);
+}
+
+// transforms.cpp:52-70 rotation_from_t
+void rotation_from_t(double t, double& c, double& s) {
+  if (std::abs(t) <= 1.0) {
+    const double den = 1.0 + t * t;
+    c = (1.0 - t * t) / den;
+    s = (2.0 * t) / den;
+  } else {
+    const double u = 1.0 / t;
+    const double den = 1.0 + u * u;
+    c = (u * u - 1.0) / den;
+    s = (2.0 * u) / den;
+  }
+}
+
+void rotation_table(double* c, double* s) {
+  for (int k = 0; k < 16; ++k) rotation_from_t(rotation_t(k), c[k], s[k]);
+}
+
+// generator.cpp:286-294 default_multipliers
+void default_multipliers(uint64_t n, uint64_t& alpha, uint64_t& beta) {
+  const auto near_odd = [](double x) { return static_cast<uint64_t>(std::llround(x)) | 1; };
+  alpha = near_odd(0.382 * static_cast<double>(n));
+  beta = near_odd(0.618 * static_cast<double>(n));
+  if (alpha == beta) beta += 2;
+}
+
 wallace_status validate(const wallace_config* c) {
   // generator.cpp:221-236 (messages name the field, test_generator.cpp:42-72)
   if (!c) return fail(WALLACE_ERR_INVALID_PARAM, "config must not be NULL");
@@ -293,10 +331,6 @@ wallace_status validate(const wallace_config* c) {
 }
 
 wallace_status check_supported(const wallace_config* c, int dtype) {
-  if (c->transform_family != 0)
-    return fail(WALLACE_ERR_UNSUPPORTED, "transform_family: rotation is not built on the B200 path");
-  if (c->mixing != 0)
-    return fail(WALLACE_ERR_UNSUPPORTED, "mixing: affine is not built on the B200 path");
   const uint64_t lim = dtype == WALLACE_F32 ? (1u << 14) : (1u << 13);
   if (c->pool_size > lim)
     return fail(WALLACE_ERR_UNSUPPORTED,
@@ -332,6 +366,9 @@ wb::FillArgs base_args(wallace_handle* h) {
   a.chi2 = h->chi2;
   a.leftover = h->d_leftover;
   a.out_stride = 0;
+  a.pass_type = h->pass_type;
+  std::memcpy(a.rot_c, h->rot_c, sizeof(a.rot_c));
+  std::memcpy(a.rot_s, h->rot_s, sizeof(a.rot_s));
   return a;
 }
 
@@ -369,13 +406,13 @@ struct Launch {
 // stream itself is advanced only by the plan kernels, in order.
 wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
   if (ls.empty()) return WALLACE_OK;
-  const size_t plan_words = h->n_pools * size_t(h->plan_cap);
+  const size_t plan_words = h->n_pools * size_t(h->plan_cap) * h->plan_words;
   WB_CUDA(cudaEventRecord(h->ev_start, h->stream));
   WB_CUDA(cudaStreamWaitEvent(h->side, h->ev_start, 0));
   auto plans = [&](size_t k) -> wallace_status {
     wb::FillArgs& a = ls[k].a;
     a.plans = h->d_plans + (k & 1) * plan_words;
-    a.plan_stride = h->plan_cap;
+    a.plan_stride = h->plan_cap * h->plan_words;
     if (a.n_passes == 0) return WALLACE_OK;
     // the buffer is free once launch k-2 finished
     if (k >= 2) WB_CUDA(cudaStreamWaitEvent(h->side, h->ev_pooled[k & 1], 0));
@@ -383,11 +420,13 @@ wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
     p.st_in = a.st_in;
     p.st_out = h->d_state;
     p.plans = const_cast<uint32_t*>(a.plans);
-    p.plan_stride = h->plan_cap;
+    p.plan_stride = h->plan_cap * h->plan_words;
     p.n_passes = a.n_passes;
     p.n_pools = static_cast<uint32_t>(h->n_pools);
-    p.rows_mask = static_cast<uint32_t>(h->N / 4 - 1);
+    // decode_pass_plan's offset mask (generator.cpp:241-244)
+    p.off_mask = static_cast<uint32_t>(h->cfg.mixing == 0 ? h->N / 4 - 1 : h->N - 1);
     p.fixed_transform = h->cfg.fixed_transform;
+    p.rotation = h->cfg.transform_family == 1;
     WB_CUDA(timed(h, h->ev_plan, h->side, [&] { return wb::launch_plan_kernel(p, h->side); }));
     ++g_launches;
     WB_CUDA(cudaEventRecord(h->ev_planned[k & 1], h->side));
@@ -540,6 +579,38 @@ int32_t wallace_decode_pass_plan(uint64_t pool_size, uint64_t w0, uint64_t w1, u
   return static_cast<int32_t>(w0 % 384u);
 }
 
+wallace_status wallace_decode_pass_plan_ex(const wallace_config* cfg, uint64_t w0, uint64_t w1,
+                                           wallace_pass_plan* out) {
+  wallace_status st = validate(cfg);
+  if (st) return st;
+  if (!out) return fail(WALLACE_ERR_INVALID_PARAM, "out must not be NULL");
+  // generator.cpp:238-257
+  *out = wallace_pass_plan{};
+  const uint64_t n = cfg->pool_size;
+  const uint64_t mask = cfg->mixing == 0 ? n / 4 - 1 : n - 1;
+  out->offset[0] = w1 & mask;
+  out->offset[1] = (w1 >> 32) & mask;
+  if (cfg->transform_family == 0) {
+    out->wallace_variant = static_cast<int32_t>(w0 % 384u);
+  } else {
+    out->t_index[0] = static_cast<int32_t>(w0 & 15);
+    out->negate[0] = static_cast<int32_t>((w0 >> 4) & 1);
+    out->t_index[1] = static_cast<int32_t>((w0 >> 5) & 15);
+    out->negate[1] = static_cast<int32_t>((w0 >> 9) & 1);
+  }
+  return WALLACE_OK;
+}
+
+void wallace_rotation_table(double t[16], double c[16], double s[16]) {
+  for (int k = 0; k < 16; ++k) {
+    if (t) t[k] = rotation_t(k);
+    double ck = 0.0, sk = 0.0;
+    rotation_from_t(rotation_t(k), ck, sk);
+    if (c) c[k] = ck;
+    if (s) s[k] = sk;
+  }
+}
+
 wallace_status wallace_host_seed_pool(const wallace_config* cfg, uint64_t seed, double* raw_out,
                                       double* reserved_prev, double* sum_sq, uint64_t s_out[4],
                                       uint64_t* draws) {
@@ -577,8 +648,24 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
   h->log2n = ilog2(h->N);
   h->stream = static_cast<cudaStream_t>(stream);
   h->chi2 = chi2_consts(*cfg);
+  h->pass_type = 2 * cfg->transform_family + cfg->mixing;
+  h->plan_words = cfg->transform_family == 1 ? 2 : 1;
   h->plan_cap = static_cast<uint32_t>(std::max<uint64_t>(
-      1, std::min<uint64_t>(kMaxPassesPerLaunch, kPlanBudgetBytes / (4 * n_pools))));
+      1, std::min<uint64_t>(kMaxPassesPerLaunch, kPlanBudgetBytes / (4 * h->plan_words * n_pools))));
+  rotation_table(h->rot_c, h->rot_s);
+  if (cfg->mixing == 1) {
+    // the kernels compile default_multipliers in; check them against the
+    // reference formula (generator.cpp:286-294) for this size
+    uint32_t ka = 0, kb = 0;
+    wb::affine_multipliers(h->log2n, &ka, &kb);
+    uint64_t ra = 0, rb = 0;
+    default_multipliers(h->N, ra, rb);
+    if (ka != ra || kb != rb) {
+      delete h;
+      return fail(WALLACE_ERR_UNSUPPORTED, "mixing: affine multipliers for pool_size %llu",
+                  static_cast<unsigned long long>(cfg->pool_size));
+    }
+  }
   h->cursor = static_cast<uint32_t>(h->N - 1);
   auto cleanup = [&](wallace_status s) {
     wallace_destroy(h);
@@ -630,7 +717,7 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
   } while (0)
   WB_CUDA_C(cudaMalloc(&h->d_pools, pools.size()));
   WB_CUDA_C(cudaMalloc(&h->d_state, n_pools * sizeof(PoolState)));
-  WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * sizeof(uint32_t)));
+  WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * h->plan_words * sizeof(uint32_t)));
   WB_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {

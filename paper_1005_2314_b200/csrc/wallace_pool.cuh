@@ -1,0 +1,1412 @@
+#pragma once
+// sm_100a kernels for the Wallace maximum-entropy normal generator.
+//
+//   plan_kernel  — the xoshiro256** pass-plan stream, one thread per pool
+//                  (baselines.cpp:33-45 + decode_pass_plan, generator.cpp:238-257)
+//   pool_kernel  — passes + emissions of one pool per CTA, pool resident in
+//                  shared memory (generator.cpp:52-85, 333-376)
+//   materialize_kernel — snapshot of a partially consumed emission before the
+//                  pool is advanced outside fill() (Generator::out_ semantics)
+//   reduce_consumer_kernel — fixed-order reduction of the fused consumer
+//
+// Numerics: every floating-point operation on the data path is an explicit
+// round-to-nearest intrinsic (__fadd_rn, __dmul_rn, ...), and the library is
+// compiled with -fmad=false, so no multiply-add is contracted — the
+// reference pins -ffp-contract=off for the same reason
+// (/root/reference/proj/CMakeLists.txt:10-14).
+#include <cuda.h>  // CUtensorMap (the map itself is encoded on the host)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "wallace_common.h"
+
+namespace wb {
+
+// ---------------------------------------------------------------------------
+// compile-time geometry
+// ---------------------------------------------------------------------------
+constexpr uint32_t gcd_c(uint32_t a, uint32_t b) { return b ? gcd_c(b, a % b) : a; }
+// transforms.cpp:161-169 default_stride: smallest odd > rows/3 coprime to rows
+constexpr uint32_t default_stride_c(uint32_t rows) {
+  uint32_t k = rows / 3 + 1;
+  if (k % 2 == 0) ++k;
+  while (gcd_c(k, rows) != 1) k += 2;
+  return k;
+}
+
+// generator.cpp:286-294 default_multipliers: odd neighbours of 0.382 n and
+// 0.618 n (llround of a positive value = floor(x + 0.5) for these sizes)
+constexpr uint32_t near_odd_c(double x) { return static_cast<uint32_t>(x + 0.5) | 1u; }
+constexpr uint32_t affine_alpha_c(uint32_t n) { return near_odd_c(0.382 * n); }
+constexpr uint32_t affine_beta_c(uint32_t n) {
+  return near_odd_c(0.618 * n) == affine_alpha_c(n) ? near_odd_c(0.618 * n) + 2 : near_odd_c(0.618 * n);
+}
+
+// Pass types (the template parameter PT of pool_kernel):
+//   0 wallace4 + stride_transpose, 1 wallace4 + affine,
+//   2 rotation + stride_transpose, 3 rotation + affine.
+constexpr int pass_type_of(int family, int mixing) { return 2 * family + mixing; }
+
+// transforms.cpp:24-35: element k of the p-th permutation of {0,1,2,3} in
+// lexicographic (std::next_permutation) order, evaluated at compile time.
+__host__ __device__ constexpr int perm_at(int p, int k) {
+  int avail[4] = {0, 1, 2, 3};
+  int n = 4;
+  const int fact[4] = {6, 2, 1, 1};
+  int out = 0;
+  for (int pos = 0; pos <= k; ++pos) {
+    const int q = p / fact[pos];
+    p %= fact[pos];
+    out = avail[q];
+    for (int j = q; j + 1 < n; ++j) avail[j] = avail[j + 1];
+    --n;
+  }
+  return out;
+}
+template <int P, int K>
+struct PermAt {
+  static constexpr int v = perm_at(P, K);
+};
+static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v == 0, "perm table");
+
+// Build-time knobs (defaults are the tuned choice; variants are built for
+// measurement by bench/tune scripts).
+#ifndef WB_INPLACE_F32
+#define WB_INPLACE_F32 0
+#endif
+#ifndef WB_INPLACE_F64
+#define WB_INPLACE_F64 0
+#endif
+#ifndef WB_REGS_INPLACE
+#define WB_REGS_INPLACE 56
+#endif
+// ABLATION builds only (timing experiments, wrong output): 1 = skip the
+// fast emission, 2 = skip its global stores, 3 = skip the scalar chain
+#ifndef WB_ABLATE
+#define WB_ABLATE 0
+#endif
+#ifndef WB_PREFETCH
+#define WB_PREFETCH 1
+#endif
+#ifndef WB_D2_STG64
+#define WB_D2_STG64 0
+#endif
+// 1: fp32 emissions shifted by 3 store [4b-1, 4b+3) (one shuffle per block)
+// instead of [4b+3, 4b+7) (three shuffles)
+#ifndef WB_D3_DOWN
+#define WB_D3_DOWN 1
+#endif
+// packed f32x2 ops for fp32 (measured slower on cfg2: 3.754-3.778 vs 3.731 ms,
+// FFMA2 latency lengthens each pass): bit 0 the butterfly and row factors, bit 1 the
+// mean-zero emission scaling
+#ifndef WB_PACKED
+#define WB_PACKED 0
+#endif
+// 1: bulk (TMA) emission when the emission is the pool itself (scale 1, mean +0)
+// and starts 16-byte aligned
+#ifndef WB_TMA
+#define WB_TMA 0
+#endif
+// 1: emission stores at one base register + immediate group offsets
+#ifndef WB_EMIT_IMM
+#define WB_EMIT_IMM 0
+#endif
+// 1: latency kernel runs the per-emission chain in a dedicated warp (measured
+// slower for one pool: the chain latency, not its placement, is the limit)
+#ifndef WB_CHAINW
+#define WB_CHAINW 0
+#endif
+// ABLATION builds only: consumer without histogram (1) / moments (2) / both (3)
+#ifndef WB_CONS_ABLATE
+#define WB_CONS_ABLATE 0
+#endif
+#ifndef WB_REGS_PP
+#define WB_REGS_PP 80
+#endif
+#ifndef WB_J_F32
+#define WB_J_F32 8
+#endif
+#ifndef WB_J_F64
+#define WB_J_F64 8
+#endif
+// 4-blocks per processing chunk (registers hold one chunk at a time)
+#ifndef WB_JC_F32
+#define WB_JC_F32 8
+#endif
+#ifndef WB_JC_F64
+#define WB_JC_F64 8
+#endif
+#ifndef WB_HS_LUT
+#define WB_HS_LUT 1
+#endif
+
+// Kernel geometry.  The template key is log2(N) for the throughput kernel
+// (many pools: few warps per pool, 8 4-blocks per thread) and log2(N) + 16
+// for the latency kernel (few pools: one 4-block per thread, up to 1024
+// threads per pool, so one pass is a short critical path).
+template <typename T, int LOG2N>
+struct Geo {
+  static constexpr bool LAT = LOG2N >= 16;
+  static constexpr int N = 1 << (LOG2N & 15);
+  static constexpr int ROWS = N / 4;
+  // groups (4-blocks) per thread: enough independent gathers per thread to
+  // hide LDS latency, few enough warps per pool for cheap barriers.
+  static constexpr int JWANT = LAT ? (ROWS > (WB_CHAINW ? 512 : 1024) ? ROWS / (WB_CHAINW ? 512 : 1024) : 1)
+                                   : (sizeof(T) == 4 ? WB_J_F32 : WB_J_F64);
+  static constexpr int J = (ROWS >= 32 * JWANT) ? JWANT : (ROWS >= 32 ? ROWS / 32 : 1);
+  static constexpr int JCWANT = LAT ? J : (sizeof(T) == 4 ? WB_JC_F32 : WB_JC_F64);
+  static constexpr int JC = J < JCWANT ? J : JCWANT;
+  static_assert(J % JC == 0, "chunking");
+  static constexpr int CT = (ROWS >= 32) ? ROWS / J : 32;  // compute threads (4-block owners)
+  static constexpr int NW = CT / 32;                       // compute warps
+  // the latency kernel adds a chain warp: the per-emission fp64 chain (chi2,
+  // division, sqrt: ~30 dependent ops) then overlaps the next pass instead of
+  // sitting on every pass's critical path
+  static constexpr bool CHAINW = LAT && WB_CHAINW;
+  static constexpr int THREADS = CT + (CHAINW ? 32 : 0);
+  static constexpr uint32_t MASK = ROWS - 1;
+  static constexpr uint32_t STRIDE = default_stride_c(ROWS) % ROWS;
+  static constexpr int VEC = 16 / sizeof(T);  // elements per 128-bit store
+  // the thread holding pool element N-1 (block ROWS-1, slot 3), group J-1
+  static constexpr int OWNER = (NW - 1) * 32 + ((ROWS - 1) & 31);
+  // in-place passes keep one pool buffer (two barriers per pass) and fit
+  // twice the pools per SM; ping-pong keeps two (one barrier per pass)
+  static constexpr bool INPLACE = sizeof(T) == 4 ? WB_INPLACE_F32 : WB_INPLACE_F64;
+  static constexpr int BUFS = INPLACE ? 1 : 2;
+  // resident CTAs per SM we ask ptxas to fit in registers: the smem limit
+  // (e.g. 6 ping-pong pools of N=4096 fp32) and a register budget
+  static constexpr int SMEM_PER_CTA = BUFS * N * sizeof(T) + 2048;
+  static constexpr int MINB_RAW = (220 * 1024) / SMEM_PER_CTA;
+  static constexpr int MINB_SMEM = MINB_RAW < 1 ? 1 : (MINB_RAW * THREADS > 2048 ? 2048 / THREADS : MINB_RAW);
+  static constexpr int REG_BUDGET = INPLACE ? WB_REGS_INPLACE : WB_REGS_PP;
+  static constexpr int MINB_REGS = 65536 / (THREADS * REG_BUDGET) < 1 ? 1 : 65536 / (THREADS * REG_BUDGET);
+  static constexpr int MINB = LAT ? 1 : (MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS);
+  // affine mixing multipliers (generator.cpp:286-294 default_multipliers);
+  // the host checks them against std::llround at handle creation
+  static constexpr uint32_t ALPHA = affine_alpha_c(N);
+  static constexpr uint32_t BETA = affine_beta_c(N);
+};
+
+// compile-time loop: f(std::integral_constant<int, i>) for i in [0, N)
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// explicit-rounding arithmetic
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+template <typename T> __device__ __forceinline__ T from_double(double x);
+template <> __device__ __forceinline__ float from_double<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ double from_double<double>(double x) { return x; }
+
+// Packed fp32 pairs (sm_100 FADD2/FMUL2/FFMA2): two independently rounded
+// lanes per instruction.  fma(x, +-1, y) is exactly the sum y +- x (the
+// product is exact), including the sign of a zero result, so the butterfly
+// below is bit-identical to the scalar add_rn/sub_rn form.  ptxas folds the
+// lane broadcasts, swaps and per-lane negations of pk2() into operand
+// modifiers.
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2_rn(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2_rn(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Second butterfly stage for output pair (S0, S1) of a permutation, times
+// the two row factors h = (h0, h1):
+//   z0 = a - d = fma(d, -1, a)     z1 = b + c = fma(c, 1, b)
+//   z2 = b - c = fma(c, -1, b)     z3 = (-a) - d = fma(d, -1, -a)
+// (transforms.hpp:89-103 op order).  The pair {z0, z3} shares a, so it uses
+// z0 = fma(a, 1, -d), z3 = fma(a, -1, -d): one broadcast per operand.
+template <int S0, int S1>
+__device__ __forceinline__ void wallace_pair(float a, float b, float c, float d, uint64_t h, float& o0,
+                                             float& o1) {
+  uint64_t z;
+  if constexpr ((S0 == 0 && S1 == 3) || (S0 == 3 && S1 == 0)) {
+    z = fma2_rn(pk2(a, a), pk2(S0 == 0 ? 1.f : -1.f, S1 == 0 ? 1.f : -1.f), pk2(-d, -d));
+  } else {
+    auto m = [&](int s) { return (s == 1 || s == 2) ? c : d; };
+    auto k = [](int s) { return s == 1 ? 1.f : -1.f; };
+    auto ad = [&](int s) { return s == 0 ? a : s == 3 ? -a : b; };
+    z = fma2_rn(pk2(m(S0), m(S1)), pk2(k(S0), k(S1)), pk2(ad(S0), ad(S1)));
+  }
+  upk2(mul2_rn(z, h), o0, o1);
+}
+
+// out = x * scale + mean with two roundings (generator.cpp:366-368).  When
+// mean is +0.0, fma(x, scale, +0) rounds x*scale once and adds +0 exactly,
+// which is bit-identical to the two-step form (including -0 + 0 = +0).
+template <typename T>
+__device__ __forceinline__ T emit_value(T x, T scale, T mean, bool mean_zero) {
+  return mean_zero ? fma_rn(x, scale, T(0)) : add_rn(mul_rn(x, scale), mean);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory vector helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sts4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void sts4(double* p, double a, double b, double c, double d) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+  reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+}
+// streaming (evict-first) global stores: the output is written once
+__device__ __forceinline__ void stg_vec(float* p, const float* v) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+}
+__device__ __forceinline__ void stg_vec(double* p, const double* v) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+}
+template <typename T>
+__device__ __forceinline__ void stg1(T* p, T v) { __stcs(p, v); }
+// streaming 128-bit store at base + OFF bytes (OFF an immediate: one base
+// register serves every group of a chunk)
+template <int OFF>
+__device__ __forceinline__ void stg_vec_at(uint64_t base, const float* v) {
+  // no "memory" clobber: nothing in the kernel reads the output, and a
+  // clobber would pin the scheduler (all stores bunched at the end)
+  asm("st.global.cs.v4.f32 [%0+%1], {%2, %3, %4, %5};" ::"l"(base), "n"(OFF), "f"(v[0]), "f"(v[1]),
+      "f"(v[2]), "f"(v[3]));
+}
+template <int OFF>
+__device__ __forceinline__ void stg_vec_at(uint64_t base, const double* v) {
+  asm("st.global.cs.v2.f64 [%0+%1], {%2, %3};" ::"l"(base), "n"(OFF), "d"(v[0]), "d"(v[1]));
+}
+#if WB_ABLATE == 2
+#define stg_vec(p, v) do { if (reinterpret_cast<uintptr_t>(p) == 1) stg_vec(p, v); } while (0)
+#endif
+
+// ---------------------------------------------------------------------------
+// chi-squared draw and the per-emission scalar chain (chi2.cpp:27-59,
+// generator.cpp:358-364, 373-375).  All in double, explicit rounding.
+// ---------------------------------------------------------------------------
+static __device__ double chi2_draw(double x, const Chi2Consts& c, uint32_t& clamped, uint32_t& flags) {
+  if (!isfinite(x)) flags |= kFlagChi2NonFinite;
+  double s;
+  if (c.method == 0) {
+    const double y = __dadd_rn(x, c.shift_c);
+    s = __dmul_rn(__dmul_rn(0.5, y), y);
+  } else if (c.method == 1) {
+    const double y = __dadd_rn(__dmul_rn(c.wh_sqrt_d, x), c.wh_one_m_d);
+    s = __dmul_rn(__dmul_rn(__dmul_rn(c.nu, y), y), y);
+  } else {
+    // a * (x*x - 1) + sqrt(2(nu - a^2)) * x + nu, evaluated left to right
+    const double t1 = __dmul_rn(c.a, __dsub_rn(__dmul_rn(x, x), 1.0));
+    const double t2 = __dmul_rn(c.cubic_c, x);
+    s = __dadd_rn(__dadd_rn(t1, t2), c.nu);
+  }
+  if (s < c.floor_v) {
+    ++clamped;
+    return c.floor_v;
+  }
+  return s;
+}
+
+struct SState {
+  double reserved_prev;
+  double sum_sq;
+  double S[2];
+  double r[2];
+  double scale[2];
+  double cur_scale;  // scale of the emission being drained by `lead`
+  double last_chi2;
+  double last_r;
+  double last_scale;
+  double renorm_k;
+  uint32_t clamp;
+  uint32_t flags;
+  int32_t renorm_ok;
+  uint32_t zero_seen;  // an exact zero was emitted by bulk stores (patch needed)
+  uint32_t ready;      // chain-warp kernels: S/r/scale of every emission <= ready published
+};
+
+// S, r, scale of the emission in `slot` from the current reserved value.
+__device__ __forceinline__ void chain_draw(SState& s, int slot, const Chi2Consts& c, double sigma) {
+  const double S = c.disable ? s.sum_sq : chi2_draw(s.reserved_prev, c, s.clamp, s.flags);
+  const double r = s.sum_sq > 0.0 ? __dsqrt_rn(__ddiv_rn(S, s.sum_sq)) : 0.0;
+  s.S[slot] = S;
+  s.r[slot] = r;
+  s.scale[slot] = __dmul_rn(sigma, r);
+}
+// after a renormalization changed sum_sq: S is kept (disable_chi2 re-reads it)
+__device__ __forceinline__ void chain_rescale(SState& s, int slot, const Chi2Consts& c, double sigma) {
+  if (c.disable) s.S[slot] = s.sum_sq;
+  const double r = s.sum_sq > 0.0 ? __dsqrt_rn(__ddiv_rn(s.S[slot], s.sum_sq)) : 0.0;
+  s.r[slot] = r;
+  s.scale[slot] = __dmul_rn(sigma, r);
+}
+// bookkeeping at the end of emission `slot` (generator.cpp:373-375)
+__device__ __forceinline__ void chain_close(SState& s, int slot, double x_last) {
+  s.reserved_prev = __dmul_rn(x_last, s.r[slot]);
+  s.last_chi2 = s.S[slot];
+  s.last_r = s.r[slot];
+  s.last_scale = s.scale[slot];
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p)))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
+}
+
+// generator.cpp:20-34 recompute_sum_sq — sequential Neumaier, one thread.
+// SELECT: branch-free form — the reference's two branches are the same
+// expression with the operands ordered by magnitude, (big - t) + small, so
+// only the running sum's 8-cycle DADD dependency is on the critical path
+// (used by the latency kernel, where the renormalisation is on the critical
+// path; the throughput kernel keeps the compact form for register pressure).
+template <bool SELECT>
+__device__ __forceinline__ void neumaier_add(double& sum, double& comp, double x) {
+  const double term = __dmul_rn(x, x);
+  const double t = __dadd_rn(sum, term);
+  if constexpr (SELECT) {
+    const bool sum_big = fabs(sum) >= fabs(term);
+    const double big = sum_big ? sum : term;
+    const double small = sum_big ? term : sum;
+    comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(big, t), small));
+  } else if (fabs(sum) >= fabs(term)) {
+    comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(sum, t), term));
+  } else {
+    comp = __dadd_rn(comp, __dadd_rn(__dsub_rn(term, t), sum));
+  }
+  sum = t;
+}
+template <typename T, bool VECTOR_LOADS>
+__device__ double neumaier_sq(const T* v, int n) {
+  double sum = 0.0, comp = 0.0;
+  if constexpr (VECTOR_LOADS && sizeof(T) == 4) {
+    const float4* q = reinterpret_cast<const float4*>(v);
+#pragma unroll 4
+    for (int i = 0; i < n / 4; ++i) {
+      const float4 f = q[i];
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.x);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.y);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.z);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.w);
+    }
+  } else if constexpr (VECTOR_LOADS) {
+    const double2* q = reinterpret_cast<const double2*>(v);
+#pragma unroll 4
+    for (int i = 0; i < n / 2; ++i) {
+      const double2 f = q[i];
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.x);
+      neumaier_add<VECTOR_LOADS>(sum, comp, f.y);
+    }
+  } else {
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) neumaier_add<false>(sum, comp, static_cast<double>(v[i]));
+  }
+  return __dadd_rn(sum, comp);
+}
+
+// generator.cpp:345-351 renormalize_.  Contains block barriers: call from
+// all threads.
+// LAT: the latency kernel (one pool per SM, the renormalisation is on the
+// critical path: vector loads, out of line); otherwise inline scalar loads
+template <typename T, int N, int THREADS, bool LAT>
+__device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
+  if (tid == 0) {
+    const double ss = neumaier_sq<T, LAT>(cur, N);
+    s.renorm_ok = ss > 0.0;
+    s.renorm_k = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
+  }
+  __syncthreads();
+  if (s.renorm_ok) {
+    const double k = s.renorm_k;
+    for (int i = tid; i < N; i += THREADS)
+      cur[i] = from_double<T>(__dmul_rn(static_cast<double>(cur[i]), k));
+    __syncthreads();
+    if (tid == 0) s.sum_sq = neumaier_sq<T, LAT>(cur, N);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// fused consumer accumulators (config 5)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Consumer {
+  double s1 = 0, s2 = 0, s3 = 0, s4 = 0;  // per-thread totals (fp64)
+  T a1 = 0, a2 = 0, a3 = 0, a4 = 0;       // per-emission partials (T)
+  uint32_t* hist;  // shared, 258 bins (under, 256, over)
+  __device__ __forceinline__ void add(T x) {
+    if (WB_CONS_ABLATE != 2 && WB_CONS_ABLATE != 3) {
+      const T x2 = mul_rn(x, x);
+      a1 = add_rn(a1, x);
+      a2 = add_rn(a2, x2);
+      a3 = fma_rn(x2, x, a3);
+      a4 = fma_rn(x2, x2, a4);
+    }
+    if (WB_CONS_ABLATE != 1 && WB_CONS_ABLATE != 3) {
+      // bin = floor((x + 8) * 16) in T, clamped to [-1, 256] (under / over)
+      const T t = mul_rn(add_rn(x, T(8)), T(16));
+      int bin = sizeof(T) == 4 ? __float2int_rd(static_cast<float>(t)) : __double2int_rd(static_cast<double>(t));
+      bin = max(-1, min(bin, 256));
+      atomicAdd(&hist[bin + 1], 1u);
+    }
+  }
+  __device__ __forceinline__ void add_group(const T* y, int n) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < n) add(y[k]);
+  }
+  // fold the per-emission partials into the fp64 totals
+  __device__ __forceinline__ void flush() {
+    s1 += static_cast<double>(a1);
+    s2 += static_cast<double>(a2);
+    s3 += static_cast<double>(a3);
+    s4 += static_cast<double>(a4);
+    a1 = a2 = a3 = a4 = T(0);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// The fast emission (full emissions: all N-1 values): values are in
+// registers in pool order; 128-bit aligned streaming stores, shifted by DELTA
+// elements with warp shuffles (the emission start e*(N-1) is misaligned in
+// 3 of 4 emissions).
+//
+// Thread t owns blocks b_j = (warp*J + j)*32 + lane.  The aligned chunk
+// [4b+DELTA, 4b+DELTA+4) holds b's tail and the first DELTA values of block
+// b+1, which lives in lane+1 — or, for lane 31, in lane 0 of group j+1.  So
+// lanes 0..30 store their group-j chunk as soon as group j is shuffled, and
+// lane 31 stores its group-(j-1) chunk when group j's shuffle delivers lane
+// 0's head.  Lane 31's last group and lane 0's first head straddle two warps
+// and use scalar stores.  Element N-1 is never emitted (generator.cpp:366).
+// ---------------------------------------------------------------------------
+template <typename T, int LOG2N, int DELTA, bool MZ>
+__device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], int c0, T (&prev)[4],
+                                           T* gbase, T sc, T mean, int lane, int warp,
+                                           int jfirst = 0) {
+  using G = Geo<T, LOG2N>;
+  constexpr int J = G::J, JC = G::JC, VEC = G::VEC;
+  static_assert(DELTA < VEC, "shift");
+  const bool l31 = lane == 31;
+  const uint32_t b0 = warp * J * 32 + lane;  // this thread's block in group 0
+  // Every lane's chunk of group j starts at cbase + 128 j elements: lanes
+  // 0..30 store their own group-j chunk, lane 31 its group-(j-1) chunk, so
+  // its base is one group (128 elements) lower.  The group offsets are then
+  // immediates of the store instructions.
+  const uint64_t cbase = reinterpret_cast<uint64_t>(gbase) +
+                         sizeof(T) * (4ull * (b0 + 32u * c0) + DELTA) -
+                         ((DELTA > 0 && l31) ? 128u * sizeof(T) : 0u);
+  auto store_group = [&](auto jjc, const T* c) {
+    constexpr int JJ = decltype(jjc)::value;
+#pragma unroll
+    for (int v = 0; v < 4; v += VEC) {
+      if (v == 0) stg_vec_at<JJ * 128 * int(sizeof(T))>(cbase, c);
+      else stg_vec_at<JJ * 128 * int(sizeof(T)) + 16>(cbase, c + 2);
+    }
+  };
+#pragma unroll
+  for (int jj = 0; jj < JC; ++jj) {
+    const int j = c0 + jj;
+    if (j < jfirst) continue;  // groups before jfirst are emitted elsewhere
+    const uint32_t b = b0 + 32 * j;
+    T y[4];
+    if constexpr ((WB_PACKED & 2) && MZ && sizeof(T) == 4) {
+      // (only the mean-zero form: ptxas contracts a packed mul.rn + add.rn
+      // pair into one FFMA2 despite the explicit rounding modifiers)
+      const uint64_t s2 = pk2(sc, sc);
+#pragma unroll
+      for (int h = 0; h < 4; h += 2)
+        upk2(fma2_rn(pk2(X[jj][h], X[jj][h + 1]), s2, pk2(0.f, 0.f)), y[h], y[h + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
+    }
+    if constexpr (WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
+      // global(4b) is 8-byte aligned: two float2 stores of the own block,
+      // no neighbour values needed
+      if (b != G::ROWS - 1) {
+        __stcs(reinterpret_cast<float2*>(gbase + 4 * b), make_float2(y[0], y[1]));
+        __stcs(reinterpret_cast<float2*>(gbase + 4 * b + 2), make_float2(y[2], y[3]));
+      } else {
+        __stcs(reinterpret_cast<float2*>(gbase + 4 * b), make_float2(y[0], y[1]));
+        stg1(gbase + 4 * b + 2, y[2]);
+      }
+    } else if constexpr (WB_D3_DOWN && VEC == 4 && DELTA == 3) {
+      // shift the other way: the aligned chunk [4b-1, 4b+3) is the previous
+      // block's last value (lane-1, or for lane 0 lane 31 of group j-1, kept
+      // in prev[0]) and this block's first three -- one shuffle, and the
+      // pool's last element X[N-1] = y[3] of block ROWS-1 falls outside
+      const T s = __shfl_sync(0xffffffffu, y[3], (lane + 31) & 31);
+      if (lane == 0 && j == jfirst) {  // head of this warp: the value before is the previous warp's
+        stg1(gbase + 4 * b + 0, y[0]);
+        stg1(gbase + 4 * b + 1, y[1]);
+        stg1(gbase + 4 * b + 2, y[2]);
+      } else {
+        const T c[4] = {lane == 0 ? prev[0] : s, y[0], y[1], y[2]};
+        stg_vec(gbase + 4 * b - 1, c);
+      }
+      if (lane == 31 && j == J - 1 && 4 * b + 3 < uint32_t(G::N - 1))
+        stg1(gbase + 4 * b + 3, y[3]);  // tail of this warp: the next warp's head is scalar
+      prev[0] = s;
+    } else if constexpr (DELTA == 0) {
+      if (b != G::ROWS - 1) {
+        if constexpr (WB_EMIT_IMM) {
+          static_for<JC>([&](auto jjc) {
+            if (decltype(jjc)::value == jj) store_group(jjc, y);
+          });
+        } else {
+#pragma unroll
+          for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * b + v, y + v);
+        }
+      } else {
+        stg1(gbase + 4 * b + 0, y[0]);
+        stg1(gbase + 4 * b + 1, y[1]);
+        stg1(gbase + 4 * b + 2, y[2]);
+      }
+    } else {
+      T sh[DELTA];
+#pragma unroll
+      for (int t = 0; t < DELTA; ++t) sh[t] = __shfl_sync(0xffffffffu, y[t], (lane + 1) & 31);
+      T c[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (DELTA + m < 4) c[m] = l31 ? prev[(DELTA + m) & 3] : y[(DELTA + m) & 3];
+        else c[m] = sh[(DELTA + m - 4) & (DELTA > 0 ? 3 : 0)];
+      }
+      if (!(l31 && j == jfirst)) {
+        if constexpr (WB_EMIT_IMM) {
+          static_for<JC>([&](auto jjc) {
+            if (decltype(jjc)::value == jj) store_group(jjc, c);
+          });
+        } else {
+          const uint32_t cb = l31 ? b - 32 : b;
+#pragma unroll
+          for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * cb + DELTA + v, c + v);
+        }
+      }
+      if (j == jfirst && lane == 0) {  // head of this warp's first block
+#pragma unroll
+        for (int t = 0; t < DELTA; ++t) stg1(gbase + 4 * b + t, y[t]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) prev[k] = y[k];
+    }
+  }
+  if constexpr (DELTA > 0 && !(WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) &&
+                !(WB_D3_DOWN && VEC == 4 && DELTA == 3)) {
+    if (l31 && c0 + JC == J) {  // last group of the warp: own tail only, the head is the next warp's
+      const uint32_t b = (warp * J + J - 1) * 32 + 31;
+#pragma unroll
+      for (int m = DELTA; m < 4; ++m)
+        if (4 * b + m < uint32_t(G::N - 1)) stg1(gbase + 4 * b + m, prev[m]);
+    }
+  }
+}
+
+template <typename T, int LOG2N, int DELTA>
+__device__ __forceinline__ void emit_chunk_mz(bool mz, const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
+                                              T (&prev)[4], T* gbase, T sc, T mean, int lane, int warp,
+                                              int jfirst = 0) {
+  if (mz) emit_chunk<T, LOG2N, DELTA, true>(X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+  else emit_chunk<T, LOG2N, DELTA, false>(X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+}
+
+// Register emission of one chunk for any shift: dispatch on delta.
+template <typename T, int LOG2N>
+__device__ __forceinline__ void emit_chunk_any(uint32_t delta, bool mz,
+                                               const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
+                                               T (&prev)[4], T* gbase, T sc, T mean, int lane,
+                                               int warp, int jfirst = 0) {
+  using G = Geo<T, LOG2N>;
+  if constexpr (G::VEC == 4) {
+    switch (delta) {
+      case 0: emit_chunk_mz<T, LOG2N, 0>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+      case 1: emit_chunk_mz<T, LOG2N, 1 % G::VEC>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+      case 2: emit_chunk_mz<T, LOG2N, 2 % G::VEC>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+      default: emit_chunk_mz<T, LOG2N, 3 % G::VEC>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst); break;
+    }
+  } else {
+    if (delta == 0) emit_chunk_mz<T, LOG2N, 0>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+    else emit_chunk_mz<T, LOG2N, 1>(mz, X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bulk (TMA) emission.  When an emission's scale is exactly 1 and the mean
+// is +0 (e.g. disable_chi2 with sigma 1 — BASELINE config 2), its values are
+// the pool itself, already in shared memory in pool order: out[i] = x[i]*1+0
+// = x[i] bit for bit, except that the reference's "+0" turns an exact -0 into
+// +0.  The emission is then issued as 2-D tensor stores of BOX elements from
+// the pool buffer (TMA takes arbitrary element coordinates, so the output's
+// misalignment costs nothing); the last (N-1) mod BOX + ... values, the
+// groups past the last full box, go through the register path; an exact zero
+// anywhere in the emission (probability ~1e-8 per value) triggers a patch
+// pass that rewrites -0 as +0 after the bulk stores have completed.
+// ---------------------------------------------------------------------------
+constexpr int kTmaBox = 256;  // elements per tensor-store box (TMA box dim limit)
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// pool_kernel: one CTA per pool.  The pool ping-pongs between two shared
+// buffers (one block barrier per pass); plans for the launch are staged in
+// shared memory; pool state persists in HBM across launches.
+//
+// One pass (generator.cpp:64-85): for b < ROWS, r = (off + b*STRIDE) mod ROWS,
+//   v_c = in[c*ROWS + r], a=v0+v1, bb=v0-v1, c=v2+v3, d=v2-v3,
+//   z = {a-d, bb+c, bb-c, -a-d}, out[4b+k] = (0.5*sign_k) * z[src_k].
+// The gather is bank-conflict-free: STRIDE is odd and ROWS a multiple of 32,
+// so 32 consecutive b hit 32 distinct banks; out[4b..4b+3] is one 128-bit
+// shared store.  The row permutation src is warp-uniform per pass and is
+// applied through a 24-way uniform branch over compile-time register moves.
+// Shared addresses are byte offsets: gather = ((rb4 + off4) & MASK4) | cur,
+// one IADD3 + one LOP3 per 4-block (the buffers sit at power-of-two offsets).
+// ---------------------------------------------------------------------------
+template <typename T, int LOG2N>
+struct Smem {
+  static constexpr int N = Geo<T, LOG2N>::N;
+  static constexpr uint32_t BUF = N * sizeof(T);  // bytes per pool buffer (power of two)
+  // pools in static shared memory when they fit the 48 KiB static limit: the
+  // buffer base then folds into the LDS/STS immediate offsets
+  static constexpr int BUFS = Geo<T, LOG2N>::BUFS;
+  static constexpr bool STATIC = BUFS * BUF <= 40 * 1024;
+};
+
+// One pass over the pool in shared memory (generator.cpp:64-85); leaves the
+// signed, permuted outputs of this thread's 4-blocks in X and stores them to
+// the next buffer.  sb = b0*STRIDE + off for this thread's first block.
+template <typename T, int LOG2N, int J, int PT = 0>
+__device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
+                                         uint32_t plan, uint32_t b0, T (&X)[J][4],
+                                         const float* hs_lut) {
+  static_assert(PT == 0 || PT == 1, "wallace4 pass types");
+  using G = Geo<T, LOG2N>;
+  constexpr int ROWS = G::ROWS;
+  constexpr uint32_t MASK4 = (ROWS - 1) * sizeof(T);
+  const uint32_t off = plan & 0xffffu;
+  const uint32_t variant = plan >> 16;
+  const uint32_t perm = variant >> 4;
+  T hs[4];
+  if constexpr (WB_HS_LUT && sizeof(T) == 4) {
+    // the four +-1/2 row factors of this variant's sign mask, one 128-bit load
+    const float4 h = reinterpret_cast<const float4*>(hs_lut)[variant & 15u];
+    hs[0] = h.x;
+    hs[1] = h.y;
+    hs[2] = h.z;
+    hs[3] = h.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+  }
+  // byte offset of row r_j = (off + b_j*STRIDE) mod ROWS, b_j = b0 + 32j
+  const uint32_t r0 = (b0 * G::STRIDE + off) * sizeof(T);
+
+  if constexpr ((WB_PACKED & 1) && sizeof(T) == 4 && PT == 0) {
+    // gather + first butterfly stage as two packed ops per 4-block:
+    // (a, b) = (v0 + v1, v0 - v1), (c, d) = (v2 + v3, v2 - v3)
+    float ab[J][2], cd[J][2];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      float v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+      if (ROWS >= 32 || b0 + 32 * j < ROWS) {
+        constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
+        const float* row = reinterpret_cast<const float*>(base + (((r0 + j * step) & MASK4) | cur_off));
+        v0 = row[0];
+        v1 = row[ROWS];
+        v2 = row[2 * ROWS];
+        v3 = row[3 * ROWS];
+      }
+      const uint64_t pm = pk2(1.f, -1.f);
+      upk2(fma2_rn(pk2(v1, v1), pm, pk2(v0, v0)), ab[j][0], ab[j][1]);
+      upk2(fma2_rn(pk2(v3, v3), pm, pk2(v2, v2)), cd[j][0], cd[j][1]);
+    }
+    const uint64_t h01 = pk2(float(hs[0]), float(hs[1]));
+    const uint64_t h23 = pk2(float(hs[2]), float(hs[3]));
+    float (&Xf)[J][4] = reinterpret_cast<float (&)[J][4]>(X);
+    switch (perm) {
+#define WB_PERM_CASE(P)                                                                              \
+  case P:                                                                                            \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {                                                  \
+      wallace_pair<PermAt<P, 0>::v, PermAt<P, 1>::v>(ab[j][0], ab[j][1], cd[j][0], cd[j][1], h01,    \
+                                                      Xf[j][0], Xf[j][1]);                           \
+      wallace_pair<PermAt<P, 2>::v, PermAt<P, 3>::v>(ab[j][0], ab[j][1], cd[j][0], cd[j][1], h23,    \
+                                                      Xf[j][2], Xf[j][3]);                           \
+    }                                                                                                \
+    break;
+      WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
+      WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
+      WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
+      WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
+      WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22) WB_PERM_CASE(23)
+      default: __builtin_unreachable();
+#undef WB_PERM_CASE
+    }
+    if constexpr (G::INPLACE) __syncthreads();
+    float* nb = reinterpret_cast<float*>(const_cast<char*>(base) + nxt_off);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) sts4(nb + 4 * b, Xf[j][0], Xf[j][1], Xf[j][2], Xf[j][3]);
+    }
+    return;
+  }
+
+  // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
+  T z[J][4];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    T v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    if (ROWS >= 32 || b0 + 32 * j < ROWS) {
+      if constexpr (PT == 0) {
+        constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
+        const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) | cur_off));
+        v0 = row[0];
+        v1 = row[ROWS];
+        v2 = row[2 * ROWS];
+        v3 = row[3 * ROWS];
+      } else {
+        // affine (generator.cpp:86-110): element 4b+c of the gathered
+        // sequence sits at (off + (4b+c)*alpha) mod N
+        constexpr uint32_t A = G::ALPHA * sizeof(T), MASKN = (G::N - 1) * sizeof(T);
+        const uint32_t e = (off + 4u * (b0 + 32u * j) * G::ALPHA) * sizeof(T);
+        v0 = *reinterpret_cast<const T*>(base + ((e & MASKN) | cur_off));
+        v1 = *reinterpret_cast<const T*>(base + (((e + A) & MASKN) | cur_off));
+        v2 = *reinterpret_cast<const T*>(base + (((e + 2 * A) & MASKN) | cur_off));
+        v3 = *reinterpret_cast<const T*>(base + (((e + 3 * A) & MASKN) | cur_off));
+      }
+    }
+    const T aa = add_rn(v0, v1);
+    const T bb = sub_rn(v0, v1);
+    const T cc = add_rn(v2, v3);
+    const T dd = sub_rn(v2, v3);
+    z[j][0] = sub_rn(aa, dd);
+    z[j][1] = add_rn(bb, cc);
+    z[j][2] = sub_rn(bb, cc);
+    z[j][3] = sub_rn(-aa, dd);
+  }
+  // signed row permutation: X[k] = (0.5*sign_k) * z[src_k]
+  switch (perm) {
+#define WB_PERM_CASE(P)                                     \
+  case P:                                                   \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {         \
+      X[j][0] = mul_rn(hs[0], z[j][PermAt<P, 0>::v]);       \
+      X[j][1] = mul_rn(hs[1], z[j][PermAt<P, 1>::v]);       \
+      X[j][2] = mul_rn(hs[2], z[j][PermAt<P, 2>::v]);       \
+      X[j][3] = mul_rn(hs[3], z[j][PermAt<P, 3>::v]);       \
+    }                                                       \
+    break;
+    WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
+    WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
+    WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
+    WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
+    WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22) WB_PERM_CASE(23)
+    default: __builtin_unreachable();  // perm = variant >> 4 < 24 (variant = w0 % 384)
+#undef WB_PERM_CASE
+  }
+  if constexpr (G::INPLACE) __syncthreads();  // every gather of this pass is done
+  T* nb = reinterpret_cast<T*>(const_cast<char*>(base) + nxt_off);
+  if constexpr (sizeof(T) == 8) {
+    // a 4-double block is 32 bytes: two 128-bit stores at a 32-byte lane
+    // stride would hit each bank twice per 8-lane phase; lanes with bit 2 set
+    // store their halves in the opposite order, which makes both stores
+    // conflict-free (lanes l and l+4 then cover complementary banks)
+    const bool swz = (b0 >> 2) & 1;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) {
+        double2* q = reinterpret_cast<double2*>(nb + 4 * b);
+        const double2 lo = make_double2(X[j][0], X[j][1]);
+        const double2 hi = make_double2(X[j][2], X[j][3]);
+        q[swz ? 1 : 0] = swz ? hi : lo;
+        q[swz ? 0 : 1] = swz ? lo : hi;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) sts4(nb + 4 * b, X[j][0], X[j][1], X[j][2], X[j][3]);
+    }
+  }
+}
+
+// One 4-block store of a pass result.  fp64: a 4-double block is 32 bytes;
+// lanes with bit 2 set store their halves in the opposite order so both
+// 128-bit stores are bank-conflict-free (see run_pass).
+template <typename T>
+__device__ __forceinline__ void store_block(T* nb, uint32_t b, T x0, T x1, T x2, T x3) {
+  if constexpr (sizeof(T) == 8) {
+    const bool swz = (b >> 2) & 1;
+    double2* q = reinterpret_cast<double2*>(nb + 4 * b);
+    const double2 lo = make_double2(x0, x1), hi = make_double2(x2, x3);
+    q[swz ? 1 : 0] = swz ? hi : lo;
+    q[swz ? 0 : 1] = swz ? lo : hi;
+  } else {
+    sts4(nb + 4 * b, x0, x1, x2, x3);
+  }
+}
+
+// One rotation pass (run_pass, generator.cpp:259-271: two half-sweeps,
+// rotation_sweep :113-172).
+//   sweep 0: gather through the mixing map (offset word 0), rotate the pairs
+//            (4b, 4b+1), (4b+2, 4b+3) -> scratch buffer (nxt_off); barrier;
+//   sweep 1: gather the scratch through the map (offset word 1), rotate the
+//            pairs (4b+1, 4b+2), (4b+3, 4b+4) and the wrap pair (N-1, 0) ->
+//            back into the current buffer.  Each thread gathers its block's
+//            two neighbours g[4b-1], g[4b+4] itself (no exchange), so every
+//            store is an aligned 4-block.
+// The pool therefore stays in `cur` (the caller does not flip buffers) and
+// this thread's 4-blocks are left in X, like run_pass.  Coefficients
+// ce = g*c, se = g*s in fp64 (exact sign flips of the table entry), rounded
+// once for T = float; out = ce*z1 + se*z2 and
+// (-se)*z1 + ce*z2 with two roundings each, as the reference.
+// Plan words: offset | t_index << 16 | negate << 20, one per sweep.
+template <typename T, int LOG2N, int J, int MIX>
+__device__ __forceinline__ void run_pass_rot(const char* base, uint32_t cur_off, uint32_t nxt_off,
+                                             uint32_t w0, uint32_t w1, uint32_t b0, T (&X)[J][4],
+                                             const double* rc, const double* rs) {
+  using G = Geo<T, LOG2N>;
+  constexpr int ROWS = G::ROWS;
+  constexpr uint32_t ES = sizeof(T);
+  constexpr uint32_t MASK4 = (ROWS - 1) * ES, MASKN = (G::N - 1) * ES;
+  constexpr uint32_t SROW = G::STRIDE * ES;  // one row step in bytes
+  auto coef = [&](uint32_t w, T& ce, T& se) {
+    const uint32_t t = (w >> 16) & 15u;
+    const bool neg = (w >> 20) & 1u;
+    ce = from_double<T>(neg ? -rc[t] : rc[t]);
+    se = from_double<T>(neg ? -rs[t] : rs[t]);
+  };
+  auto ld = [&](uint32_t byte_off, uint32_t buf) -> T {
+    return *reinterpret_cast<const T*>(base + (byte_off | buf));
+  };
+  // ---- sweep 0 ----
+  {
+    T ce, se;
+    coef(w0, ce, se);
+    const T nse = -se;
+    const uint32_t off = w0 & 0xffffu;
+    T* nb = reinterpret_cast<T*>(const_cast<char*>(base) + nxt_off);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      if (ROWS >= 32 || b < ROWS) {
+        T g[4];
+        if constexpr (MIX == 0) {
+          const uint32_t r = ((off + b * G::STRIDE) * ES) & MASK4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) g[c] = ld(r + c * ROWS * ES, cur_off);
+        } else {
+          constexpr uint32_t A = G::ALPHA * ES;
+          const uint32_t e = (off + 4u * b * G::ALPHA) * ES;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) g[c] = ld((e + c * A) & MASKN, cur_off);
+        }
+        store_block(nb, b, add_rn(mul_rn(ce, g[0]), mul_rn(se, g[1])),
+                    add_rn(mul_rn(nse, g[0]), mul_rn(ce, g[1])),
+                    add_rn(mul_rn(ce, g[2]), mul_rn(se, g[3])),
+                    add_rn(mul_rn(nse, g[2]), mul_rn(ce, g[3])));
+      }
+    }
+  }
+  __syncthreads();  // the whole sweep-0 result is in the scratch buffer
+  // ---- sweep 1 ----
+  {
+    T ce, se;
+    coef(w1, ce, se);
+    const T nse = -se;
+    const uint32_t off = w1 & 0xffffu;
+    T* cb = reinterpret_cast<T*>(const_cast<char*>(base) + cur_off);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint32_t b = b0 + 32 * j;
+      X[j][0] = X[j][1] = X[j][2] = X[j][3] = T(0);
+      if (ROWS >= 32 || b < ROWS) {
+        T h[4], hm, hp;  // g[4b..4b+3], g[4b-1], g[4b+4] (indices mod N)
+        if constexpr (MIX == 0) {
+          // element 4q+c at column c, row (off + q*stride) mod rows
+          const uint32_t r = ((off + b * G::STRIDE) * ES) & MASK4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) h[c] = ld(r + c * ROWS * ES, nxt_off);
+          hm = ld(((r - SROW) & MASK4) + 3 * ROWS * ES, nxt_off);
+          hp = ld((r + SROW) & MASK4, nxt_off);
+        } else {
+          constexpr uint32_t B = G::BETA * ES;
+          const uint32_t e = (off + 4u * b * G::BETA) * ES;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) h[c] = ld((e + c * B) & MASKN, nxt_off);
+          hm = ld((e - B) & MASKN, nxt_off);
+          hp = ld((e + 4 * B) & MASKN, nxt_off);
+        }
+        X[j][0] = add_rn(mul_rn(nse, hm), mul_rn(ce, h[0]));
+        X[j][1] = add_rn(mul_rn(ce, h[1]), mul_rn(se, h[2]));
+        X[j][2] = add_rn(mul_rn(nse, h[1]), mul_rn(ce, h[2]));
+        X[j][3] = add_rn(mul_rn(ce, h[3]), mul_rn(se, hp));
+        store_block(cb, b, X[j][0], X[j][1], X[j][2], X[j][3]);
+      }
+    }
+  }
+}
+
+// Emission of the values already in registers (fast path) into the fused
+// consumer instead of memory.
+template <typename T, int LOG2N, int JCL>
+__device__ __forceinline__ void consume_chunk(const T (&X)[JCL][4], Consumer<T>& cons, T sc, T mean,
+                                              bool mz, uint32_t b0c) {
+  using G = Geo<T, LOG2N>;
+#pragma unroll
+  for (int j = 0; j < JCL; ++j) {
+    const uint32_t b = b0c + 32 * j;
+    T y[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean, mz);
+    cons.add_group(y, b == G::ROWS - 1 ? 3 : 4);
+  }
+}
+
+template <typename T, int LOG2N, int MODE, int PT>
+__global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
+    pool_kernel(const __grid_constant__ FillArgs a) {
+  using G = Geo<T, LOG2N>;
+  using SM = Smem<T, LOG2N>;
+  constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
+  constexpr uint32_t BUF = SM::BUF;
+  constexpr bool FAST = ROWS >= 32;
+  // buffer 0 at offset 0, buffer 1 at BUF (a power of two above every gather
+  // offset, so `| cur_off` selects the buffer); plans in dynamic smem
+  constexpr uint32_t FLIP = G::INPLACE ? 0u : BUF;  // cur_off ^ FLIP = next buffer
+  // rotation passes (PT 2, 3) use the other buffer as sweep scratch and end
+  // in the current one; their plans are two words per pass
+  constexpr bool ROT = PT >= 2;
+  constexpr uint32_t PFLIP = ROT ? 0u : FLIP;
+  constexpr uint32_t PW = ROT ? 2u : 1u;
+  static_assert(!ROT || (G::JC == G::J && !G::CHAINW && !G::INPLACE),
+                "rotation passes hold all 4-blocks of a thread across their inner barrier");
+  __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? SM::BUFS * BUF : 16];
+  extern __shared__ __align__(1024) unsigned char dsmem[];
+  unsigned char* const pbase = SM::STATIC ? s_pool : dsmem;
+  T* const pools = reinterpret_cast<T*>(pbase);
+  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::BUFS * BUF));
+  __shared__ SState s;
+  __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
+  __shared__ __align__(16) float s_hs[64];  // sign mask -> (0.5*sign_k)_k (transforms.cpp:88)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t b0 = warp * J * 32 + lane;  // first 4-block of this thread
+  const bool compute = !G::CHAINW || tid < G::CT;  // owns 4-blocks (else: chain warp)
+  const uint64_t pool = blockIdx.x;
+  const bool mean_zero = a.mean_is_zero != 0;
+  const T mean_t = from_double<T>(a.mean);
+
+  // ---- prologue: state, pool, plans ----------------------------------------
+  if (tid == 0) {
+    const PoolState& st = a.st_in[pool];
+    s.reserved_prev = st.reserved_prev;
+    s.sum_sq = st.sum_sq;
+    s.cur_scale = st.scale;
+    s.last_chi2 = st.last_chi2;
+    s.last_r = st.r;
+    s.last_scale = st.scale;
+    s.clamp = 0;
+    s.zero_seen = 0;
+    s.ready = 0;
+    s.flags = st.flags;
+    if (MODE != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
+  }
+  if constexpr (MODE == kModeConsume)
+    for (int i = tid; i < 258; i += THREADS) s_hist[i] = 0;
+  for (int i = tid; i < 64; i += THREADS) s_hs[i] = ((i >> 2) >> (i & 3)) & 1 ? -0.5f : 0.5f;
+  {
+    const float4* src = reinterpret_cast<const float4*>(static_cast<const T*>(a.pools_in) + pool * N);
+    float4* dst = reinterpret_cast<float4*>(pools);
+    constexpr int NV = N * sizeof(T) / 16;
+    for (int i = tid; i < NV; i += THREADS) dst[i] = __ldcs(src + i);
+  }
+  for (uint32_t i = tid; i < a.n_passes * PW; i += THREADS) s_plans[i] = a.plans[pool * a.plan_stride + i];
+  const uint64_t pass0 = a.st_in[pool].pass_count;
+  const uint32_t cursor0 = a.st_in[pool].cursor;
+  __syncthreads();
+
+  T* const out_pool = static_cast<T*>(a.out) + pool * a.out_stride + a.out_offset;
+  Consumer<T> cons;
+  cons.hist = s_hist;
+
+  // ---- drain the partially consumed emission --------------------------------
+  if (MODE != kModePasses && a.lead > 0) {
+    const T sc = from_double<T>(s.cur_scale);
+    const bool mat = (s.flags & kFlagLeftover) != 0;
+    const T* lo = static_cast<const T*>(a.leftover) + pool * (N - 1);
+    for (uint32_t i = tid; i < a.lead; i += THREADS) {
+      const uint32_t idx = cursor0 + i;
+      const T v = mat ? lo[idx] : emit_value(pools[idx], sc, mean_t, mean_zero);
+      if constexpr (MODE == kModeConsume) cons.add(v);
+      else stg1(out_pool + i, v);
+    }
+    if constexpr (MODE == kModeConsume) cons.flush();
+  }
+
+  const char* const cbase = reinterpret_cast<const char*>(pbase);
+  uint32_t cur_off = 0;
+  uint32_t pc = static_cast<uint32_t>(pass0 + 1) & 255u;  // pass count after the next pass, mod 256
+  uint32_t p = 0;                                          // plan index
+
+  if constexpr (MODE == kModePasses) {
+    for (; p < a.n_passes; ++p) {
+      const uint32_t plan_p = s_plans[p * PW];
+      if (compute) {
+        for (int c0 = 0; c0 < J; c0 += G::JC) {
+          T X[G::JC][4];
+          if constexpr (ROT)
+            run_pass_rot<T, LOG2N, G::JC, PT & 1>(cbase, cur_off, cur_off ^ FLIP, plan_p, s_plans[p * PW + 1],
+                                                  b0 + 32 * c0, X, a.rot_c, a.rot_s);
+          else
+            run_pass<T, LOG2N, G::JC, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+        }
+      }
+      __syncthreads();
+      cur_off ^= PFLIP;
+      if (pc == 0) renormalize<T, N, THREADS, G::LAT>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
+      pc = (pc + 1) & 255u;
+    }
+  } else {
+    uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
+    // bulk-store geometry (see "Bulk (TMA) emission"): boxes cover pool
+    // elements [0, TMA_ELEMS); 4-blocks from TAIL_B on go through registers
+    constexpr int TMA_ELEMS = ((N - 1) / kTmaBox) * kTmaBox;
+    constexpr int TAIL_B = TMA_ELEMS / 4;
+    constexpr bool TMA_GEOM = MODE == kModeFill && FAST && !G::LAT && TMA_ELEMS > 0 && TAIL_B % 32 == 0;
+    // groups of the last warp at or past TAIL_B (the tail is in the last warp)
+    constexpr int TAIL_J = TMA_GEOM ? (TAIL_B - (G::NW - 1) * J * 32) / 32 : 0;
+    static_assert(!TMA_GEOM || (TAIL_J >= 0 && TAIL_J < J), "tail must sit in the last warp");
+    bool bulk_pending = false;
+    T* gbase = out_pool + a.lead;  // element 0 of the current emission
+    for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
+      const int slot = e & 1;
+      const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
+      for (uint32_t q = 1; q <= a.d; ++q, ++p) {
+        const bool emit_pass = q == a.d;
+        const bool renorm_now = pc == 0;
+        const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
+        // the emission scale is final before this pass (published behind at
+        // least one barrier); load it up front so its latency hides
+        const double scd = WB_PREFETCH ? s.scale[slot] : 0.0;
+        if (!WB_PREFETCH || ROT) plan = s_plans[p * PW];
+        const uint32_t plan_p = plan;
+        const uint32_t plan_q = ROT ? s_plans[p * PW + 1] : 0u;  // rotation: sweep-1 word
+        if (WB_PREFETCH && !ROT) plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
+        const bool do_emit = fast && WB_ABLATE != 1 && WB_ABLATE != 4;
+        T sc = T(0);
+        uint32_t delta = 0;
+        if (do_emit) {
+          sc = from_double<T>(WB_PREFETCH ? scd : s.scale[slot]);
+          delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
+                  (G::VEC - 1);
+        }
+        // the pool itself is the emission: bulk stores from shared memory
+        // (tensor stores need 16-byte-aligned coordinates: only emissions that
+        // start aligned, delta == 0, go out this way)
+        const bool bulk = TMA_GEOM && WB_TMA && do_emit && a.tma_ok && mean_zero && sc == T(1) && delta == 0;
+        bool zero_seen = false;
+        T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
+        T x_last = T(0);
+        if (G::CHAINW && do_emit && compute) {
+          // S/r/scale of emission e come from the chain warp: one lane per
+          // warp polls (acquire), __syncwarp orders the other lanes' reads
+          if (lane == 0)
+            while (ld_acquire_cta(&s.ready) < e) __nanosleep(32);
+          __syncwarp();
+          sc = from_double<T>(*static_cast<volatile double*>(&s.scale[slot]));
+        }
+        // chunk of 4-blocks held in registers at a time (half chunks for the
+        // consumer remove its spills but cost a second permutation dispatch
+        // per pass: measured slower)
+        constexpr int JCL = G::JC;
+        for (int c0 = 0; c0 < J && compute; c0 += JCL) {
+          T X[JCL][4];
+          if constexpr (ROT)
+            run_pass_rot<T, LOG2N, JCL, PT & 1>(cbase, cur_off, cur_off ^ FLIP, plan_p, plan_q, b0 + 32 * c0, X,
+                                                a.rot_c, a.rot_s);
+          else
+            run_pass<T, LOG2N, JCL, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+          if (do_emit) {
+            if constexpr (MODE == kModeFill) {
+              if (bulk) {
+#pragma unroll
+                for (int jj = 0; jj < G::JC; ++jj)
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) zero_seen |= X[jj][k] == T(0);
+                if (warp == G::NW - 1 && c0 + G::JC > TAIL_J)
+                  emit_chunk_any<T, LOG2N>(delta, true, X, c0, prev, gbase, sc, mean_t, lane, warp, TAIL_J);
+              } else {
+                emit_chunk_any<T, LOG2N>(delta, mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
+              }
+            } else {
+              consume_chunk<T, LOG2N, JCL>(X, cons, sc, mean_t, mean_zero, b0 + 32 * c0);
+            }
+          }
+          x_last = X[JCL - 1][3];
+        }
+        if constexpr (MODE == kModeConsume)
+          if (do_emit) cons.flush();
+        if (bulk) {
+          fence_proxy_async_smem();  // this thread's pool stores -> visible to the bulk copies
+          if (zero_seen) s.zero_seen = 1;
+        }
+        if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3) {
+          chain_close(s, slot, static_cast<double>(x_last));
+          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+        }
+        // the bulk copies of the previous emission must have read their
+        // source before this barrier releases the buffer for overwriting
+        if (bulk_pending && tid == 0) bulk_wait_read();
+        bulk_pending = false;
+#if WB_ABLATE == 4
+        // timing-only: the previous bulk store must have read its source
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+        __syncthreads();
+        cur_off ^= PFLIP;
+        T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+        if (G::CHAINW && fast && tid == G::CT) {
+          // generator.cpp:373-375 for emission e, then S/r/scale of e+1; the
+          // compute warps pick them up at emission e+1 (acquire on s.ready)
+          chain_close(s, slot, static_cast<double>(cur[N - 1]));
+          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+          st_release_cta(&s.ready, e + 1);
+        }
+        if (bulk) {
+          if (tid == 0) {
+            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
+            const int x0 = static_cast<int>(a.out_offset + a.lead + uint64_t(e) * (N - 1));
+#pragma unroll 1
+            for (int k = 0; k < TMA_ELEMS / kTmaBox; ++k)
+              tma_store_2d(&a.tmap, src + k * kTmaBox * sizeof(T), x0 + k * kTmaBox, static_cast<int>(pool));
+            bulk_commit();
+          }
+          bulk_pending = true;
+          if (s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk stores landed
+            if (tid == 0) {
+              bulk_wait_all();
+              fence_proxy_async_global();
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < uint32_t(TMA_ELEMS); i += THREADS)
+              if (cur[i] == T(0) && signbit(cur[i])) stg1(gbase + i, T(0));
+            __syncthreads();
+            if (tid == 0) s.zero_seen = 0;
+            __syncthreads();
+          }
+        }
+#if WB_ABLATE == 4
+        // timing-only: emission as one bulk (TMA) store of the pool buffer to an
+        // aligned-down address (wrong output; measures the store-path cost)
+        if (fast && tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const unsigned long long dst = reinterpret_cast<unsigned long long>(gbase) & ~15ull;
+          const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                       "r"(uint32_t((N - 1) * sizeof(T)) & ~15u)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+#endif
+        if (renorm_now) {
+          if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
+          renormalize<T, N, THREADS, G::LAT>(cur, s, tid);
+          // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
+          if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
+          __syncthreads();
+        }
+        if (emit_pass && !fast) {
+          // slow emission from shared memory: the partial last emission, an
+          // emission right after a renormalisation, pools below 128 values
+          const T sc = from_double<T>(s.scale[slot]);
+          for (uint32_t i = tid; i < limit; i += THREADS) {
+            const T v = emit_value(cur[i], sc, mean_t, mean_zero);
+            if constexpr (MODE == kModeConsume) cons.add(v);
+            else stg1(gbase + i, v);
+          }
+          if constexpr (MODE == kModeConsume) cons.flush();
+          if (tid == 0) {
+            chain_close(s, slot, static_cast<double>(cur[N - 1]));
+            if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+            s.ready = e + 1;
+          }
+          __syncthreads();
+        }
+        pc = (pc + 1) & 255u;
+      }
+    }
+    if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
+    if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
+  }
+#if WB_ABLATE == 4
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncthreads();
+#endif
+  T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+
+  // ---- epilogue: pool and state back to HBM ---------------------------------
+  {
+    float4* dst = reinterpret_cast<float4*>(static_cast<T*>(a.pools_out) + pool * N);
+    const float4* src = reinterpret_cast<const float4*>(cur);
+    constexpr int NV = N * sizeof(T) / 16;
+    for (int i = tid; i < NV; i += THREADS) dst[i] = src[i];
+  }
+  if constexpr (MODE == kModeConsume) {
+    // fixed-order block reduction of the moment sums
+    __shared__ double s_red[4][32];
+    double v[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] = __dadd_rn(v[k], __shfl_down_sync(0xffffffffu, v[k], o));
+    }
+    if (lane == 0)
+      for (int k = 0; k < 4; ++k) s_red[k][warp] = v[k];
+    __syncthreads();
+    if (tid < 4) {
+      double acc = 0.0;
+      for (int w = 0; w < G::NW; ++w) acc = __dadd_rn(acc, s_red[tid][w]);
+      a.part_sums[pool * 4 + tid] = acc;
+    }
+    for (int i = tid; i < 258; i += THREADS) a.part_hist[pool * 258 + i] = s_hist[i];
+  }
+  if (tid == 0) {
+    PoolState& so = a.st_out[pool];
+    so.reserved_prev = s.reserved_prev;
+    so.sum_sq = s.sum_sq;
+    so.pass_count = pass0 + a.n_passes;
+    so.clamp_count = a.st_in[pool].clamp_count + s.clamp;
+    uint32_t flags = s.flags;
+    so.scale = s.last_scale;
+    so.r = s.last_r;
+    so.last_chi2 = s.last_chi2;
+    if (MODE != kModePasses && a.n_emit > 0) {
+      so.cursor = a.last_limit;
+      flags &= ~kFlagLeftover;
+    } else {
+      so.cursor = cursor0 + (MODE != kModePasses ? a.lead : 0);
+    }
+    so.flags = flags;
+    so.seed = a.st_in[pool].seed;
+    if (a.n_passes == 0 && &so != &a.st_in[pool]) {  // no plan launch copied the stream
+      for (int k = 0; k < 4; ++k) so.s[k] = a.st_in[pool].s[k];
+      so.draws = a.st_in[pool].draws;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-callable launch table
+// ---------------------------------------------------------------------------
+template <typename T, int LOG2N, int MODE, int PT>
+cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
+  using SM = Smem<T, LOG2N>;
+  constexpr size_t PW = PT >= 2 ? 2 : 1;
+  const size_t plans = (a.n_passes * 4 * PW + 15) & ~size_t(15);
+  const size_t smem = (SM::STATIC ? 0 : SM::BUFS * size_t(SM::BUF)) + plans;
+  auto fn = pool_kernel<T, LOG2N, MODE, PT>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(SM::STATIC ? 16 * 1024 : SM::BUFS * SM::BUF + 16 * 1024));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  fn<<<dim3(unsigned(n_pools)), dim3(Geo<T, LOG2N>::THREADS), smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, int LOG2N, int PT>
+cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
+  switch (a.mode) {
+    case kModeFill: return launch_pool_mode<T, LOG2N, kModeFill, PT>(a, n_pools, stream);
+    case kModePasses: return launch_pool_mode<T, LOG2N, kModePasses, PT>(a, n_pools, stream);
+    default: return launch_pool_mode<T, LOG2N, kModeConsume, PT>(a, n_pools, stream);
+  }
+}
+
+template <typename T, int PT>
+cudaError_t launch_pool_dispatch(int log2n, const FillArgs& a, uint64_t n_pools, cudaStream_t s) {
+  switch (log2n) {
+    // latency kernels (key log2(N) + 16)
+    case 16 + 8: return launch_pool<T, 16 + 8, PT>(a, n_pools, s);
+    case 16 + 9: return launch_pool<T, 16 + 9, PT>(a, n_pools, s);
+    case 16 + 10: return launch_pool<T, 16 + 10, PT>(a, n_pools, s);
+    case 16 + 11: return launch_pool<T, 16 + 11, PT>(a, n_pools, s);
+    case 16 + 12: return launch_pool<T, 16 + 12, PT>(a, n_pools, s);
+    case 16 + 13: return launch_pool<T, 16 + 13, PT>(a, n_pools, s);
+    case 16 + 14:
+      if constexpr (sizeof(T) == 4) return launch_pool<T, 16 + 14, PT>(a, n_pools, s);
+      else return cudaErrorInvalidValue;
+    case 5: return launch_pool<T, 5, PT>(a, n_pools, s);
+    case 6: return launch_pool<T, 6, PT>(a, n_pools, s);
+    case 7: return launch_pool<T, 7, PT>(a, n_pools, s);
+    case 8: return launch_pool<T, 8, PT>(a, n_pools, s);
+    case 9: return launch_pool<T, 9, PT>(a, n_pools, s);
+    case 10: return launch_pool<T, 10, PT>(a, n_pools, s);
+    case 11: return launch_pool<T, 11, PT>(a, n_pools, s);
+    case 12: return launch_pool<T, 12, PT>(a, n_pools, s);
+    case 13: return launch_pool<T, 13, PT>(a, n_pools, s);
+    case 14:
+      if constexpr (sizeof(T) == 4) return launch_pool<T, 14, PT>(a, n_pools, s);
+      else return cudaErrorInvalidValue;
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// one translation unit per pass type (pool_pt<PT>.cu) defines this
+template <int PT>
+cudaError_t launch_pool_pt(int dtype, int log2n, const FillArgs& a, uint64_t n_pools, cudaStream_t s);
+
+}  // namespace wb

@@ -15,8 +15,8 @@
 
 // ---- the reference library, through the test shim (oracle/ref_shim.cpp) ----
 extern "C" {
-void* ref_create(uint64_t pool_size, int chi2_method, uint64_t discard_every, double mean,
-                 double sigma, uint64_t seed, int fixed, int disable_chi2);
+void* ref_create_ex(uint64_t pool_size, int chi2_method, uint64_t discard_every, double mean,
+                    double sigma, uint64_t seed, int fixed, int disable_chi2, int family, int mixing);
 void ref_destroy(void* g);
 int ref_fill(void* g, double* out, uint64_t count);
 double ref_next_normal(void* g);
@@ -66,8 +66,9 @@ static int g_checks = 0, g_fail = 0;
 struct Ref {
   void* g;
   explicit Ref(const wb::GeneratorConfig& c)
-      : g(ref_create(c.pool_size, static_cast<int>(c.chi2_method), c.discard_every, c.out_mean,
-                     c.out_sigma, c.seed, c.diag.fixed_transform, c.diag.disable_chi2)) {}
+      : g(ref_create_ex(c.pool_size, static_cast<int>(c.chi2_method), c.discard_every, c.out_mean,
+                        c.out_sigma, c.seed, c.diag.fixed_transform, c.diag.disable_chi2,
+                        static_cast<int>(c.transform_family), static_cast<int>(c.mixing))) {}
   ~Ref() { ref_destroy(g); }
   std::vector<double> fill(size_t n) {
     std::vector<double> v(n);
@@ -113,9 +114,27 @@ int main() {
     cfg.out_mean = 0.0;
     cfg.validate();
     CHECK_THROWS_AS(wb::Generator(cfg_of(48, 0)), wb::ConfigError);
-    wb::GeneratorConfig rot = cfg_of(128, 1);
-    rot.transform_family = wb::TransformFamily::rotation;
-    CHECK_THROWS_AS(wb::Generator(rot), wb::UnsupportedError);
+    // the on-chip pool limit (fp64 pools above 2^13) is the one reported
+    // UnsupportedError of the drop-in
+    CHECK_THROWS_AS(wb::Generator(cfg_of(1u << 14, 1)), wb::UnsupportedError);
+  }
+  // rotation family and affine mixing (generator.cpp:86-172): the same
+  // stream as the reference, through next_normal / fill / step_pass
+  for (int fm = 1; fm < 4; ++fm) {
+    wb::GeneratorConfig c = cfg_of(256, 7 + fm);
+    c.transform_family = fm >= 2 ? wb::TransformFamily::rotation : wb::TransformFamily::wallace4;
+    c.mixing = (fm & 1) ? wb::MixingScheme::affine : wb::MixingScheme::stride_transpose;
+    c.discard_every = 2;
+    wb::Generator g(c);
+    Ref r(c);
+    CHECK(same_bits(g.fill(5000), r.fill(5000)));
+    bool nn = true;
+    std::vector<double> rn = r.fill(300);
+    for (int i = 0; i < 300; ++i) nn = nn && g.next_normal() == rn[i];
+    CHECK(nn);
+    g.step_pass();
+    ref_step_pass(r.g);
+    CHECK(same_bits(g.fill(1000), r.fill(1000)));
   }
   // :74-82 identical config gives a bit-identical stream (and == reference)
   {

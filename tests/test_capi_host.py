@@ -96,7 +96,34 @@ def test_host_seeding_matches_reference_polar(ref, n, seed):
     assert dr.value + 32 == g.stats()["uniform_draws"]
 
 
-def test_unsupported_options_are_explicit():
-    for kw in (dict(transform_family=1), dict(mixing=1)):
-        cfg = pb.GeneratorConfig(**kw)
-        cfg.validate()  # valid in the reference
+def test_rotation_and_affine_configs_are_valid():
+    for kw in (dict(transform_family=1), dict(mixing=1), dict(transform_family=1, mixing=1)):
+        pb.GeneratorConfig(**kw).validate()  # valid in the reference and built here
+
+
+def test_rotation_table_vs_reference(ref):
+    """The host computes the 16-entry table from its construction
+    (transforms.cpp:39-70); it must equal the reference's bit for bit."""
+    L, R = _capi.load(), ref.ref_lib()
+    t1, c1, s1 = (C.c_double * 16)(), (C.c_double * 16)(), (C.c_double * 16)()
+    t2, c2, s2 = (C.c_double * 16)(), (C.c_double * 16)(), (C.c_double * 16)()
+    L.wallace_rotation_table(t1, c1, s1)
+    R.ref_rotation_table(t2, c2, s2)
+    assert list(t1) == list(t2) and list(c1) == list(c2) and list(s1) == list(s2)
+
+
+@pytest.mark.parametrize("fam,mix", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_plan_decode_ex_vs_reference(ref, fam, mix):
+    L, R = _capi.load(), ref.ref_lib()
+    rng = np.random.default_rng(5)
+    for n in (32, 1024, 4096, 16384):
+        cfg = pb.GeneratorConfig(pool_size=n, transform_family=fam, mixing=mix).to_c()
+        for _ in range(200):
+            w0, w1 = (int(x) for x in rng.integers(0, 2**64, 2, dtype=np.uint64))
+            got = _capi.wallace_pass_plan()
+            assert L.wallace_decode_pass_plan_ex(C.byref(cfg), w0, w1, C.byref(got)) == 0
+            ints, offs = (C.c_int32 * 5)(), (C.c_uint64 * 2)()
+            R.ref_decode_pass_plan_ex(n, fam, mix, w0, w1, ints, offs)
+            assert (got.wallace_variant, got.t_index[0], got.t_index[1], got.negate[0],
+                    got.negate[1]) == tuple(ints)
+            assert (got.offset[0], got.offset[1]) == tuple(offs)
