@@ -44,6 +44,17 @@ CONFIGS = {
     5: dict(name="cfg5: 65536 pools x N=1024 fp32, 1 pass/output, cubic_a, 2^34 variates consumed in-kernel",
             kw=dict(pool_size=1024, discard_every=1), pools=65536, count=1 << 18, dtype="f32",
             consume=True),
+    # the other GeneratorConfig axes on config 2's shape (not BASELINE lines):
+    # wallace4 + affine mixing, rotation + stride_transpose, rotation + affine
+    6: dict(name="cfg2 shape, wallace4 + affine mixing: 16384 pools x N=4096 fp32, d=2, no chi2",
+            kw=dict(pool_size=4096, discard_every=2, disable_chi2=True, mixing=1), pools=16384,
+            count=1 << 18, dtype="f32"),
+    7: dict(name="cfg2 shape, rotation + stride_transpose: 16384 pools x N=4096 fp32, d=2, no chi2",
+            kw=dict(pool_size=4096, discard_every=2, disable_chi2=True, transform_family=1),
+            pools=16384, count=1 << 18, dtype="f32"),
+    8: dict(name="cfg2 shape, rotation + affine mixing: 16384 pools x N=4096 fp32, d=2, no chi2",
+            kw=dict(pool_size=4096, discard_every=2, disable_chi2=True, transform_family=1, mixing=1),
+            pools=16384, count=1 << 18, dtype="f32"),
 }
 METRIC = "normal variates/sec at 1 B200 and % of HBM write roofline vs CPU ref"
 UNIT = "variates/s"
@@ -136,9 +147,10 @@ def cpu_reference_run(cfg, n_pools, count, threads, seed_base=1):
     L = oracle.ref_lib()
     ti, tf = C.c_double(), C.c_double()
     kw = cfg["kw"]
-    L.ref_run_job(kw["pool_size"], kw.get("chi2_method", 2), kw["discard_every"],
-                  int(kw.get("disable_chi2", False)), seed_base, n_pools, count, threads,
-                  C.byref(ti), C.byref(tf))
+    L.ref_run_job_ex(kw["pool_size"], kw.get("chi2_method", 2), kw["discard_every"],
+                     int(kw.get("disable_chi2", False)), kw.get("transform_family", 0),
+                     kw.get("mixing", 0), seed_base, n_pools, count, threads, C.byref(ti),
+                     C.byref(tf))
     return tf.value, ti.value
 
 

@@ -160,6 +160,9 @@ def ref_lib():
         L.ref_run_job.argtypes = [u64, C.c_int, u64, C.c_int, u64, u64, u64, C.c_int,
                                   P(f64), P(f64)]
         L.ref_run_job.restype = f64
+        L.ref_run_job_ex.argtypes = [u64, C.c_int, u64, C.c_int, C.c_int, C.c_int, u64, u64, u64,
+                                     C.c_int, P(f64), P(f64)]
+        L.ref_run_job_ex.restype = f64
         _ref = L
     return _ref
 

@@ -223,10 +223,23 @@ void ref_moments(const double* x, uint64_t n, double out[4]) {
 // bench chunking (bench.cpp:43-59), folded into a sink so no work is elided.
 // Each phase is timed by wall clock across all threads and summed over
 // batches.  Returns the sink.
+double ref_run_job_ex(uint64_t pool_size, int chi2_method, uint64_t discard_every,
+                      int disable_chi2, int family, int mixing, uint64_t seed_base,
+                      uint64_t n_pools, uint64_t count_per_pool, int threads,
+                      double* init_seconds, double* fill_seconds);
+
 double ref_run_job(uint64_t pool_size, int chi2_method, uint64_t discard_every,
                    int disable_chi2, uint64_t seed_base, uint64_t n_pools,
                    uint64_t count_per_pool, int threads, double* init_seconds,
                    double* fill_seconds) {
+  return ref_run_job_ex(pool_size, chi2_method, discard_every, disable_chi2, 0, 0, seed_base,
+                        n_pools, count_per_pool, threads, init_seconds, fill_seconds);
+}
+
+double ref_run_job_ex(uint64_t pool_size, int chi2_method, uint64_t discard_every,
+                      int disable_chi2, int family, int mixing, uint64_t seed_base,
+                      uint64_t n_pools, uint64_t count_per_pool, int threads,
+                      double* init_seconds, double* fill_seconds) {
   std::vector<double> sinks(static_cast<size_t>(threads), 0.0);
   double t_init = 0.0, t_fill = 0.0;
   const uint64_t batch = 1024;
@@ -250,7 +263,7 @@ double ref_run_job(uint64_t pool_size, int chi2_method, uint64_t discard_every,
     const auto c0 = std::chrono::steady_clock::now();
     run([&](int, uint64_t p) {
       gens[p] = new maxent::Generator(to_cfg(pool_size, chi2_method, discard_every, 0.0, 1.0,
-                                             seed_base + b0 + p, 0, disable_chi2));
+                                             seed_base + b0 + p, 0, disable_chi2, family, mixing));
     });
     const auto c1 = std::chrono::steady_clock::now();
     run([&](int t, uint64_t p) {

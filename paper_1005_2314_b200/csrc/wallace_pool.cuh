@@ -718,6 +718,32 @@ struct Smem {
   static constexpr bool STATIC = BUFS * BUF <= 40 * 1024;
 };
 
+// Affine-mixing gathers without bank conflicts.  Lanes with consecutive
+// 4-blocks b read elements (off + (4b + c)*alpha) mod N; for a fixed column c
+// those are 4*alpha apart, so a warp would hit only 8 of the 32 banks (fp32;
+// 4 of 16 per half-warp for fp64).  Lane group g (lanes 8g..8g+7 for fp32,
+// 4g..4g+3 within each half-warp for fp64) reads column k ^ g in its k-th
+// load instead: 4*(b mod 8) + (k ^ g) covers every bank once.  The values
+// are then put back in column order with selects.
+template <typename T>
+__device__ __forceinline__ uint32_t affine_lane_group(uint32_t lane) {
+  return (lane >> (sizeof(T) == 4 ? 3 : 2)) & 3u;
+}
+template <typename T, uint32_t A, uint32_t MASKN>
+__device__ __forceinline__ void affine_gather4(const char* base, uint32_t buf, uint32_t e, uint32_t g,
+                                               T (&v)[4]) {
+  T L[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    L[k] = *reinterpret_cast<const T*>(base + (((e + (uint32_t(k) ^ g) * A) & MASKN) | buf));
+  const bool x1 = g & 1u, x2 = g & 2u;
+  const T t0 = x1 ? L[1] : L[0], t1 = x1 ? L[0] : L[1], t2 = x1 ? L[3] : L[2], t3 = x1 ? L[2] : L[3];
+  v[0] = x2 ? t2 : t0;
+  v[1] = x2 ? t3 : t1;
+  v[2] = x2 ? t0 : t2;
+  v[3] = x2 ? t1 : t3;
+}
+
 // One pass over the pool in shared memory (generator.cpp:64-85); leaves the
 // signed, permuted outputs of this thread's 4-blocks in X and stores them to
 // the next buffer.  sb = b0*STRIDE + off for this thread's first block.
@@ -815,10 +841,12 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
         // sequence sits at (off + (4b+c)*alpha) mod N
         constexpr uint32_t A = G::ALPHA * sizeof(T), MASKN = (G::N - 1) * sizeof(T);
         const uint32_t e = (off + 4u * (b0 + 32u * j) * G::ALPHA) * sizeof(T);
-        v0 = *reinterpret_cast<const T*>(base + ((e & MASKN) | cur_off));
-        v1 = *reinterpret_cast<const T*>(base + (((e + A) & MASKN) | cur_off));
-        v2 = *reinterpret_cast<const T*>(base + (((e + 2 * A) & MASKN) | cur_off));
-        v3 = *reinterpret_cast<const T*>(base + (((e + 3 * A) & MASKN) | cur_off));
+        T v[4];
+        affine_gather4<T, A, MASKN>(base, cur_off, e, affine_lane_group<T>(b0 & 31u), v);
+        v0 = v[0];
+        v1 = v[1];
+        v2 = v[2];
+        v3 = v[3];
       }
     }
     const T aa = add_rn(v0, v1);
@@ -943,10 +971,8 @@ __device__ __forceinline__ void run_pass_rot(const char* base, uint32_t cur_off,
 #pragma unroll
           for (int c = 0; c < 4; ++c) g[c] = ld(r + c * ROWS * ES, cur_off);
         } else {
-          constexpr uint32_t A = G::ALPHA * ES;
           const uint32_t e = (off + 4u * b * G::ALPHA) * ES;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) g[c] = ld((e + c * A) & MASKN, cur_off);
+          affine_gather4<T, G::ALPHA * ES, MASKN>(base, cur_off, e, affine_lane_group<T>(b0 & 31u), g);
         }
         store_block(nb, b, add_rn(mul_rn(ce, g[0]), mul_rn(se, g[1])),
                     add_rn(mul_rn(nse, g[0]), mul_rn(ce, g[1])),
@@ -979,10 +1005,19 @@ __device__ __forceinline__ void run_pass_rot(const char* base, uint32_t cur_off,
         } else {
           constexpr uint32_t B = G::BETA * ES;
           const uint32_t e = (off + 4u * b * G::BETA) * ES;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) h[c] = ld((e + c * B) & MASKN, nxt_off);
-          hm = ld((e - B) & MASKN, nxt_off);
-          hp = ld((e + 4 * B) & MASKN, nxt_off);
+          const uint32_t lane = b0 & 31u;
+          affine_gather4<T, B, MASKN>(base, nxt_off, e, affine_lane_group<T>(lane), h);
+          if constexpr (ROWS >= 32) {
+            // the neighbours are the adjacent lanes' end values (lane 0 and
+            // lane 31 reach into the previous / next group: direct loads)
+            hm = __shfl_up_sync(0xffffffffu, h[3], 1);
+            hp = __shfl_down_sync(0xffffffffu, h[0], 1);
+            if (lane == 0) hm = ld((e - B) & MASKN, nxt_off);
+            if (lane == 31) hp = ld((e + 4 * B) & MASKN, nxt_off);
+          } else {
+            hm = ld((e - B) & MASKN, nxt_off);
+            hp = ld((e + 4 * B) & MASKN, nxt_off);
+          }
         }
         X[j][0] = add_rn(mul_rn(nse, hm), mul_rn(ce, h[0]));
         X[j][1] = add_rn(mul_rn(ce, h[1]), mul_rn(se, h[2]));
