@@ -10,7 +10,6 @@
 //               (decode_pass_plan, generator.cpp:238-257)
 #pragma once
 
-#include <cuda.h>  // CUtensorMap
 
 #include <cstdint>
 
@@ -59,6 +58,8 @@ enum Mode : int32_t {
   kModeFill = 0,     // emit into the caller's buffer
   kModePasses = 1,   // passes only (warm-up / step_pass)
   kModeConsume = 2,  // emit into fused moment/histogram consumer
+  kModeFillBulk = 3, // emit into the caller's buffer, every emission the pool
+                     // itself (scale 1, mean +0): bulk copies from shared memory
 };
 
 struct FillArgs {
@@ -76,7 +77,7 @@ struct FillArgs {
   uint32_t last_limit;    // values taken from the last emission (<= N-1)
   int32_t mode;
   int32_t mean_is_zero;   // out_mean == +0.0: x*scale+0 fused (bit-identical)
-  int32_t tma_ok;         // the output tensor map is valid for this launch
+  int32_t pad_ab;
   void* out;              // T, pool-major
   uint64_t out_stride;    // elements per pool slice
   uint64_t out_offset;    // element offset inside each slice
@@ -93,8 +94,6 @@ struct FillArgs {
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]
-  // 2-D tensor map of the output (count x n_pools) for bulk emissions
-  CUtensorMap tmap;
 };
 
 struct PlanArgs {

@@ -8,7 +8,6 @@
 // the reference uses (bit parity of the seeded pool); the 16 warm-up passes
 // then run on the device.  Seeding is spread over host threads, one pool at a
 // time per thread.
-#include <cuda.h>  // CUtensorMap / cuTensorMapEncodeTiled signature
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -16,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -184,42 +184,6 @@ int ilog2(uint64_t v) {
   return l;
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (the
-// library links cudart statically and never links libcuda directly).
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return static_cast<EncodeTiledFn>(nullptr);
-    return reinterpret_cast<EncodeTiledFn>(p);
-  }();
-  return fn;
-}
-
-// 2-D map of a pool-major output [n_pools][count], box 256 x 1, for the
-// bulk-store emission path.  False when the layout does not allow it
-// (alignment, stride, coordinate range); the kernel then emits from registers.
-bool make_output_map(CUtensorMap* map, void* out, uint64_t count, uint64_t n_pools, size_t esize) {
-  if (!out || (reinterpret_cast<uintptr_t>(out) & 15) || (count * esize) % 16 || count >= (1ull << 31) ||
-      n_pools >= (1ull << 31) || count < 256)
-    return false;
-  const EncodeTiledFn fn = encode_tiled();
-  if (!fn) return false;
-  const cuuint64_t dims[2] = {count, n_pools};
-  const cuuint64_t strides[1] = {count * esize};
-  const cuuint32_t box[2] = {256, 1};
-  const cuuint32_t estr[2] = {1, 1};
-  return fn(map, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out,
-            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 constexpr uint64_t kPlanBudgetBytes = 128ull << 20;
 constexpr uint32_t kMaxPassesPerLaunch = 2048;
 constexpr uint64_t kMagic = 0x5741'4c4c'4143'4531ull;  // "WALLACE1"
@@ -248,6 +212,7 @@ struct wallace_handle {
   cudaEvent_t ev_start = nullptr, ev_planned[2] = {nullptr, nullptr}, ev_pooled[2] = {nullptr, nullptr};
   int key = 0;        // kernel key: log2(N) (+16 for the latency kernel)
   int kmode = 0;      // 0 auto, 1 throughput, 2 latency
+  bool bulk_ok = false;  // fills may use the bulk-emission kernel
   void* d_leftover = nullptr;
   void* d_snap_pools = nullptr;
   PoolState* d_snap_state = nullptr;
@@ -493,15 +458,13 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
   const uint64_t d = h->cfg.discard_every;
   uint64_t produced = 0;
   bool first = true;
-  CUtensorMap tmap;
-  std::memset(&tmap, 0, sizeof(tmap));
-  const bool tma_ok = mode == wb::kModeFill && make_output_map(&tmap, out, count, h->n_pools, h->esize);
   std::vector<Launch> ls;
   while (produced < count) {
     wb::FillArgs a = base_args(h);
-    a.tma_ok = tma_ok ? 1 : 0;
-    a.tmap = tmap;
     a.mode = mode;
+    // every emission is the pool itself (scale exactly 1, mean +0): the
+    // bulk-emission kernel (throughput geometry, wallace4 passes)
+    if (mode == wb::kModeFill && h->bulk_ok && h->key < 16 && h->log2n >= 7) a.mode = wb::kModeFillBulk;
     a.out = out;
     a.out_stride = count;
     a.out_offset = produced;
@@ -725,6 +688,13 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
     WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_pooled[i], cudaEventDisableTiming));
   }
   select_kernel(h);
+  {
+    // disable_chi2 makes S = sum_sq, so r = S/sum_sq = 1 and scale = sigma
+    // exactly; with sigma 1 and mean +0 each emitted value is x*1+0
+    const char* nb = std::getenv("WALLACE_B200_NO_BULK");
+    h->bulk_ok = cfg->disable_chi2 && cfg->out_sigma == 1.0 && cfg->out_mean == 0.0 &&
+                 !std::signbit(cfg->out_mean) && h->pass_type < 2 && !(nb && nb[0] == '1');
+  }
   WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,
                             h->stream));
   WB_CUDA_C(cudaMemcpyAsync(h->d_state, states.data(), n_pools * sizeof(PoolState),
@@ -951,6 +921,9 @@ wallace_status wallace_inject_pool(wallace_handle* h, uint64_t pool, const doubl
     std::memcpy(buf.data(), values, n * sizeof(double));
     ss = neumaier_sq(values, n);
   }
+  // a non-finite pool makes the emission scale NaN instead of exactly 1:
+  // no bulk emissions for this handle from now on
+  if (!std::isfinite(ss)) h->bulk_ok = false;
   WB_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(h->d_pools) + pool * h->N * h->esize,
                           buf.data(), buf.size(), cudaMemcpyHostToDevice, h->stream));
   WB_CUDA(cudaMemcpyAsync(&h->d_state[pool].sum_sq, &ss, sizeof(double), cudaMemcpyHostToDevice,
@@ -1032,6 +1005,24 @@ wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint6
     return fail(WALLACE_ERR_INVALID_PARAM, "load_state: image does not match this handle");
   p += 64;
   const size_t pb = h->n_pools * h->N * h->esize;
+  if (h->bulk_ok) {  // see wallace_inject_pool: bulk emissions need finite pools
+    const uint64_t cnt = h->n_pools * h->N;
+    bool finite = true;
+    if (h->dtype == WALLACE_F32) {
+      for (uint64_t i = 0; i < cnt && finite; ++i) {
+        float v;
+        std::memcpy(&v, p + i * 4, 4);
+        finite = std::isfinite(v);
+      }
+    } else {
+      for (uint64_t i = 0; i < cnt && finite; ++i) {
+        double v;
+        std::memcpy(&v, p + i * 8, 8);
+        finite = std::isfinite(v);
+      }
+    }
+    if (!finite) h->bulk_ok = false;
+  }
   WB_CUDA(cudaMemcpyAsync(h->d_pools, p, pb, cudaMemcpyHostToDevice, h->stream));
   p += pb;
   WB_CUDA(cudaMemcpyAsync(h->d_state, p, h->n_pools * sizeof(PoolState), cudaMemcpyHostToDevice,

@@ -14,7 +14,6 @@
 // compiled with -fmad=false, so no multiply-add is contracted — the
 // reference pins -ffp-contract=off for the same reason
 // (/root/reference/proj/CMakeLists.txt:10-14).
-#include <cuda.h>  // CUtensorMap (the map itself is encoded on the host)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -104,10 +103,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_PACKED
 #define WB_PACKED 0
 #endif
-// 1: bulk (TMA) emission when the emission is the pool itself (scale 1, mean +0)
-// and starts 16-byte aligned
-#ifndef WB_TMA
-#define WB_TMA 0
+// 1: the host uses the bulk-emission kernel (cp.async.bulk from a shifted
+// shared buffer) when every emission is the pool itself (scale 1, mean +0)
+#ifndef WB_BULK
+#define WB_BULK 1
 #endif
 // 1: emission stores at one base register + immediate group offsets
 #ifndef WB_EMIT_IMM
@@ -301,6 +300,19 @@ __device__ __forceinline__ void stg_vec_at(uint64_t base, const double* v) {
 }
 #if WB_ABLATE == 2
 #define stg_vec(p, v) do { if (reinterpret_cast<uintptr_t>(p) == 1) stg_vec(p, v); } while (0)
+#endif
+#if WB_ABLATE == 6
+// timing-only: no global stores; the values stay live through an XOR fold
+// (one conditional store per emission chunk keeps the fold itself alive)
+__device__ uint32_t g_ablate_sink;
+__device__ __forceinline__ uint32_t ablate_fold(const float* v) {
+  return __float_as_uint(v[0]) ^ __float_as_uint(v[1]) ^ __float_as_uint(v[2]) ^ __float_as_uint(v[3]);
+}
+__device__ __forceinline__ uint32_t ablate_fold(const double* v) {
+  return __float_as_uint(float(v[0])) ^ __float_as_uint(float(v[1]));
+}
+__device__ __forceinline__ uint32_t ablate_fold1(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ uint32_t ablate_fold1(double v) { return __float_as_uint(float(v)); }
 #endif
 
 // ---------------------------------------------------------------------------
@@ -510,13 +522,50 @@ struct Consumer {
 // 0's head.  Lane 31's last group and lane 0's first head straddle two warps
 // and use scalar stores.  Element N-1 is never emitted (generator.cpp:366).
 // ---------------------------------------------------------------------------
-template <typename T, int LOG2N, int DELTA, bool MZ>
+#if WB_ABLATE == 6
+#define stg_vec(p, v) do { ablate_x ^= ablate_fold(v); } while (0)
+#define stg1(p, v) do { ablate_x ^= ablate_fold1(v); } while (0)
+#endif
+template <typename T>
+__device__ __forceinline__ bool is_neg_zero(T x) {
+  if constexpr (sizeof(T) == 4) return __float_as_uint(x) == 0x80000000u;
+  else return static_cast<unsigned long long>(__double_as_longlong(x)) == 0x8000000000000000ull;
+}
+
+// SMD (shared destination): instead of emitting y = x*scale + mean to global
+// memory, write the raw pool values x themselves -- all N of them, element
+// N-1 included -- into a shared buffer whose layout is shifted by the
+// emission's misalignment (see "Bulk emission"); zf collects whether any
+// value is an exact -0 (which the emission must turn into +0).
+template <typename T, int LOG2N, int DELTA, bool MZ, bool SMD = false>
 __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], int c0, T (&prev)[4],
                                            T* gbase, T sc, T mean, int lane, int warp,
-                                           int jfirst = 0) {
+                                           int jfirst = 0, uint32_t* zf = nullptr) {
   using G = Geo<T, LOG2N>;
   constexpr int J = G::J, JC = G::JC, VEC = G::VEC;
+  constexpr uint32_t NLIM = SMD ? G::N : G::N - 1;  // elements written
   static_assert(DELTA < VEC, "shift");
+#if WB_ABLATE == 6
+  uint32_t ablate_x = 0;
+  struct Flush {
+    uint32_t& x;
+    __device__ ~Flush() {
+      if (x == 0x9e3779b9u) g_ablate_sink = x;
+    }
+  } ablate_flush{ablate_x};
+#endif
+  auto put_vec = [&](T* p, const T* v) {
+    if constexpr (SMD) {
+      if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+      else *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    } else {
+      stg_vec(p, v);
+    }
+  };
+  auto put1 = [&](T* p, T v) {
+    if constexpr (SMD) *p = v;
+    else stg1(p, v);
+  };
   const bool l31 = lane == 31;
   const uint32_t b0 = warp * J * 32 + lane;  // this thread's block in group 0
   // Every lane's chunk of group j starts at cbase + 128 j elements: lanes
@@ -534,13 +583,21 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       else stg_vec_at<JJ * 128 * int(sizeof(T)) + 16>(cbase, c + 2);
     }
   };
+  (void)store_group;
+  uint32_t z = 0;
 #pragma unroll
   for (int jj = 0; jj < JC; ++jj) {
     const int j = c0 + jj;
     if (j < jfirst) continue;  // groups before jfirst are emitted elsewhere
     const uint32_t b = b0 + 32 * j;
     T y[4];
-    if constexpr ((WB_PACKED & 2) && MZ && sizeof(T) == 4) {
+    if constexpr (SMD) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y[k] = X[jj][k];
+        z |= is_neg_zero(y[k]) ? 1u : 0u;
+      }
+    } else if constexpr ((WB_PACKED & 2) && MZ && sizeof(T) == 4) {
       // (only the mean-zero form: ptxas contracts a packed mul.rn + add.rn
       // pair into one FFMA2 despite the explicit rounding modifiers)
       const uint64_t s2 = pk2(sc, sc);
@@ -551,7 +608,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
 #pragma unroll
       for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
     }
-    if constexpr (WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
+    if constexpr (!SMD && WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
       // global(4b) is 8-byte aligned: two float2 stores of the own block,
       // no neighbour values needed
       if (b != G::ROWS - 1) {
@@ -568,30 +625,30 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       // pool's last element X[N-1] = y[3] of block ROWS-1 falls outside
       const T s = __shfl_sync(0xffffffffu, y[3], (lane + 31) & 31);
       if (lane == 0 && j == jfirst) {  // head of this warp: the value before is the previous warp's
-        stg1(gbase + 4 * b + 0, y[0]);
-        stg1(gbase + 4 * b + 1, y[1]);
-        stg1(gbase + 4 * b + 2, y[2]);
+        put1(gbase + 4 * b + 0, y[0]);
+        put1(gbase + 4 * b + 1, y[1]);
+        put1(gbase + 4 * b + 2, y[2]);
       } else {
         const T c[4] = {lane == 0 ? prev[0] : s, y[0], y[1], y[2]};
-        stg_vec(gbase + 4 * b - 1, c);
+        put_vec(gbase + 4 * b - 1, c);
       }
-      if (lane == 31 && j == J - 1 && 4 * b + 3 < uint32_t(G::N - 1))
-        stg1(gbase + 4 * b + 3, y[3]);  // tail of this warp: the next warp's head is scalar
+      if (lane == 31 && j == J - 1 && 4 * b + 3 < NLIM)
+        put1(gbase + 4 * b + 3, y[3]);  // tail of this warp: the next warp's head is scalar
       prev[0] = s;
     } else if constexpr (DELTA == 0) {
-      if (b != G::ROWS - 1) {
-        if constexpr (WB_EMIT_IMM) {
+      if (SMD || b != G::ROWS - 1) {
+        if constexpr (WB_EMIT_IMM && !SMD) {
           static_for<JC>([&](auto jjc) {
             if (decltype(jjc)::value == jj) store_group(jjc, y);
           });
         } else {
 #pragma unroll
-          for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * b + v, y + v);
+          for (int v = 0; v < 4; v += VEC) put_vec(gbase + 4 * b + v, y + v);
         }
       } else {
-        stg1(gbase + 4 * b + 0, y[0]);
-        stg1(gbase + 4 * b + 1, y[1]);
-        stg1(gbase + 4 * b + 2, y[2]);
+        put1(gbase + 4 * b + 0, y[0]);
+        put1(gbase + 4 * b + 1, y[1]);
+        put1(gbase + 4 * b + 2, y[2]);
       }
     } else {
       T sh[DELTA];
@@ -604,41 +661,65 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         else c[m] = sh[(DELTA + m - 4) & (DELTA > 0 ? 3 : 0)];
       }
       if (!(l31 && j == jfirst)) {
-        if constexpr (WB_EMIT_IMM) {
+        if constexpr (WB_EMIT_IMM && !SMD) {
           static_for<JC>([&](auto jjc) {
             if (decltype(jjc)::value == jj) store_group(jjc, c);
           });
         } else {
           const uint32_t cb = l31 ? b - 32 : b;
 #pragma unroll
-          for (int v = 0; v < 4; v += VEC) stg_vec(gbase + 4 * cb + DELTA + v, c + v);
+          for (int v = 0; v < 4; v += VEC) put_vec(gbase + 4 * cb + DELTA + v, c + v);
         }
       }
       if (j == jfirst && lane == 0) {  // head of this warp's first block
 #pragma unroll
-        for (int t = 0; t < DELTA; ++t) stg1(gbase + 4 * b + t, y[t]);
+        for (int t = 0; t < DELTA; ++t) put1(gbase + 4 * b + t, y[t]);
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) prev[k] = y[k];
     }
   }
-  if constexpr (DELTA > 0 && !(WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) &&
+  if constexpr (DELTA > 0 && !(!SMD && WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) &&
                 !(WB_D3_DOWN && VEC == 4 && DELTA == 3)) {
     if (l31 && c0 + JC == J) {  // last group of the warp: own tail only, the head is the next warp's
       const uint32_t b = (warp * J + J - 1) * 32 + 31;
 #pragma unroll
       for (int m = DELTA; m < 4; ++m)
-        if (4 * b + m < uint32_t(G::N - 1)) stg1(gbase + 4 * b + m, prev[m]);
+        if (4 * b + m < NLIM) put1(gbase + 4 * b + m, prev[m]);
     }
   }
+  if constexpr (SMD) *zf |= z;
 }
 
+#if WB_ABLATE == 6
+#undef stg_vec
+#undef stg1
+#endif
 template <typename T, int LOG2N, int DELTA>
 __device__ __forceinline__ void emit_chunk_mz(bool mz, const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
                                               T (&prev)[4], T* gbase, T sc, T mean, int lane, int warp,
                                               int jfirst = 0) {
   if (mz) emit_chunk<T, LOG2N, DELTA, true>(X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
   else emit_chunk<T, LOG2N, DELTA, false>(X, c0, prev, gbase, sc, mean, lane, warp, jfirst);
+}
+
+// The shifted shared-memory write of an emission pass (bulk emission): the
+// raw values, dispatched on the shift.
+template <typename T, int LOG2N>
+__device__ __forceinline__ void shift_chunk_any(uint32_t delta, const T (&X)[Geo<T, LOG2N>::JC][4], int c0,
+                                                T (&prev)[4], T* sbase, int lane, int warp, uint32_t* zf) {
+  using G = Geo<T, LOG2N>;
+  if constexpr (G::VEC == 4) {
+    switch (delta) {
+      case 0: emit_chunk<T, LOG2N, 0, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf); break;
+      case 1: emit_chunk<T, LOG2N, 1 % G::VEC, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf); break;
+      case 2: emit_chunk<T, LOG2N, 2 % G::VEC, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf); break;
+      default: emit_chunk<T, LOG2N, 3 % G::VEC, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf); break;
+    }
+  } else {
+    if (delta == 0) emit_chunk<T, LOG2N, 0, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf);
+    else emit_chunk<T, LOG2N, 1, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf);
+  }
 }
 
 // Register emission of one chunk for any shift: dispatch on delta.
@@ -662,23 +743,22 @@ __device__ __forceinline__ void emit_chunk_any(uint32_t delta, bool mz,
 }
 
 // ---------------------------------------------------------------------------
-// Bulk (TMA) emission.  When an emission's scale is exactly 1 and the mean
-// is +0 (e.g. disable_chi2 with sigma 1 — BASELINE config 2), its values are
-// the pool itself, already in shared memory in pool order: out[i] = x[i]*1+0
-// = x[i] bit for bit, except that the reference's "+0" turns an exact -0 into
-// +0.  The emission is then issued as 2-D tensor stores of BOX elements from
-// the pool buffer (TMA takes arbitrary element coordinates, so the output's
-// misalignment costs nothing); the last (N-1) mod BOX + ... values, the
-// groups past the last full box, go through the register path; an exact zero
-// anywhere in the emission (probability ~1e-8 per value) triggers a patch
-// pass that rewrites -0 as +0 after the bulk stores have completed.
+// Bulk emission.  When an emission's scale is exactly 1 and the mean is +0
+// (disable_chi2 with sigma 1 makes r = S/sum_sq = 1 exactly -- BASELINE
+// config 2), out[i] = x[i]*1 + 0 is the pool value itself, bit for bit,
+// except that the "+0" turns an exact -0 into +0.  The emission pass then
+// writes its result into shared memory shifted by the output's misalignment
+// sigma (element i at slot i + sigma, so slot and global address agree mod
+// 16 bytes; the same shuffle realignment as the register emission), and one
+// thread sends the aligned middle of the emission to global memory with a
+// single cp.async.bulk while the next pass runs.  The <= 3 head and tail
+// values go out as scalar stores, and an exact -0 anywhere in the emission
+// (an exact cancellation in the butterfly, rare) triggers a patch that
+// rewrites it as +0 once the bulk copy has landed.  The next pass gathers
+// from the shifted buffer (the shift is part of its buffer base).
 // ---------------------------------------------------------------------------
-constexpr int kTmaBox = 256;  // elements per tensor-store box (TMA box dim limit)
-
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(x), "r"(y), "r"(smem)
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -715,7 +795,11 @@ struct Smem {
   // pools in static shared memory when they fit the 48 KiB static limit: the
   // buffer base then folds into the LDS/STS immediate offsets
   static constexpr int BUFS = Geo<T, LOG2N>::BUFS;
-  static constexpr bool STATIC = BUFS * BUF <= 40 * 1024;
+  // buffers sit BSTRIDE apart: 16 bytes of slack after each pool for the
+  // shifted layout of a bulk emission (up to 3 fp32 / 1 fp64 elements)
+  static constexpr uint32_t BSTRIDE = BUF + 16;
+  static constexpr uint32_t TOTAL = BUFS * BSTRIDE;
+  static constexpr bool STATIC = TOTAL <= 40 * 1024;
 };
 
 // Affine-mixing gathers without bank conflicts.  Lanes with consecutive
@@ -735,7 +819,7 @@ __device__ __forceinline__ void affine_gather4(const char* base, uint32_t buf, u
   T L[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
-    L[k] = *reinterpret_cast<const T*>(base + (((e + (uint32_t(k) ^ g) * A) & MASKN) | buf));
+    L[k] = *reinterpret_cast<const T*>(base + (((e + (uint32_t(k) ^ g) * A) & MASKN) + buf));
   const bool x1 = g & 1u, x2 = g & 2u;
   const T t0 = x1 ? L[1] : L[0], t1 = x1 ? L[0] : L[1], t2 = x1 ? L[3] : L[2], t3 = x1 ? L[2] : L[3];
   v[0] = x2 ? t2 : t0;
@@ -750,7 +834,7 @@ __device__ __forceinline__ void affine_gather4(const char* base, uint32_t buf, u
 template <typename T, int LOG2N, int J, int PT = 0>
 __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
                                          uint32_t plan, uint32_t b0, T (&X)[J][4],
-                                         const float* hs_lut) {
+                                         const float* hs_lut, bool store = true) {
   static_assert(PT == 0 || PT == 1, "wallace4 pass types");
   using G = Geo<T, LOG2N>;
   constexpr int ROWS = G::ROWS;
@@ -782,7 +866,7 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
       float v0 = 0, v1 = 0, v2 = 0, v3 = 0;
       if (ROWS >= 32 || b0 + 32 * j < ROWS) {
         constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
-        const float* row = reinterpret_cast<const float*>(base + (((r0 + j * step) & MASK4) | cur_off));
+        const float* row = reinterpret_cast<const float*>(base + (((r0 + j * step) & MASK4) + cur_off));
         v0 = row[0];
         v1 = row[ROWS];
         v2 = row[2 * ROWS];
@@ -814,6 +898,7 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
 #undef WB_PERM_CASE
     }
     if constexpr (G::INPLACE) __syncthreads();
+    if (!store) return;
     float* nb = reinterpret_cast<float*>(const_cast<char*>(base) + nxt_off);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -831,7 +916,7 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
     if (ROWS >= 32 || b0 + 32 * j < ROWS) {
       if constexpr (PT == 0) {
         constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
-        const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) | cur_off));
+        const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) + cur_off));
         v0 = row[0];
         v1 = row[ROWS];
         v2 = row[2 * ROWS];
@@ -878,6 +963,7 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
 #undef WB_PERM_CASE
   }
   if constexpr (G::INPLACE) __syncthreads();  // every gather of this pass is done
+  if (!store) return;  // the caller writes the shifted layout (bulk emission)
   T* nb = reinterpret_cast<T*>(const_cast<char*>(base) + nxt_off);
   if constexpr (sizeof(T) == 8) {
     // a 4-double block is 32 bytes: two 128-bit stores at a 32-byte lane
@@ -952,7 +1038,7 @@ __device__ __forceinline__ void run_pass_rot(const char* base, uint32_t cur_off,
     se = from_double<T>(neg ? -rs[t] : rs[t]);
   };
   auto ld = [&](uint32_t byte_off, uint32_t buf) -> T {
-    return *reinterpret_cast<const T*>(base + (byte_off | buf));
+    return *reinterpret_cast<const T*>(base + (byte_off + buf));
   };
   // ---- sweep 0 ----
   {
@@ -1053,9 +1139,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
   constexpr uint32_t BUF = SM::BUF;
   constexpr bool FAST = ROWS >= 32;
-  // buffer 0 at offset 0, buffer 1 at BUF (a power of two above every gather
-  // offset, so `| cur_off` selects the buffer); plans in dynamic smem
-  constexpr uint32_t FLIP = G::INPLACE ? 0u : BUF;  // cur_off ^ FLIP = next buffer
+  // buffer 0 at offset 0, buffer 1 at BSTRIDE; plans in dynamic smem
+  constexpr uint32_t FLIP = G::INPLACE ? 0u : SM::BSTRIDE;  // cur_off ^ FLIP = next buffer
   // rotation passes (PT 2, 3) use the other buffer as sweep scratch and end
   // in the current one; their plans are two words per pass
   constexpr bool ROT = PT >= 2;
@@ -1063,11 +1148,11 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   constexpr uint32_t PW = ROT ? 2u : 1u;
   static_assert(!ROT || (G::JC == G::J && !G::CHAINW && !G::INPLACE),
                 "rotation passes hold all 4-blocks of a thread across their inner barrier");
-  __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? SM::BUFS * BUF : 16];
+  __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? SM::TOTAL : 16];
   extern __shared__ __align__(1024) unsigned char dsmem[];
   unsigned char* const pbase = SM::STATIC ? s_pool : dsmem;
   T* const pools = reinterpret_cast<T*>(pbase);
-  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::BUFS * BUF));
+  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::TOTAL));
   __shared__ SState s;
   __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
   __shared__ __align__(16) float s_hs[64];  // sign mask -> (0.5*sign_k)_k (transforms.cpp:88)
@@ -1128,6 +1213,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
 
   const char* const cbase = reinterpret_cast<const char*>(pbase);
   uint32_t cur_off = 0;
+  uint32_t sh = 0;  // byte shift of the current buffer's layout (after a bulk emission pass)
   uint32_t pc = static_cast<uint32_t>(pass0 + 1) & 255u;  // pass count after the next pass, mod 256
   uint32_t p = 0;                                          // plan index
 
@@ -1151,14 +1237,11 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     }
   } else {
     uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
-    // bulk-store geometry (see "Bulk (TMA) emission"): boxes cover pool
-    // elements [0, TMA_ELEMS); 4-blocks from TAIL_B on go through registers
-    constexpr int TMA_ELEMS = ((N - 1) / kTmaBox) * kTmaBox;
-    constexpr int TAIL_B = TMA_ELEMS / 4;
-    constexpr bool TMA_GEOM = MODE == kModeFill && FAST && !G::LAT && TMA_ELEMS > 0 && TAIL_B % 32 == 0;
-    // groups of the last warp at or past TAIL_B (the tail is in the last warp)
-    constexpr int TAIL_J = TMA_GEOM ? (TAIL_B - (G::NW - 1) * J * 32) / 32 : 0;
-    static_assert(!TMA_GEOM || (TAIL_J >= 0 && TAIL_J < J), "tail must sit in the last warp");
+    // bulk emission (see "Bulk emission") for the throughput geometry
+    // bulk emission (its own instantiation: the register emission path is
+    // compiled out there, which keeps the general kernel's registers)
+    constexpr bool BULK_OK = MODE == kModeFillBulk;
+    static_assert(!BULK_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE), "bulk geometry");
     bool bulk_pending = false;
     T* gbase = out_pool + a.lead;  // element 0 of the current emission
     for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
@@ -1175,19 +1258,23 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         const uint32_t plan_p = plan;
         const uint32_t plan_q = ROT ? s_plans[p * PW + 1] : 0u;  // rotation: sweep-1 word
         if (WB_PREFETCH && !ROT) plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
-        const bool do_emit = fast && WB_ABLATE != 1 && WB_ABLATE != 4;
+        const bool do_emit = fast && WB_ABLATE != 1;
         T sc = T(0);
         uint32_t delta = 0;
         if (do_emit) {
           sc = from_double<T>(WB_PREFETCH ? scd : s.scale[slot]);
           delta = (G::VEC - (uint32_t)((reinterpret_cast<uintptr_t>(gbase) / sizeof(T)) & (G::VEC - 1))) &
                   (G::VEC - 1);
+#if WB_ABLATE == 5
+          delta = 0;  // timing-only: every emission aligned (stores at an aligned-down base)
+#endif
         }
-        // the pool itself is the emission: bulk stores from shared memory
-        // (tensor stores need 16-byte-aligned coordinates: only emissions that
-        // start aligned, delta == 0, go out this way)
-        const bool bulk = TMA_GEOM && WB_TMA && do_emit && a.tma_ok && mean_zero && sc == T(1) && delta == 0;
-        bool zero_seen = false;
+        // the emission is the pool itself: shifted shared write + bulk copy
+        const bool bulk = BULK_OK && do_emit;
+        // element shift of the layout this pass writes (bulk) so that slot
+        // and global address of every emitted element agree mod 16 bytes
+        const uint32_t sigma = (G::VEC - delta) & (G::VEC - 1);
+        uint32_t zf = 0;
         T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
         T x_last = T(0);
         if (G::CHAINW && do_emit && compute) {
@@ -1208,18 +1295,21 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             run_pass_rot<T, LOG2N, JCL, PT & 1>(cbase, cur_off, cur_off ^ FLIP, plan_p, plan_q, b0 + 32 * c0, X,
                                                 a.rot_c, a.rot_s);
           else
-            run_pass<T, LOG2N, JCL, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
+            run_pass<T, LOG2N, JCL, PT>(cbase, cur_off + sh, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs,
+                                        !bulk);
           if (do_emit) {
-            if constexpr (MODE == kModeFill) {
-              if (bulk) {
-#pragma unroll
-                for (int jj = 0; jj < G::JC; ++jj)
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) zero_seen |= X[jj][k] == T(0);
-                if (warp == G::NW - 1 && c0 + G::JC > TAIL_J)
-                  emit_chunk_any<T, LOG2N>(delta, true, X, c0, prev, gbase, sc, mean_t, lane, warp, TAIL_J);
+            if constexpr (MODE != kModeConsume) {
+              if constexpr (BULK_OK) {
+                T* sb = reinterpret_cast<T*>(pbase + (cur_off ^ FLIP)) + sigma;
+                shift_chunk_any<T, LOG2N>(delta, X, c0, prev, sb, lane, warp, &zf);
               } else {
+#if WB_ABLATE == 5
+                emit_chunk_any<T, LOG2N>(delta, mean_zero, X, c0, prev,
+                                         reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(gbase) & ~uintptr_t(15)),
+                                         sc, mean_t, lane, warp);
+#else
                 emit_chunk_any<T, LOG2N>(delta, mean_zero, X, c0, prev, gbase, sc, mean_t, lane, warp);
+#endif
               }
             } else {
               consume_chunk<T, LOG2N, JCL>(X, cons, sc, mean_t, mean_zero, b0 + 32 * c0);
@@ -1230,24 +1320,21 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         if constexpr (MODE == kModeConsume)
           if (do_emit) cons.flush();
         if (bulk) {
-          fence_proxy_async_smem();  // this thread's pool stores -> visible to the bulk copies
-          if (zero_seen) s.zero_seen = 1;
+          fence_proxy_async_smem();  // this thread's shared stores -> visible to the bulk copy
+          if (zf) s.zero_seen = 1;
         }
         if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3) {
           chain_close(s, slot, static_cast<double>(x_last));
           if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
         }
-        // the bulk copies of the previous emission must have read their
-        // source before this barrier releases the buffer for overwriting
+        // the bulk copy of the previous emission must have read its source
+        // before this barrier releases that buffer for overwriting
         if (bulk_pending && tid == 0) bulk_wait_read();
         bulk_pending = false;
-#if WB_ABLATE == 4
-        // timing-only: the previous bulk store must have read its source
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#endif
         __syncthreads();
         cur_off ^= PFLIP;
-        T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+        sh = bulk ? sigma * uint32_t(sizeof(T)) : 0u;
+        T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
         if (G::CHAINW && fast && tid == G::CT) {
           // generator.cpp:373-375 for emission e, then S/r/scale of e+1; the
           // compute warps pick them up at emission e+1 (acquire on s.ready)
@@ -1255,42 +1342,35 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
           st_release_cta(&s.ready, e + 1);
         }
-        if (bulk) {
+        if (BULK_OK && bulk) {
+          // the aligned middle [delta, delta + L) in one copy; the <= VEC-1
+          // head values [0, delta) and tail values [delta + L, N-1) as
+          // scalar stores of x*1 + 0
+          constexpr uint32_t NE = N - 1;
+          const uint32_t L = ((NE - delta) / G::VEC) * G::VEC;
           if (tid == 0) {
-            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
-            const int x0 = static_cast<int>(a.out_offset + a.lead + uint64_t(e) * (N - 1));
-#pragma unroll 1
-            for (int k = 0; k < TMA_ELEMS / kTmaBox; ++k)
-              tma_store_2d(&a.tmap, src + k * kTmaBox * sizeof(T), x0 + k * kTmaBox, static_cast<int>(pool));
+            bulk_s2g(gbase + delta, static_cast<uint32_t>(__cvta_generic_to_shared(cur + delta)),
+                     L * uint32_t(sizeof(T)));
             bulk_commit();
+          } else if (uint32_t(tid) <= NE - L) {
+            const uint32_t t = tid - 1;
+            const uint32_t i = t < delta ? t : L + t;
+            stg1(gbase + i, fma_rn(cur[i], T(1), T(0)));
           }
           bulk_pending = true;
-          if (s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk stores landed
+          if (s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk copy landed
             if (tid == 0) {
               bulk_wait_all();
               fence_proxy_async_global();
             }
             __syncthreads();
-            for (uint32_t i = tid; i < uint32_t(TMA_ELEMS); i += THREADS)
-              if (cur[i] == T(0) && signbit(cur[i])) stg1(gbase + i, T(0));
+            for (uint32_t i = delta + tid; i < delta + L; i += THREADS)
+              if (is_neg_zero(cur[i])) stg1(gbase + i, T(0));
             __syncthreads();
             if (tid == 0) s.zero_seen = 0;
             __syncthreads();
           }
         }
-#if WB_ABLATE == 4
-        // timing-only: emission as one bulk (TMA) store of the pool buffer to an
-        // aligned-down address (wrong output; measures the store-path cost)
-        if (fast && tid == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          const unsigned long long dst = reinterpret_cast<unsigned long long>(gbase) & ~15ull;
-          const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(cur));
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
-                       "r"(uint32_t((N - 1) * sizeof(T)) & ~15u)
-                       : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-#endif
         if (renorm_now) {
           if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
           renormalize<T, N, THREADS, G::LAT>(cur, s, tid);
@@ -1321,18 +1401,17 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
     if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
   }
-#if WB_ABLATE == 4
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  __syncthreads();
-#endif
-  T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+  T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
 
   // ---- epilogue: pool and state back to HBM ---------------------------------
-  {
+  if (sh == 0) {
     float4* dst = reinterpret_cast<float4*>(static_cast<T*>(a.pools_out) + pool * N);
     const float4* src = reinterpret_cast<const float4*>(cur);
     constexpr int NV = N * sizeof(T) / 16;
     for (int i = tid; i < NV; i += THREADS) dst[i] = src[i];
+  } else {  // the last pass was a bulk emission: shifted layout
+    T* dst = static_cast<T*>(a.pools_out) + pool * N;
+    for (int i = tid; i < N; i += THREADS) dst[i] = cur[i];
   }
   if constexpr (MODE == kModeConsume) {
     // fixed-order block reduction of the moment sums
@@ -1386,7 +1465,7 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
   using SM = Smem<T, LOG2N>;
   constexpr size_t PW = PT >= 2 ? 2 : 1;
   const size_t plans = (a.n_passes * 4 * PW + 15) & ~size_t(15);
-  const size_t smem = (SM::STATIC ? 0 : SM::BUFS * size_t(SM::BUF)) + plans;
+  const size_t smem = (SM::STATIC ? 0 : size_t(SM::TOTAL)) + plans;
   auto fn = pool_kernel<T, LOG2N, MODE, PT>;
   static bool configured = false;  // per instantiation
   if (!configured) {
@@ -1394,7 +1473,7 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
                                          cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(SM::STATIC ? 16 * 1024 : SM::BUFS * SM::BUF + 16 * 1024));
+                               int(SM::STATIC ? 16 * 1024 : SM::TOTAL + 16 * 1024));
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -1406,6 +1485,12 @@ template <typename T, int LOG2N, int PT>
 cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
   switch (a.mode) {
     case kModeFill: return launch_pool_mode<T, LOG2N, kModeFill, PT>(a, n_pools, stream);
+    case kModeFillBulk:
+      // the host selects it for the throughput geometry and wallace4 only
+      if constexpr (LOG2N < 16 && LOG2N >= 7 && PT < 2)
+        return launch_pool_mode<T, LOG2N, kModeFillBulk, PT>(a, n_pools, stream);
+      else
+        return cudaErrorInvalidValue;
     case kModePasses: return launch_pool_mode<T, LOG2N, kModePasses, PT>(a, n_pools, stream);
     default: return launch_pool_mode<T, LOG2N, kModeConsume, PT>(a, n_pools, stream);
   }

@@ -294,3 +294,76 @@ def test_unit_scale_emission_with_exact_zeros(cuda, n):
             assert_same(got[p], want, f"{dtype} n={n} pool {p}")
         assert np.any(got[0] == 0)
         assert not np.any(np.signbit(got[0][got[0] == 0]))
+
+
+# ---- bulk emission (scale exactly 1, mean +0: the emission is the pool) ------
+BULK_CONFIGS = [
+    dict(pool_size=4096, discard_every=2, disable_chi2=True),   # config 2's shape
+    dict(pool_size=1024, discard_every=1, disable_chi2=True),   # every pass emits, renormalisations
+    dict(pool_size=512, discard_every=3, disable_chi2=True),
+    dict(pool_size=128, discard_every=2, disable_chi2=True),
+]
+
+
+@pytest.mark.parametrize("bulk", [True, False], ids=["bulk", "register"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("kw", BULK_CONFIGS, ids=lambda k: f"N{k['pool_size']}_d{k['discard_every']}")
+def test_bulk_emission_matches_oracle(cuda, monkeypatch, kw, dtype, bulk):
+    """The bulk-emission kernel (shifted shared layout + cp.async.bulk) and
+    the register path give the oracle's stream, every emission alignment
+    (count not a multiple of 4, so emission starts cycle through all
+    shifts), head/tail values and the pool state."""
+    if not bulk:
+        monkeypatch.setenv("WALLACE_B200_NO_BULK", "1")
+    n = kw["pool_size"]
+    seeds = list(range(100, 164))
+    count = (300 // kw["discard_every"]) * (n - 1) + 7
+    b = pb.PoolBatch(gcfg(**kw), n_pools=len(seeds), seeds=seeds, dtype=dtype)
+    b.set_kernel_mode("throughput")
+    out = b.fill(count).cpu().numpy()
+    for p in (0, 1, 31, 63):
+        o = OracleGen(ocfg(seed=seeds[p], **kw), dtype)
+        assert_same(out[p], o.fill(count), f"pool {p}")
+        np.testing.assert_array_equal(bits(b.pool(p)), bits(o.pool()))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_bulk_emission_negative_zero_patch(cuda, dtype):
+    """A constant pool makes the butterfly cancel exactly: the passes produce
+    -0 pool values, which the emission (x*1 + 0) must turn into +0 -- the
+    bulk path patches them after its copy lands."""
+    kw = dict(pool_size=1024, discard_every=1, disable_chi2=True)
+    seeds = list(range(7, 7 + 40))
+    b = pb.PoolBatch(gcfg(**kw), n_pools=len(seeds), seeds=seeds, dtype=dtype)
+    b.set_kernel_mode("throughput")
+    o = OracleGen(ocfg(seed=seeds[3], **kw), dtype)
+    const = np.ones(1024)
+    b.inject_pool(const, pool=3)
+    o.inject_pool(const)
+    want = o.fill(20 * 1023 + 3)
+    got = b.fill(20 * 1023 + 3).cpu().numpy()[3]
+    assert_same(got, want, "constant pool")
+    assert np.count_nonzero(want == 0) > 0 and not np.any(np.signbit(want[want == 0]))
+
+
+def test_bulk_disabled_by_nonfinite_pool(cuda):
+    """A non-finite injected pool makes the emission scale NaN (not exactly
+    1): the handle stops using bulk emissions and matches the oracle
+    (NaN positions and every finite value)."""
+    kw = dict(pool_size=1024, discard_every=1, disable_chi2=True)
+    seeds = list(range(50, 90))
+    b = pb.PoolBatch(gcfg(**kw), n_pools=len(seeds), seeds=seeds, dtype="f32")
+    b.set_kernel_mode("throughput")
+    o = OracleGen(ocfg(seed=seeds[0], **kw), "f32")
+    v = np.linspace(-1, 1, 1024)
+    v[17] = np.inf
+    b.inject_pool(v, pool=0)
+    o.inject_pool(v)
+    got = b.fill(5 * 1023 + 2).cpu().numpy()[0]
+    want = o.fill(5 * 1023 + 2)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    fin = ~np.isnan(want)
+    assert_same(got[fin], want[fin], "finite values")
+    # the other pools keep their exact streams
+    o1 = OracleGen(ocfg(seed=seeds[1], **kw), "f32")
+    assert_same(b.fill(3000).cpu().numpy()[1], (o1.fill(5 * 1023 + 2), o1.fill(3000))[1], "pool 1")
