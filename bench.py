@@ -240,13 +240,21 @@ def run_ours(args):
     launches0 = pb.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    import ctypes as C
+    L = pb._capi.load()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        # per-launch CUDA events on the handle's stream bracket every
+        # pool_kernel / plan_kernel launch of the timed steps (roofline below)
+        L.wallace_profile_begin(batch.h)
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+    pool_ms, plan_ms = C.c_double(), C.c_double()
+    pool_n, plan_n = C.c_uint64(), C.c_uint64()
+    L.wallace_profile_end(batch.h, C.byref(pool_ms), C.byref(pool_n), C.byref(plan_ms), C.byref(plan_n))
     ms = ev0.elapsed_time(ev1)
     launches = pb.kernel_launches() - launches0
     if dist:
@@ -256,18 +264,10 @@ def run_ours(args):
     variates_rank = n_pools * count
     value = world * variates_rank * args.steps / (ms / 1e3)
 
-    # dominant kernel timing: pool_kernel bracketed by events on its stream
-    pb._capi.load().wallace_profile_begin(batch.h)
-    for _ in range(max(3, min(args.steps, 10))):
-        step()
-    import ctypes as C
-    pool_ms, plan_ms = C.c_double(), C.c_double()
-    pool_n, plan_n = C.c_uint64(), C.c_uint64()
-    pb._capi.load().wallace_profile_end(batch.h, C.byref(pool_ms), C.byref(pool_n),
-                                        C.byref(plan_ms), C.byref(plan_n))
+    # dominant kernel timing: pool_kernel launches of the timed steps
     peak, peak_src = measured_peaks()
     per_launch_ms = pool_ms.value / max(1, pool_n.value)
-    launches_per_step = pool_n.value / max(3, min(args.steps, 10))
+    launches_per_step = pool_n.value / args.steps
     alg_bytes = variates_rank * esize / launches_per_step  # written per launch
     roofline = None
     if not consume:

@@ -356,6 +356,8 @@ struct SState {
   uint32_t flags;
   int32_t renorm_ok;
   uint32_t zero_seen;  // an exact zero was emitted by bulk stores (patch needed)
+  uint32_t x_last_bulk_set;  // bulk kernels: the last emission was a fast one
+  double x_last_bulk;        // ... and its pool element N-1
   uint32_t ready;      // chain-warp kernels: S/r/scale of every emission <= ready published
 };
 
@@ -1175,6 +1177,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     s.last_scale = st.scale;
     s.clamp = 0;
     s.zero_seen = 0;
+    s.x_last_bulk_set = 0;
     s.ready = 0;
     s.flags = st.flags;
     if (MODE != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
@@ -1324,8 +1327,19 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           if (zf) s.zero_seen = 1;
         }
         if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3) {
-          chain_close(s, slot, static_cast<double>(x_last));
-          if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+          if constexpr (BULK_OK) {
+            // bulk kernels run with disable_chi2: S = sum_sq, r and scale are
+            // functions of the current sum_sq alone, nothing in the launch
+            // reads them, and only the last emission's values persist
+            // (reserved_prev, last_*): the chain runs once, after the loop
+            if (e + 1 == a.n_emit) {
+              s.x_last_bulk = static_cast<double>(x_last);
+              s.x_last_bulk_set = 1;
+            }
+          } else {
+            chain_close(s, slot, static_cast<double>(x_last));
+            if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+          }
         }
         // the bulk copy of the previous emission must have read its source
         // before this barrier releases that buffer for overwriting
@@ -1381,6 +1395,14 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         if (emit_pass && !fast) {
           // slow emission from shared memory: the partial last emission, an
           // emission right after a renormalisation, pools below 128 values
+          if constexpr (BULK_OK) {
+            // the fast emissions skipped the chain: this emission's scale on
+            // demand (after a renormalisation chain_rescale already has it)
+            if (!renorm_now) {
+              if (tid == 0) chain_draw(s, slot, a.chi2, a.sigma);
+              __syncthreads();
+            }
+          }
           const T sc = from_double<T>(s.scale[slot]);
           for (uint32_t i = tid; i < limit; i += THREADS) {
             const T v = emit_value(cur[i], sc, mean_t, mean_zero);
@@ -1396,6 +1418,15 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           __syncthreads();
         }
         pc = (pc + 1) & 255u;
+      }
+    }
+    if constexpr (BULK_OK) {
+      // the last emission's chain (see above); a slow last emission closed it already
+      __syncthreads();
+      if (tid == G::OWNER && s.x_last_bulk_set) {
+        const int slot = (a.n_emit - 1) & 1;
+        chain_draw(s, slot, a.chi2, a.sigma);
+        chain_close(s, slot, s.x_last_bulk);
       }
     }
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies

@@ -321,10 +321,20 @@ def test_bulk_emission_matches_oracle(cuda, monkeypatch, kw, dtype, bulk):
     b = pb.PoolBatch(gcfg(**kw), n_pools=len(seeds), seeds=seeds, dtype=dtype)
     b.set_kernel_mode("throughput")
     out = b.fill(count).cpu().numpy()
+    out2 = b.fill(2 * n + 3).cpu().numpy()   # state carried across launches
+    vals, res, chi = b.next_pool()
+    vals = vals.cpu().numpy()
     for p in (0, 1, 31, 63):
         o = OracleGen(ocfg(seed=seeds[p], **kw), dtype)
         assert_same(out[p], o.fill(count), f"pool {p}")
+        assert_same(out2[p], o.fill(2 * n + 3), f"pool {p} second fill")
+        ov, ores, ochi = o.next_pool()
+        assert_same(vals[p], ov, f"pool {p} next_pool")
+        assert res[p] == ores and chi[p] == ochi
         np.testing.assert_array_equal(bits(b.pool(p)), bits(o.pool()))
+        st = o.stats()
+        info = b.info(p)
+        assert info["reserved_prev"] == st["reserved_prev"] and info["sum_sq"] == st["sum_sq"]
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
