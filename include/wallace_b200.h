@@ -202,6 +202,25 @@ uint64_t wallace_default_stride(uint64_t rows);
 int32_t wallace_decode_pass_plan(uint64_t pool_size, uint64_t transform_word,
                                  uint64_t offset_word, uint64_t* offset0);
 
+/* ---- defect suite, GPU-resident (stats.cpp) ---------------------------------
+ * cross_pool_correlation(Generator&, opts) (stats.cpp:310-338) for every pool
+ * of the batch: `passes` step_pass() calls; for probe k the reference's
+ * ProbeAccumulator sums over x = pool_before[in_j[k]] and y =
+ * pool_after[out_i[k]], in pass order, fp64 (bit-identical per pool):
+ * acc[(pool * n_probes + k) * 6 + {0..5}] = {sx, sxx, sy, syy, sxy, sxy2}.
+ * 1 <= n_probes <= 32; the pools advance by `passes`.  Synchronous. */
+wallace_status wallace_cross_pool_probes(wallace_handle* h, uint64_t passes, uint32_t n_probes,
+                                         const uint64_t* out_i, const uint64_t* in_j, double* acc);
+/* pool_sum_squares_test (stats.cpp:340-369) and rare_event_adjacency
+ * (:424-447) for every pool: `emissions` next_pool() calls; per emission the
+ * total reserved^2 + sum v^2 of the standardized values (fp64; a tree sum,
+ * equal to the reference's sequential sum to rounding) and the mark "some
+ * |v| > threshold".  totals / marks: [n_pools][emissions].  The handle's
+ * config must have out_mean 0 and out_sigma 1 (the reference standardizes
+ * the same way).  Synchronous. */
+wallace_status wallace_pool_defect_stats(wallace_handle* h, uint64_t emissions, double threshold,
+                                         double* totals, uint8_t* marks);
+
 /* maxent::PassPlan (generator.hpp:50-55) and decode_pass_plan(cfg, w0, w1)
  * (generator.cpp:238-257) for every family/mixing combination. */
 typedef struct wallace_pass_plan {

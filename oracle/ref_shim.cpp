@@ -196,6 +196,66 @@ void ref_decode_pass_plan_ex(uint64_t pool_size, int family, int mixing, uint64_
   offsets[1] = plan.offset[1];
 }
 
+// The reference's defect-suite reports (stats.cpp), for pinning the GPU
+// accumulators: out[k*4 + {0..3}] = statistic, expected, se, z of report k.
+int ref_cross_pool_correlation(void* g, uint64_t pool_pairs, uint32_t n_probes,
+                               const uint64_t* out_i, const uint64_t* in_j, double* out) {
+  try {
+    maxent::CrossPoolOptions o;
+    o.pool_pairs = pool_pairs;
+    for (uint32_t k = 0; k < n_probes; ++k) o.probes.push_back({out_i[k], in_j[k]});
+    const auto reps = maxent::cross_pool_correlation(*static_cast<maxent::Generator*>(g), o);
+    for (size_t k = 0; k < reps.size(); ++k) {
+      out[k * 4 + 0] = reps[k].statistic;
+      out[k * 4 + 1] = reps[k].expected;
+      out[k * 4 + 2] = reps[k].std_error;
+      out[k * 4 + 3] = reps[k].z_score;
+    }
+    return static_cast<int>(reps.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_pool_sum_squares(uint64_t pool_size, int chi2_method, uint64_t discard_every, uint64_t seed,
+                         int disable_chi2, int family, int mixing, uint64_t pools, double* out) {
+  try {
+    const auto r = maxent::pool_sum_squares_test(
+        to_cfg(pool_size, chi2_method, discard_every, 0.0, 1.0, seed, 0, disable_chi2, family, mixing),
+        pools);
+    const maxent::TestReport* rs[2] = {&r.mean_report, &r.variance_report};
+    for (int k = 0; k < 2; ++k) {
+      out[k * 4 + 0] = rs[k]->statistic;
+      out[k * 4 + 1] = rs[k]->expected;
+      out[k * 4 + 2] = rs[k]->std_error;
+      out[k * 4 + 3] = rs[k]->z_score;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_rare_event_adjacency(uint64_t pool_size, int chi2_method, uint64_t discard_every,
+                             uint64_t seed, int disable_chi2, uint64_t samples, double threshold,
+                             double* out) {
+  try {
+    const auto r = maxent::rare_event_adjacency(
+        to_cfg(pool_size, chi2_method, discard_every, 0.0, 1.0, seed, 0, disable_chi2), samples,
+        threshold);
+    out[0] = r.statistic;
+    out[1] = r.expected;
+    out[2] = r.std_error;
+    out[3] = r.z_score;
+    return r.name.find("[no-marks]") != std::string::npos ? 1 : 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 void ref_polar(uint64_t seed, uint64_t n, double* out) {
   maxent::BaselineState s(seed);
   for (uint64_t i = 0; i < n; ++i) out[i] = maxent::polar_next(s);

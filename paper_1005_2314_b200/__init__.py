@@ -260,6 +260,36 @@ class PoolBatch:
         _check(self.L.wallace_set_stream(self.h, self._stream))
 
 
+    # ---- defect suite (stats.cpp), GPU-resident -------------------------
+    def cross_pool_probes(self, passes: int, probes=None) -> np.ndarray:
+        """cross_pool_correlation on every pool (stats.cpp:310-338): advance
+        `passes` step_pass() and return the ProbeAccumulator sums
+        [n_pools, n_probes, 6] = (sx, sxx, sy, syy, sxy, sxy2) of
+        x = pool_before[in_j], y = pool_after[out_i].  probes: (out_i, in_j)
+        pairs, default stats.default_probes(N)."""
+        from . import stats
+        probes = stats.default_probes(self.cfg.pool_size) if probes is None else list(probes)
+        k = len(probes)
+        oi = (C.c_uint64 * k)(*[int(p[0]) for p in probes])
+        ij = (C.c_uint64 * k)(*[int(p[1]) for p in probes])
+        acc = np.zeros((self.n_pools, k, 6), dtype=np.float64)
+        _check(self.L.wallace_cross_pool_probes(self.h, int(passes), k, oi, ij,
+                                                acc.ctypes.data_as(C.POINTER(C.c_double))))
+        return acc
+
+    def pool_defect_stats(self, emissions: int, threshold: float = 4.0):
+        """pool_sum_squares_test / rare_event_adjacency on every pool
+        (stats.cpp:340-369, 424-447): `emissions` next_pool() calls; returns
+        (totals [n_pools, emissions] = reserved^2 + sum v^2, marks
+        [n_pools, emissions] = any |v| > threshold).  Needs a standardized
+        config (out_mean 0, out_sigma 1)."""
+        totals = np.zeros((self.n_pools, int(emissions)), dtype=np.float64)
+        marks = np.zeros((self.n_pools, int(emissions)), dtype=np.uint8)
+        _check(self.L.wallace_pool_defect_stats(self.h, int(emissions), float(threshold),
+                                                totals.ctypes.data_as(C.POINTER(C.c_double)),
+                                                marks.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return totals, marks.astype(bool)
+
 def boxmuller_consume(n_streams: int, count: int, seed_base: int = 1, seeds=None, stream=None):
     """Box-Muller comparator on UniformState(seed) streams (baselines.cpp:80-92)."""
     L = _capi.load()

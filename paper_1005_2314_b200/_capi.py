@@ -99,6 +99,8 @@ SYMBOLS = [
     ("wallace_decode_pass_plan", i32, [u64, u64, u64, P(u64)]),
     ("wallace_decode_pass_plan_ex", i32, [P(wallace_config), u64, u64, P(wallace_pass_plan)]),
     ("wallace_rotation_table", None, [P(C.c_double), P(C.c_double), P(C.c_double)]),
+    ("wallace_cross_pool_probes", i32, [vp, u64, C.c_uint32, P(u64), P(u64), P(C.c_double)]),
+    ("wallace_pool_defect_stats", i32, [vp, u64, C.c_double, P(C.c_double), P(C.c_uint8)]),
 ]
 
 _lib = None

@@ -60,6 +60,8 @@ enum Mode : int32_t {
   kModeConsume = 2,  // emit into fused moment/histogram consumer
   kModeFillBulk = 3, // emit into the caller's buffer, every emission the pool
                      // itself (scale 1, mean +0): bulk copies from shared memory
+  kModeDefect = 4,   // emit into the defect-suite consumer: per-emission sum
+                     // of squares (+ reserved^2) and rare-event mark
 };
 
 struct FillArgs {
@@ -91,6 +93,16 @@ struct FillArgs {
   int32_t pad_pt;
   double rot_c[16];
   double rot_s[16];
+  // defect suite: kModeDefect per-emission outputs, kModePasses probes
+  double* def_totals;     // [n_pools][def_stride]: reserved^2 + sum v^2 per emission
+  uint8_t* def_marks;     // [n_pools][def_stride]: any |v| > def_threshold
+  uint64_t def_stride;
+  uint64_t def_e0;        // emission index of this launch's first emission
+  double def_threshold;
+  double* probe_acc;      // [n_pools][n_probes][6]: sx, sxx, sy, syy, sxy, sxy2
+  uint32_t n_probes;      // 0 = no probes
+  uint32_t probe_out[32];
+  uint32_t probe_in[32];
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]

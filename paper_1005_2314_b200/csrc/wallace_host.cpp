@@ -213,6 +213,14 @@ struct wallace_handle {
   int key = 0;        // kernel key: log2(N) (+16 for the latency kernel)
   int kmode = 0;      // 0 auto, 1 throughput, 2 latency
   bool bulk_ok = false;  // fills may use the bulk-emission kernel
+  // defect suite (wallace_cross_pool_probes / wallace_pool_defect_stats)
+  double* d_probe_acc = nullptr;
+  uint32_t n_probes = 0;  // active only inside wallace_cross_pool_probes
+  uint32_t probe_out[32] = {}, probe_in[32] = {};
+  double* d_def_totals = nullptr;
+  uint8_t* d_def_marks = nullptr;
+  uint64_t def_stride = 0;
+  double def_threshold = 0.0;
   void* d_leftover = nullptr;
   void* d_snap_pools = nullptr;
   PoolState* d_snap_state = nullptr;
@@ -332,6 +340,14 @@ wb::FillArgs base_args(wallace_handle* h) {
   a.leftover = h->d_leftover;
   a.out_stride = 0;
   a.pass_type = h->pass_type;
+  a.n_probes = h->n_probes;
+  a.probe_acc = h->d_probe_acc;
+  std::memcpy(a.probe_out, h->probe_out, sizeof(a.probe_out));
+  std::memcpy(a.probe_in, h->probe_in, sizeof(a.probe_in));
+  a.def_totals = h->d_def_totals;
+  a.def_marks = h->d_def_marks;
+  a.def_stride = h->def_stride;
+  a.def_threshold = h->def_threshold;
   std::memcpy(a.rot_c, h->rot_c, sizeof(a.rot_c));
   std::memcpy(a.rot_s, h->rot_s, sizeof(a.rot_s));
   return a;
@@ -465,6 +481,7 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     // every emission is the pool itself (scale exactly 1, mean +0): the
     // bulk-emission kernel (throughput geometry, wallace4 passes)
     if (mode == wb::kModeFill && h->bulk_ok && h->key < 16 && h->log2n >= 7) a.mode = wb::kModeFillBulk;
+    if (mode == wb::kModeDefect) a.def_e0 = produced / (h->N - 1);  // defect runs start at an emission
     a.out = out;
     a.out_stride = count;
     a.out_offset = produced;
@@ -901,6 +918,68 @@ wallace_status wallace_step_pass(wallace_handle* h, uint64_t n_passes) {
   wallace_status st = materialize(h);
   if (st) return st;
   return run_passes(h, n_passes);
+}
+
+wallace_status wallace_cross_pool_probes(wallace_handle* h, uint64_t passes, uint32_t n_probes,
+                                         const uint64_t* out_i, const uint64_t* in_j, double* acc) {
+  if (!h || !out_i || !in_j || !acc) return fail(WALLACE_ERR_INVALID_PARAM, "handle/probes/acc must not be NULL");
+  if (n_probes < 1 || n_probes > 32) return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_probes: 1..32 probes");
+  if (passes < 1) return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_probes: passes must be >= 1");
+  for (uint32_t k = 0; k < n_probes; ++k)
+    if (out_i[k] >= h->N || in_j[k] >= h->N)
+      return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_correlation: probe index out of range");
+  wallace_status st = materialize(h);
+  if (st) return st;
+  const size_t bytes = h->n_pools * n_probes * 6 * sizeof(double);
+  WB_CUDA(cudaMalloc(&h->d_probe_acc, bytes));
+  cudaError_t e = cudaMemsetAsync(h->d_probe_acc, 0, bytes, h->stream);
+  if (e == cudaSuccess) {
+    h->n_probes = n_probes;
+    for (uint32_t k = 0; k < n_probes; ++k) {
+      h->probe_out[k] = static_cast<uint32_t>(out_i[k]);
+      h->probe_in[k] = static_cast<uint32_t>(in_j[k]);
+    }
+    st = run_passes(h, passes);
+    h->n_probes = 0;
+    if (!st) e = cudaMemcpyAsync(acc, h->d_probe_acc, bytes, cudaMemcpyDeviceToHost, h->stream);
+    if (!st && e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  }
+  cudaFree(h->d_probe_acc);
+  h->d_probe_acc = nullptr;
+  if (st) return st;
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "cross_pool_probes: %s", cudaGetErrorString(e));
+  return WALLACE_OK;
+}
+
+wallace_status wallace_pool_defect_stats(wallace_handle* h, uint64_t emissions, double threshold,
+                                         double* totals, uint8_t* marks) {
+  if (!h || !totals || !marks) return fail(WALLACE_ERR_INVALID_PARAM, "handle/totals/marks must not be NULL");
+  if (emissions < 1) return fail(WALLACE_ERR_INVALID_PARAM, "pool_defect_stats: emissions must be >= 1");
+  if (!(h->cfg.out_mean == 0.0) || !(h->cfg.out_sigma == 1.0))
+    return fail(WALLACE_ERR_INVALID_PARAM,
+                "pool_defect_stats: the handle's config must be standardized (out_mean 0, out_sigma 1)");
+  const size_t n = h->n_pools * emissions;
+  WB_CUDA(cudaMalloc(&h->d_def_totals, n * sizeof(double)));
+  cudaError_t e = cudaMalloc(&h->d_def_marks, n);
+  wallace_status st = WALLACE_OK;
+  if (e == cudaSuccess) {
+    h->def_stride = emissions;
+    h->def_threshold = threshold;
+    // next_pool: refill_ + cursor_ = out_.size() -- the partial buffer is
+    // discarded and every step is one whole emission (generator.cpp:401-405)
+    h->cursor = static_cast<uint32_t>(h->N - 1);
+    st = run_emit(h, nullptr, emissions * (h->N - 1), wb::kModeDefect, h->d_state, h->d_pools);
+    if (!st) e = cudaMemcpyAsync(totals, h->d_def_totals, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    if (!st && e == cudaSuccess) e = cudaMemcpyAsync(marks, h->d_def_marks, n, cudaMemcpyDeviceToHost, h->stream);
+    if (!st && e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  }
+  cudaFree(h->d_def_totals);
+  cudaFree(h->d_def_marks);
+  h->d_def_totals = nullptr;
+  h->d_def_marks = nullptr;
+  if (st) return st;
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "pool_defect_stats: %s", cudaGetErrorString(e));
+  return WALLACE_OK;
 }
 
 wallace_status wallace_inject_pool(wallace_handle* h, uint64_t pool, const double* values,

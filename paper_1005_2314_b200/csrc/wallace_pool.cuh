@@ -1133,6 +1133,32 @@ __device__ __forceinline__ void consume_chunk(const T (&X)[JCL][4], Consumer<T>&
   }
 }
 
+// Defect-suite consumer of one chunk (stats.cpp:340-369 pool_sum_squares_test,
+// :424-447 rare_event_adjacency): the fp64 sum of squares of this thread's
+// emitted (standardized) values and whether any |v| exceeds the threshold.
+// Element N-1 is the reserved value, not emitted.
+template <typename T, int LOG2N, int JCL>
+__device__ __forceinline__ void defect_chunk(const T (&X)[JCL][4], double& dsum, bool& mark, T sc, T mean,
+                                             bool mz, uint32_t b0c, double thr) {
+  using G = Geo<T, LOG2N>;
+#pragma unroll
+  for (int j = 0; j < JCL; ++j) {
+    const uint32_t b = b0c + 32 * j;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k == 3 && b == G::ROWS - 1) continue;
+      const double v = static_cast<double>(emit_value(X[j][k], sc, mean, mz));
+      dsum = __dadd_rn(dsum, __dmul_rn(v, v));
+      mark |= fabs(v) > thr;
+    }
+  }
+}
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 template <typename T, int LOG2N, int MODE, int PT>
 __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     pool_kernel(const __grid_constant__ FillArgs a) {
@@ -1157,6 +1183,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::TOTAL));
   __shared__ SState s;
   __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
+  // defect suite: per-warp partial sums / marks of the last two emissions
+  __shared__ double s_def[MODE == kModeDefect ? 2 : 1][MODE == kModeDefect ? G::NW : 1];
+  __shared__ uint32_t s_defm[MODE == kModeDefect ? 2 : 1][MODE == kModeDefect ? G::NW : 1];
   __shared__ __align__(16) float s_hs[64];  // sign mask -> (0.5*sign_k)_k (transforms.cpp:88)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1209,7 +1238,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       const uint32_t idx = cursor0 + i;
       const T v = mat ? lo[idx] : emit_value(pools[idx], sc, mean_t, mean_zero);
       if constexpr (MODE == kModeConsume) cons.add(v);
-      else stg1(out_pool + i, v);
+      else if constexpr (MODE != kModeDefect) stg1(out_pool + i, v);  // (defect runs start at an emission)
     }
     if constexpr (MODE == kModeConsume) cons.flush();
   }
@@ -1221,7 +1250,17 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   uint32_t p = 0;                                          // plan index
 
   if constexpr (MODE == kModePasses) {
+    // cross-pool probes (stats.cpp:310-338, cross_pool_correlation on a
+    // streaming generator): thread k follows probe k, x = pool[in_j] before
+    // the pass, y = pool[out_i] after it (and after a renormalisation, as
+    // step_pass); the ProbeAccumulator sums in pass order, fp64
+    const bool probe = tid < int(a.n_probes);
+    double pa[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (probe)
+      for (int k = 0; k < 6; ++k) pa[k] = a.probe_acc[(pool * a.n_probes + tid) * 6 + k];
     for (; p < a.n_passes; ++p) {
+      double px = 0.0;
+      if (probe) px = static_cast<double>(reinterpret_cast<const T*>(pbase + cur_off)[a.probe_in[tid]]);
       const uint32_t plan_p = s_plans[p * PW];
       if (compute) {
         for (int c0 = 0; c0 < J; c0 += G::JC) {
@@ -1237,7 +1276,19 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       cur_off ^= PFLIP;
       if (pc == 0) renormalize<T, N, THREADS, G::LAT>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
       pc = (pc + 1) & 255u;
+      if (probe) {
+        const double y = static_cast<double>(reinterpret_cast<const T*>(pbase + cur_off)[a.probe_out[tid]]);
+        pa[0] = __dadd_rn(pa[0], px);
+        pa[1] = __dadd_rn(pa[1], __dmul_rn(px, px));
+        pa[2] = __dadd_rn(pa[2], y);
+        pa[3] = __dadd_rn(pa[3], __dmul_rn(y, y));
+        const double w = __dmul_rn(px, y);
+        pa[4] = __dadd_rn(pa[4], w);
+        pa[5] = __dadd_rn(pa[5], __dmul_rn(w, w));
+      }
     }
+    if (probe)
+      for (int k = 0; k < 6; ++k) a.probe_acc[(pool * a.n_probes + tid) * 6 + k] = pa[k];
   } else {
     uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
     // bulk emission (see "Bulk emission") for the throughput geometry
@@ -1278,6 +1329,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         // and global address of every emitted element agree mod 16 bytes
         const uint32_t sigma = (G::VEC - delta) & (G::VEC - 1);
         uint32_t zf = 0;
+        double dsum = 0.0;  // defect suite: this thread's sum of squares / mark
+        bool dmark = false;
         T prev[4] = {T(0), T(0), T(0), T(0)};  // lane 31's pending block (emission)
         T x_last = T(0);
         if (G::CHAINW && do_emit && compute) {
@@ -1301,7 +1354,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             run_pass<T, LOG2N, JCL, PT>(cbase, cur_off + sh, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs,
                                         !bulk);
           if (do_emit) {
-            if constexpr (MODE != kModeConsume) {
+            if constexpr (MODE == kModeDefect) {
+              defect_chunk<T, LOG2N, JCL>(X, dsum, dmark, sc, mean_t, mean_zero, b0 + 32 * c0, a.def_threshold);
+            } else if constexpr (MODE != kModeConsume) {
               if constexpr (BULK_OK) {
                 T* sb = reinterpret_cast<T*>(pbase + (cur_off ^ FLIP)) + sigma;
                 shift_chunk_any<T, LOG2N>(delta, X, c0, prev, sb, lane, warp, &zf);
@@ -1322,6 +1377,16 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         }
         if constexpr (MODE == kModeConsume)
           if (do_emit) cons.flush();
+        if constexpr (MODE == kModeDefect) {
+          if (do_emit) {
+            const double ws = warp_sum_f64(dsum);
+            const bool wm = __any_sync(0xffffffffu, dmark);
+            if (lane == 0) {
+              s_def[slot][warp] = ws;
+              s_defm[slot][warp] = wm;
+            }
+          }
+        }
         if (bulk) {
           fence_proxy_async_smem();  // this thread's shared stores -> visible to the bulk copy
           if (zf) s.zero_seen = 1;
@@ -1355,6 +1420,20 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           chain_close(s, slot, static_cast<double>(cur[N - 1]));
           if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
           st_release_cta(&s.ready, e + 1);
+        }
+        if constexpr (MODE == kModeDefect) {
+          // the emission's total: reserved^2 (chain_close ran before the
+          // barrier) plus the warp partials in warp order; its mark
+          if (do_emit && tid == 0) {
+            double t = __dmul_rn(s.reserved_prev, s.reserved_prev);
+            uint32_t m = 0;
+            for (int w = 0; w < G::NW; ++w) {
+              t = __dadd_rn(t, s_def[slot][w]);
+              m |= s_defm[slot][w];
+            }
+            a.def_totals[pool * a.def_stride + a.def_e0 + e] = t;
+            a.def_marks[pool * a.def_stride + a.def_e0 + e] = m ? 1 : 0;
+          }
         }
         if (BULK_OK && bulk) {
           // the aligned middle [delta, delta + L) in one copy; the <= VEC-1
@@ -1404,16 +1483,44 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             }
           }
           const T sc = from_double<T>(s.scale[slot]);
+          double ds = 0.0;
+          bool dm = false;
           for (uint32_t i = tid; i < limit; i += THREADS) {
             const T v = emit_value(cur[i], sc, mean_t, mean_zero);
-            if constexpr (MODE == kModeConsume) cons.add(v);
-            else stg1(gbase + i, v);
+            if constexpr (MODE == kModeConsume) {
+              cons.add(v);
+            } else if constexpr (MODE == kModeDefect) {
+              const double dv = static_cast<double>(v);
+              ds = __dadd_rn(ds, __dmul_rn(dv, dv));
+              dm |= fabs(dv) > a.def_threshold;
+            } else {
+              stg1(gbase + i, v);
+            }
           }
           if constexpr (MODE == kModeConsume) cons.flush();
+          if constexpr (MODE == kModeDefect) {
+            const double ws = warp_sum_f64(ds);
+            const bool wm = __any_sync(0xffffffffu, dm);
+            if (lane == 0) {
+              s_def[slot][warp] = ws;
+              s_defm[slot][warp] = wm;
+            }
+            __syncthreads();
+          }
           if (tid == 0) {
             chain_close(s, slot, static_cast<double>(cur[N - 1]));
             if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
             s.ready = e + 1;
+            if constexpr (MODE == kModeDefect) {
+              double t = __dmul_rn(s.reserved_prev, s.reserved_prev);
+              uint32_t m = 0;
+              for (int w = 0; w < G::NW; ++w) {
+                t = __dadd_rn(t, s_def[slot][w]);
+                m |= s_defm[slot][w];
+              }
+              a.def_totals[pool * a.def_stride + a.def_e0 + e] = t;
+              a.def_marks[pool * a.def_stride + a.def_e0 + e] = m ? 1 : 0;
+            }
           }
           __syncthreads();
         }
@@ -1523,6 +1630,7 @@ cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream
       else
         return cudaErrorInvalidValue;
     case kModePasses: return launch_pool_mode<T, LOG2N, kModePasses, PT>(a, n_pools, stream);
+    case kModeDefect: return launch_pool_mode<T, LOG2N, kModeDefect, PT>(a, n_pools, stream);
     default: return launch_pool_mode<T, LOG2N, kModeConsume, PT>(a, n_pools, stream);
   }
 }
