@@ -1141,6 +1141,9 @@ template <typename T, int LOG2N, int JCL>
 __device__ __forceinline__ void defect_chunk(const T (&X)[JCL][4], double& dsum, bool& mark, T sc, T mean,
                                              bool mz, uint32_t b0c, double thr) {
   using G = Geo<T, LOG2N>;
+  // four independent accumulators (one per block slot) keep the fp64 add
+  // chain short; the order is a tree anyway (reference: sequential)
+  double d4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < JCL; ++j) {
     const uint32_t b = b0c + 32 * j;
@@ -1148,10 +1151,11 @@ __device__ __forceinline__ void defect_chunk(const T (&X)[JCL][4], double& dsum,
     for (int k = 0; k < 4; ++k) {
       if (k == 3 && b == G::ROWS - 1) continue;
       const double v = static_cast<double>(emit_value(X[j][k], sc, mean, mz));
-      dsum = __dadd_rn(dsum, __dmul_rn(v, v));
+      d4[k] = __dadd_rn(d4[k], __dmul_rn(v, v));
       mark |= fabs(v) > thr;
     }
   }
+  dsum = __dadd_rn(dsum, __dadd_rn(__dadd_rn(d4[0], d4[1]), __dadd_rn(d4[2], d4[3])));
 }
 __device__ __forceinline__ double warp_sum_f64(double v) {
 #pragma unroll
