@@ -202,6 +202,24 @@ uint64_t wallace_default_stride(uint64_t rows);
 int32_t wallace_decode_pass_plan(uint64_t pool_size, uint64_t transform_word,
                                  uint64_t offset_word, uint64_t* offset0);
 
+/* ---- stream wire format (cmd_gen.cpp:39-57) ---------------------------------
+ * `count` further values of every pool written to the file descriptor `fd`,
+ * pool-major (pool p's values at [p*count, (p+1)*count) in value units, as
+ * wallace_fill): WALLACE_FMT_F64LE consecutive 8-byte little-endian IEEE
+ * doubles, no header (an fp32 stream widened exactly); WALLACE_FMT_TEXT one
+ * "%.17g\n" line per value (round-trips the double; one pool only);
+ * WALLACE_FMT_F32LE 4-byte floats (fp32 handles).  For one pool this is the
+ * byte stream of the reference's `gen --format f64le|text`.  Several pools
+ * need a binary format and a seekable fd.  Generation, the device->host copy
+ * and the formatting/writing of consecutive chunks overlap (double-buffered
+ * pinned staging).  Synchronous; leaves the file position after the block. */
+typedef enum wallace_format {
+  WALLACE_FMT_F64LE = 0,
+  WALLACE_FMT_TEXT = 1,
+  WALLACE_FMT_F32LE = 2
+} wallace_format;
+wallace_status wallace_write_stream(wallace_handle* h, uint64_t count, int32_t format, int32_t fd);
+
 /* ---- defect suite, GPU-resident (stats.cpp) ---------------------------------
  * cross_pool_correlation(Generator&, opts) (stats.cpp:310-338) for every pool
  * of the batch: `passes` step_pass() calls; for probe k the reference's

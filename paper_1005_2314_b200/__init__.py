@@ -260,6 +260,28 @@ class PoolBatch:
         _check(self.L.wallace_set_stream(self.h, self._stream))
 
 
+    # ---- stream wire format (cmd_gen.cpp:39-57) --------------------------
+    FORMATS = {"f64le": 0, "text": 1, "f32le": 2}
+
+    def write_stream(self, out, count: int, fmt: str = "f64le") -> None:
+        """Write `count` further values of every pool (pool-major) to `out`
+        (a path, an open binary file or a file descriptor) in the reference's
+        gen formats: f64le (8-byte LE doubles), text ("%.17g" lines, one
+        pool), f32le (fp32 handles)."""
+        import os
+        if isinstance(out, int):
+            fd, close = out, False
+        elif hasattr(out, "fileno"):
+            out.flush()
+            fd, close = out.fileno(), False
+        else:
+            fd, close = os.open(str(out), os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644), True
+        try:
+            _check(self.L.wallace_write_stream(self.h, int(count), self.FORMATS[fmt], fd))
+        finally:
+            if close:
+                os.close(fd)
+
     # ---- defect suite (stats.cpp), GPU-resident -------------------------
     def cross_pool_probes(self, passes: int, probes=None) -> np.ndarray:
         """cross_pool_correlation on every pool (stats.cpp:310-338): advance

@@ -100,6 +100,7 @@ SYMBOLS = [
     ("wallace_decode_pass_plan_ex", i32, [P(wallace_config), u64, u64, P(wallace_pass_plan)]),
     ("wallace_rotation_table", None, [P(C.c_double), P(C.c_double), P(C.c_double)]),
     ("wallace_cross_pool_probes", i32, [vp, u64, C.c_uint32, P(u64), P(u64), P(C.c_double)]),
+    ("wallace_write_stream", i32, [vp, u64, i32, i32]),
     ("wallace_pool_defect_stats", i32, [vp, u64, C.c_double, P(C.c_double), P(C.c_uint8)]),
 ]
 

@@ -9,9 +9,12 @@
 // then run on the device.  Seeding is spread over host threads, one pool at a
 // time per thread.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cerrno>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -237,6 +240,13 @@ struct wallace_handle {
   // staging for fill_host
   void* d_stage = nullptr;
   uint64_t stage_bytes = 0;
+  // write_stream: two device + two pinned chunk buffers, a copy stream and
+  // events, kept across calls (pinning is slow)
+  void* ws_dev[2] = {nullptr, nullptr};
+  void* ws_host[2] = {nullptr, nullptr};
+  size_t ws_bytes = 0;
+  cudaStream_t ws_stream = nullptr;
+  cudaEvent_t ws_ef[2] = {nullptr, nullptr}, ws_ec[2] = {nullptr, nullptr};
 
   // profiling (wallace_profile_begin/end)
   bool profiling = false;
@@ -742,6 +752,13 @@ wallace_status wallace_destroy(wallace_handle* h) {
   cudaFree(h->d_part_sums);
   cudaFree(h->d_part_hist);
   cudaFree(h->d_stage);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(h->ws_dev[k]);
+    cudaFreeHost(h->ws_host[k]);
+    if (h->ws_ef[k]) cudaEventDestroy(h->ws_ef[k]);
+    if (h->ws_ec[k]) cudaEventDestroy(h->ws_ec[k]);
+  }
+  if (h->ws_stream) cudaStreamDestroy(h->ws_stream);
   for (auto& pr : h->ev_pool) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto& pr : h->ev_plan) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto e : h->ev_free) cudaEventDestroy(e);
@@ -797,6 +814,173 @@ wallace_status wallace_fill(wallace_handle* h, void* dev_out, uint64_t count) {
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (!dev_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
   return run_emit(h, dev_out, count, wb::kModeFill, h->d_state, h->d_pools);
+}
+
+// ---- stream wire format (cmd_gen.cpp:39-57) --------------------------------
+namespace {
+
+// write all of buf at offset (seekable) or at the current position
+bool write_all(int fd, const char* buf, size_t n, bool positional, off_t off) {
+  while (n > 0) {
+    const ssize_t w = positional ? ::pwrite(fd, buf, n, off) : ::write(fd, buf, n);
+    if (w < 0) {
+      if (errno == EINTR) continue;
+      return false;
+    }
+    buf += w;
+    n -= static_cast<size_t>(w);
+    off += w;
+  }
+  return true;
+}
+
+// One chunk [n_pools][ck] (host, dtype esize) -> file.  Binary formats land
+// pool-major at offset base + (p * count + k0) * out_size; text (one pool)
+// is appended: "%.17g\n" per value, formatted by several threads into
+// per-thread buffers that are written in order.
+bool write_chunk(int fd, int fmt, const unsigned char* src, size_t esize, uint64_t n_pools, uint64_t ck,
+                 uint64_t count, uint64_t k0, bool positional, off_t base, unsigned threads) {
+  auto value = [&](uint64_t i) -> double {
+    if (esize == 4) {
+      float f;
+      std::memcpy(&f, src + i * 4, 4);
+      return static_cast<double>(f);
+    }
+    double d;
+    std::memcpy(&d, src + i * 8, 8);
+    return d;
+  };
+  if (fmt == WALLACE_FMT_TEXT) {
+    const uint64_t per = (ck + threads - 1) / threads;
+    std::vector<std::string> parts(threads);
+    std::vector<std::thread> ts;
+    for (unsigned t = 0; t < threads; ++t) {
+      ts.emplace_back([&, t] {
+        const uint64_t i0 = t * per, i1 = std::min<uint64_t>(ck, i0 + per);
+        std::string& out = parts[t];
+        out.reserve((i1 > i0 ? i1 - i0 : 0) * 24);
+        char b[40];
+        for (uint64_t i = i0; i < i1; ++i) {
+          const int len = std::snprintf(b, sizeof b, "%.17g\n", value(i));
+          out.append(b, static_cast<size_t>(len));
+        }
+      });
+    }
+    for (auto& t : ts) t.join();
+    for (const auto& part : parts)
+      if (!write_all(fd, part.data(), part.size(), false, 0)) return false;
+    return true;
+  }
+  const size_t osz = fmt == WALLACE_FMT_F32LE ? 4 : 8;
+  // little-endian host: f64le of a double / f32le of a float is its bytes
+  std::atomic<uint64_t> next{0};
+  std::atomic<bool> ok{true};
+  std::vector<std::thread> ts;
+  for (unsigned t = 0; t < std::max(1u, std::min<unsigned>(threads, static_cast<unsigned>(n_pools))); ++t) {
+    ts.emplace_back([&] {
+      std::vector<unsigned char> conv;
+      for (;;) {
+        const uint64_t p = next.fetch_add(1);
+        if (p >= n_pools || !ok) break;
+        const unsigned char* row = src + p * ck * esize;
+        const char* data = reinterpret_cast<const char*>(row);
+        if (osz != esize) {  // fp32 values as f64le
+          conv.resize(ck * 8);
+          for (uint64_t i = 0; i < ck; ++i) {
+            float f;
+            std::memcpy(&f, row + i * 4, 4);
+            const double d = f;
+            std::memcpy(conv.data() + i * 8, &d, 8);
+          }
+          data = reinterpret_cast<const char*>(conv.data());
+        }
+        const off_t off = base + static_cast<off_t>((p * count + k0) * osz);
+        if (!write_all(fd, data, ck * osz, positional, off)) ok = false;
+      }
+    });
+  }
+  for (auto& t : ts) t.join();
+  return ok;
+}
+
+}  // namespace
+
+wallace_status wallace_write_stream(wallace_handle* h, uint64_t count, int32_t format, int32_t fd) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "write_stream: count must be >= 1");
+  if (format != WALLACE_FMT_F64LE && format != WALLACE_FMT_TEXT && format != WALLACE_FMT_F32LE)
+    return fail(WALLACE_ERR_INVALID_PARAM, "write_stream: format must be f64le, text or f32le");
+  if (format == WALLACE_FMT_F32LE && h->dtype != WALLACE_F32)
+    return fail(WALLACE_ERR_INVALID_PARAM, "write_stream: f32le needs an fp32 handle");
+  const off_t base = ::lseek(fd, 0, SEEK_CUR);
+  const bool seekable = base != static_cast<off_t>(-1);
+  if (h->n_pools > 1 && (format == WALLACE_FMT_TEXT || !seekable))
+    return fail(WALLACE_ERR_INVALID_PARAM,
+                "write_stream: several pools need a binary format and a seekable file (pool-major layout)");
+  const bool positional = seekable && format != WALLACE_FMT_TEXT;
+  // chunk along the per-pool count: about an eighth of the block (so the
+  // stages overlap), within [16, 512] MiB; whole emissions per launch for
+  // large batches
+  const uint64_t row = h->n_pools * h->esize;
+  const uint64_t want = std::min<uint64_t>(512ull << 20, std::max<uint64_t>(16ull << 20, row * count / 8));
+  const uint64_t c = std::max<uint64_t>(1, std::min<uint64_t>(count, want / row));
+  const size_t bytes = h->n_pools * c * h->esize;
+  cudaError_t e = cudaSuccess;
+  if (h->ws_bytes < bytes) {
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(h->ws_dev[k]);
+      cudaFreeHost(h->ws_host[k]);
+      h->ws_dev[k] = h->ws_host[k] = nullptr;
+    }
+    h->ws_bytes = 0;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = cudaMalloc(&h->ws_dev[k], bytes);
+      if (e == cudaSuccess) e = cudaMallocHost(&h->ws_host[k], bytes);
+    }
+    if (e == cudaSuccess) h->ws_bytes = bytes;
+  }
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    if (!h->ws_ef[k]) e = cudaEventCreateWithFlags(&h->ws_ef[k], cudaEventDisableTiming);
+    if (e == cudaSuccess && !h->ws_ec[k]) e = cudaEventCreateWithFlags(&h->ws_ec[k], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess && !h->ws_stream) e = cudaStreamCreateWithFlags(&h->ws_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "write_stream: %s", cudaGetErrorString(e));
+  void* const* d = h->ws_dev;
+  void* const* hb = h->ws_host;
+  cudaStream_t cs = h->ws_stream;
+  cudaEvent_t* ef = h->ws_ef;
+  cudaEvent_t* ec = h->ws_ec;
+  const unsigned threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const uint64_t nk = (count + c - 1) / c;
+  wallace_status st = WALLACE_OK;
+  for (uint64_t k = 0; k <= nk && !st; ++k) {
+    if (k < nk) {
+      // generate chunk k into d[k&1] (free once chunk k-2's copy is done)
+      const uint64_t ck = std::min<uint64_t>(c, count - k * c);
+      if (k >= 2 && (e = cudaStreamWaitEvent(h->stream, ec[k & 1], 0)) != cudaSuccess) break;
+      if ((st = wallace_fill(h, d[k & 1], ck))) break;
+      if ((e = cudaEventRecord(ef[k & 1], h->stream)) != cudaSuccess) break;
+      if ((e = cudaStreamWaitEvent(cs, ef[k & 1], 0)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(hb[k & 1], d[k & 1], h->n_pools * ck * h->esize, cudaMemcpyDeviceToHost, cs)) !=
+          cudaSuccess)
+        break;
+      if ((e = cudaEventRecord(ec[k & 1], cs)) != cudaSuccess) break;
+    }
+    if (k >= 1) {
+      // write chunk k-1 while chunk k is generated and copied
+      const uint64_t j = k - 1, cj = std::min<uint64_t>(c, count - j * c);
+      if ((e = cudaEventSynchronize(ec[j & 1])) != cudaSuccess) break;
+      if (!write_chunk(fd, format, static_cast<const unsigned char*>(hb[j & 1]), h->esize, h->n_pools, cj,
+                       count, j * c, positional, base, threads))
+        st = fail(WALLACE_ERR_INVALID_PARAM, "write_stream: write failed (errno %d)", errno);
+    }
+  }
+  if (!st && e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "write_stream: %s", cudaGetErrorString(e));
+  if (!st && positional)  // leave the file position after the written block
+    ::lseek(fd, base + static_cast<off_t>(h->n_pools * count * (format == WALLACE_FMT_F32LE ? 4 : 8)), SEEK_SET);
+  cudaStreamSynchronize(h->stream);
+  cudaStreamSynchronize(cs);
+  return st;
 }
 
 wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t count) {
