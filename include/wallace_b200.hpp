@@ -15,8 +15,11 @@
 // between calls behave exactly as in the reference (generator.cpp:387-413).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <limits>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -106,6 +109,12 @@ struct NormalPool {
   double sum_sq = 0.0;
 };
 
+// maxent::ProbePair (stats.hpp:78-81)
+struct ProbePair {
+  std::size_t out_i;
+  std::size_t in_j;
+};
+
 // Many independent pools on the device (one reference Generator per pool).
 class PoolBatch {
  public:
@@ -150,6 +159,31 @@ class PoolBatch {
     std::vector<double> r(cfg_.pool_size);
     check(wallace_get_pool(h_, pool, r.data(), r.size()));
     return r;
+  }
+  // The gen wire format (cmd_gen.cpp:39-57): `count_per_pool` further
+  // values of every pool to fd, pool-major (see wallace_write_stream).
+  void write_stream(int fd, std::uint64_t count_per_pool, wallace_format fmt = WALLACE_FMT_F64LE) {
+    check(wallace_write_stream(h_, count_per_pool, fmt, fd));
+  }
+  // Defect-suite accumulators (stats.cpp): `passes` step_pass() with the
+  // ProbeAccumulator sums [n_pools][probes][6]; `emissions` next_pool()
+  // with the per-emission totals and rare-event marks [n_pools][emissions].
+  std::vector<double> cross_pool_probes(std::uint64_t passes, std::span<const ProbePair> probes) {
+    std::vector<std::uint64_t> oi, ij;
+    for (const auto& p : probes) {
+      oi.push_back(p.out_i);
+      ij.push_back(p.in_j);
+    }
+    std::vector<double> acc(n_pools_ * probes.size() * 6);
+    check(wallace_cross_pool_probes(h_, passes, static_cast<std::uint32_t>(probes.size()), oi.data(), ij.data(),
+                                    acc.data()));
+    return acc;
+  }
+  void pool_defect_stats(std::uint64_t emissions, double threshold, std::vector<double>& totals,
+                         std::vector<std::uint8_t>& marks) {
+    totals.resize(n_pools_ * emissions);
+    marks.resize(n_pools_ * emissions);
+    check(wallace_pool_defect_stats(h_, emissions, threshold, totals.data(), marks.data()));
   }
   wallace_handle* handle() const { return h_; }
   const GeneratorConfig& config() const { return cfg_; }
@@ -243,5 +277,162 @@ class Generator {
   std::vector<double> last_pool_;
   mutable NormalPool pool_cache_;
 };
+
+// ---- defect suite (stats.hpp / stats.cpp), accumulated on the device -------
+
+// maxent::TestReport (stats.hpp:37-49, stats.cpp:58-75)
+struct TestReport {
+  std::string name;
+  double statistic = 0.0;
+  double expected = 0.0;
+  double std_error = 0.0;
+  double z_score = 0.0;
+  bool pass = false;
+  static TestReport make(std::string name, double statistic, double expected, double std_error) {
+    TestReport r;
+    r.name = std::move(name);
+    r.statistic = statistic;
+    r.expected = expected;
+    r.std_error = std_error;
+    if (std_error > 0.0) {
+      r.z_score = (statistic - expected) / std_error;
+    } else {
+      r.z_score = statistic == expected ? 0.0
+                                        : std::copysign(std::numeric_limits<double>::infinity(),
+                                                        statistic - expected);
+    }
+    r.pass = std::abs(r.z_score) <= 5.0;
+    return r;
+  }
+};
+
+// maxent::MomentSummary / moments (stats.hpp:23-35, stats.cpp:25-56)
+struct MomentSummary {
+  std::size_t count = 0;
+  double mean = 0.0;
+  double variance = 0.0;
+  double skewness = 0.0;
+  double excess_kurtosis = 0.0;
+};
+inline MomentSummary moments(std::span<const double> samples) {
+  if (samples.size() < 2) throw InvalidParameterError("moments: need at least 2 samples");
+  double mean = 0.0, m2 = 0.0, m3 = 0.0, m4 = 0.0;
+  std::size_t n = 0;
+  for (const double x : samples) {
+    const double n1 = static_cast<double>(n);
+    ++n;
+    const double nn = static_cast<double>(n);
+    const double delta = x - mean;
+    const double delta_n = delta / nn;
+    const double delta_n2 = delta_n * delta_n;
+    const double term1 = delta * delta_n * n1;
+    mean += delta_n;
+    m4 += term1 * delta_n2 * (nn * nn - 3.0 * nn + 3.0) + 6.0 * delta_n2 * m2 - 4.0 * delta_n * m3;
+    m3 += term1 * delta_n * (nn - 2.0) - 3.0 * delta_n * m2;
+    m2 += term1;
+  }
+  MomentSummary out;
+  out.count = n;
+  out.mean = mean;
+  out.variance = m2 / static_cast<double>(n - 1);
+  if (m2 > 0.0) {
+    const double nn = static_cast<double>(n);
+    out.skewness = std::sqrt(nn) * m3 / std::pow(m2, 1.5);
+    out.excess_kurtosis = nn * m4 / (m2 * m2) - 3.0;
+  }
+  return out;
+}
+
+// maxent::CrossPoolOptions (stats.hpp:83-95), streaming variant
+struct CrossPoolOptions {
+  std::size_t pool_pairs = 100000;  // >= 1e3
+  std::vector<ProbePair> probes;    // empty -> default spread of 8 probes
+};
+
+// stats.cpp:310-338 on a streaming generator: the probe sums are accumulated
+// on the device in pass order (bit-identical), finalized here as
+// ProbeAccumulator::finalize (stats.cpp:202-234).
+inline std::vector<TestReport> cross_pool_correlation(Generator& gen, const CrossPoolOptions& opts) {
+  if (opts.pool_pairs < 1000) throw InvalidParameterError("cross_pool_correlation: pool_pairs must be >= 1000");
+  const std::size_t n = gen.config().pool_size;
+  std::vector<ProbePair> probes = opts.probes;
+  if (probes.empty())
+    for (std::size_t k = 0; k < 8; ++k) probes.push_back({(5 * k) % n, (11 * k + 3) % n});
+  for (const auto& p : probes)
+    if (p.out_i >= n || p.in_j >= n) throw InvalidParameterError("cross_pool_correlation: probe index out of range");
+  const std::vector<double> acc = gen.batch().cross_pool_probes(opts.pool_pairs, probes);
+  std::vector<TestReport> reports;
+  const double nn = static_cast<double>(opts.pool_pairs);
+  for (std::size_t k = 0; k < probes.size(); ++k) {
+    const double* a = acc.data() + k * 6;
+    const std::string name =
+        "cross_pool_corr.i" + std::to_string(probes[k].out_i) + ".j" + std::to_string(probes[k].in_j);
+    const double mx = a[0] / nn, my = a[2] / nn;
+    const double vx = a[1] / nn - mx * mx, vy = a[3] / nn - my * my;
+    if (!(vx > 0.0) || !(vy > 0.0))
+      throw InvalidParameterError("cross_pool_correlation: zero-variance pool values at probe " + name);
+    const double denom = std::sqrt(vx * vy);
+    const double cov = a[4] / nn - mx * my;
+    const double mean_xy = a[4] / nn;
+    const double var_xy = a[5] / nn - mean_xy * mean_xy;
+    const double se = std::sqrt(var_xy / nn) / denom;
+    reports.push_back(TestReport::make(name, cov / denom, 0.0, se));
+  }
+  return reports;
+}
+
+// maxent::PoolSumSquares / pool_sum_squares_test (stats.cpp:340-369); the
+// per-pool sums are tree-ordered on the device (equal to rounding).
+struct PoolSumSquares {
+  TestReport mean_report;
+  TestReport variance_report;
+};
+inline PoolSumSquares pool_sum_squares_test(const GeneratorConfig& cfg, std::size_t pools) {
+  if (pools < 1000) throw InvalidParameterError("pool_sum_squares_test: pools must be >= 1000");
+  GeneratorConfig standardized = cfg;
+  standardized.out_mean = 0.0;
+  standardized.out_sigma = 1.0;
+  PoolBatch b(standardized, 1, &standardized.seed, WALLACE_F64);
+  std::vector<double> sums;
+  std::vector<std::uint8_t> marks;
+  b.pool_defect_stats(pools, std::numeric_limits<double>::infinity(), sums, marks);
+  const MomentSummary m = moments(sums);
+  const double nu = static_cast<double>(cfg.pool_size);
+  const double pp = static_cast<double>(pools);
+  const double se_mean = std::sqrt(m.variance / pp);
+  const double se_var = m.variance * std::sqrt(std::max(m.excess_kurtosis + 2.0, 0.0) / pp);
+  return {TestReport::make("pool_sum_squares.mean", m.mean, nu, se_mean),
+          TestReport::make("pool_sum_squares.variance", m.variance, 2.0 * nu, se_var)};
+}
+
+// maxent::rare_event_adjacency (stats.cpp:375-403, 424-447): marks from the
+// device, AdjacencyCounter over the consecutive emissions.
+inline TestReport rare_event_adjacency(const GeneratorConfig& cfg, std::size_t samples, double threshold) {
+  if (threshold < 3.0) throw InvalidParameterError("rare_event_adjacency: threshold must be >= 3");
+  if (samples < 100000) throw InvalidParameterError("rare_event_adjacency: samples must be >= 1e5");
+  GeneratorConfig standardized = cfg;
+  standardized.out_mean = 0.0;
+  standardized.out_sigma = 1.0;
+  const std::size_t pools = samples / (cfg.pool_size - 1);
+  PoolBatch b(standardized, 1, &standardized.seed, WALLACE_F64);
+  std::vector<double> sums;
+  std::vector<std::uint8_t> marks;
+  b.pool_defect_stats(pools, threshold, sums, marks);
+  std::uint64_t successors = 0, base = 0, cond_pop = 0, cond = 0;
+  for (std::size_t p = 1; p < pools; ++p) {
+    ++successors;
+    if (marks[p]) ++base;
+    if (marks[p - 1]) {
+      ++cond_pop;
+      if (marks[p]) ++cond;
+    }
+  }
+  std::string name = "rare_event_adjacency.pool" + std::to_string(cfg.pool_size);
+  if (cond_pop == 0 || base == 0) return TestReport::make(name + "[no-marks]", 1.0, 1.0, 0.0);
+  const double b_rate = static_cast<double>(base) / static_cast<double>(successors);
+  const double c_rate = static_cast<double>(cond) / static_cast<double>(cond_pop);
+  const double se_cond = std::sqrt(b_rate * (1.0 - b_rate) / static_cast<double>(cond_pop));
+  return TestReport::make(name, c_rate / b_rate, 1.0, se_cond / b_rate);
+}
 
 }  // namespace wallace_b200

@@ -27,6 +27,12 @@ void ref_get_pool(void* g, double* raw);
 void ref_get_stats(void* g, uint64_t* pass_count, uint64_t* draws, uint64_t* clamp,
                    double* sum_sq, double* reserved_prev);
 double ref_chi2_sample(double x, uint64_t nu, int method, int* clamped);
+int ref_cross_pool_correlation(void* g, uint64_t pool_pairs, uint32_t n_probes, const uint64_t* out_i,
+                               const uint64_t* in_j, double* out);
+int ref_pool_sum_squares(uint64_t pool_size, int chi2_method, uint64_t discard_every, uint64_t seed,
+                         int disable_chi2, int family, int mixing, uint64_t pools, double* out);
+int ref_rare_event_adjacency(uint64_t pool_size, int chi2_method, uint64_t discard_every, uint64_t seed,
+                             int disable_chi2, uint64_t samples, double threshold, double* out);
 }
 
 namespace wb = wallace_b200;
@@ -341,6 +347,45 @@ int main() {
     ok = ok && g.pass_count() == pc && g.uniform_draws() == dr && g.chi2_clamp_count() == cl &&
          g.pool().sum_sq == ss && g.pool().reserved_prev == rpv;
     CHECK(ok);
+  }
+  // stats.cpp defect suite through the drop-in (device accumulators)
+  {
+    wb::GeneratorConfig c = cfg_of(256, 9);
+    wb::Generator g(c);
+    Ref r(c);
+    wb::CrossPoolOptions o;
+    o.pool_pairs = 1500;
+    const auto mine = wb::cross_pool_correlation(g, o);
+    std::vector<uint64_t> oi, ij;
+    for (std::size_t k = 0; k < 8; ++k) {
+      oi.push_back((5 * k) % 256);
+      ij.push_back((11 * k + 3) % 256);
+    }
+    double out[32];
+    CHECK(ref_cross_pool_correlation(r.g, 1500, 8, oi.data(), ij.data(), out) == 8);
+    bool same = mine.size() == 8;
+    for (std::size_t k = 0; k < mine.size() && same; ++k)
+      same = mine[k].statistic == out[4 * k] && mine[k].expected == out[4 * k + 1] &&
+             mine[k].std_error == out[4 * k + 2] && mine[k].z_score == out[4 * k + 3];
+    CHECK(same);  // bit-identical probe sums -> identical reports
+    CHECK(same_bits(g.fill(1000), r.fill(1000)));  // the stream continues identically
+    CHECK_THROWS_AS(wb::cross_pool_correlation(g, wb::CrossPoolOptions{10, {}}), wb::InvalidParameterError);
+
+    wb::GeneratorConfig c2 = cfg_of(64, 3);
+    const wb::TestReport ra = wb::rare_event_adjacency(c2, 200000, 3.0);
+    double ro[4];
+    CHECK(ref_rare_event_adjacency(64, 2, 1, 3, 0, 200000, 3.0, ro) == 0);
+    CHECK(ra.statistic == ro[0] && ra.std_error == ro[2] && ra.z_score == ro[3]);
+    CHECK_THROWS_AS(wb::rare_event_adjacency(c2, 200000, 2.0), wb::InvalidParameterError);
+
+    wb::GeneratorConfig c3 = cfg_of(128, 5);
+    c3.discard_every = 2;
+    const wb::PoolSumSquares ps = wb::pool_sum_squares_test(c3, 1200);
+    double po[8];
+    CHECK(ref_pool_sum_squares(128, 2, 2, 5, 0, 0, 0, 1200, po) == 0);
+    CHECK(std::abs(ps.mean_report.statistic - po[0]) <= 1e-9 * po[0]);
+    CHECK(std::abs(ps.variance_report.statistic - po[4]) <= 1e-9 * po[4]);
+    CHECK(ps.mean_report.pass && ps.variance_report.pass);
   }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
