@@ -90,6 +90,17 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools,
 
 wallace_status wallace_destroy(wallace_handle* h);
 
+/* wallace_create with options.  WALLACE_CREATE_DEVICE_SEED runs the
+ * constructor's Polar fill and normalisation (generator.cpp:309-327) on the
+ * device, one CTA per pool: the xoshiro stream, the Polar acceptance
+ * sequence and the draw counts are exact, but the Polar values use CUDA's
+ * fp64 log, which can differ from the host glibc log by an ulp, so the
+ * seeded pools are within a few ulps of wallace_create's -- a fast start for
+ * large batches, NOT a parity path. */
+enum { WALLACE_CREATE_DEVICE_SEED = 1 };
+wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, const uint64_t* seeds,
+                                 wallace_dtype dtype, void* stream, uint32_t flags, wallace_handle** out);
+
 /* Generator::fill(std::span<double>) (generator.cpp:387-399) for every pool:
  * dev_out is a DEVICE buffer of n_pools * count_per_pool elements of the
  * handle's dtype, pool-major (pool p at [p*count, (p+1)*count)).  Exactly

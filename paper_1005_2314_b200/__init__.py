@@ -109,7 +109,10 @@ class PoolBatch:
     """
 
     def __init__(self, cfg: GeneratorConfig, n_pools: int = 1, seeds: Optional[Sequence[int]] = None,
-                 dtype: str = "f32", stream=None):
+                 dtype: str = "f32", stream=None, device_seed: bool = False):
+        """device_seed=True seeds the pools on the device (wallace_create_ex,
+        WALLACE_CREATE_DEVICE_SEED): exact xoshiro/Polar acceptance stream,
+        CUDA log -- within a few ulps of the host seeding, not a parity path."""
         self.L = _capi.load()
         self.cfg = cfg
         self.n_pools = int(n_pools)
@@ -127,8 +130,8 @@ class PoolBatch:
                 raise InvalidParameterError("seeds must have n_pools entries")
             seeds_ptr = seeds_arr.ctypes.data_as(C.POINTER(C.c_uint64))
         h = C.c_void_p()
-        _check(self.L.wallace_create(C.byref(cfg.to_c()), self.n_pools, seeds_ptr, self._dt,
-                                     self._stream, C.byref(h)))
+        _check(self.L.wallace_create_ex(C.byref(cfg.to_c()), self.n_pools, seeds_ptr, self._dt,
+                                        self._stream, 1 if device_seed else 0, C.byref(h)))
         self.h = h
 
     # -- lifecycle ---------------------------------------------------------

@@ -101,6 +101,7 @@ SYMBOLS = [
     ("wallace_rotation_table", None, [P(C.c_double), P(C.c_double), P(C.c_double)]),
     ("wallace_cross_pool_probes", i32, [vp, u64, C.c_uint32, P(u64), P(u64), P(C.c_double)]),
     ("wallace_write_stream", i32, [vp, u64, i32, i32]),
+    ("wallace_create_ex", i32, [P(wallace_config), u64, P(u64), i32, vp, C.c_uint32, P(vp)]),
     ("wallace_pool_defect_stats", i32, [vp, u64, C.c_double, P(C.c_double), P(C.c_uint8)]),
 ]
 

@@ -34,6 +34,8 @@ cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t
                                cudaStream_t s);
 int pool_kernel_threads(int dtype, int log2n);
 void affine_multipliers(int log2n, uint32_t* alpha, uint32_t* beta);
+cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
+                        PoolState* st, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
 cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void* leftover,
                                uint64_t n_pools, uint32_t N, double mean, cudaStream_t s);
@@ -619,7 +621,15 @@ wallace_status wallace_host_seed_pool(const wallace_config* cfg, uint64_t seed, 
 
 wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const uint64_t* seeds,
                               wallace_dtype dtype, void* stream, wallace_handle** out) {
+  return wallace_create_ex(cfg, n_pools, seeds, dtype, stream, 0u, out);
+}
+
+wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, const uint64_t* seeds,
+                                 wallace_dtype dtype, void* stream, uint32_t flags, wallace_handle** out) {
   if (!out) return fail(WALLACE_ERR_INVALID_PARAM, "out must not be NULL");
+  if (flags & ~uint32_t(WALLACE_CREATE_DEVICE_SEED))
+    return fail(WALLACE_ERR_INVALID_PARAM, "create: unknown flags");
+  const bool device_seed = (flags & WALLACE_CREATE_DEVICE_SEED) != 0;
   *out = nullptr;
   wallace_status st = validate(cfg);
   if (st) return st;
@@ -664,9 +674,9 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
 
   // ---- host seeding (parallel over pools) ----
   const uint64_t N = h->N;
-  std::vector<unsigned char> pools(n_pools * N * h->esize);
-  std::vector<PoolState> states(n_pools);
-  {
+  std::vector<unsigned char> pools(device_seed ? 0 : n_pools * N * h->esize);
+  std::vector<PoolState> states(device_seed ? 0 : n_pools);
+  if (!device_seed) {
     std::atomic<uint64_t> next{0};
     unsigned nt = std::max(1u, std::thread::hardware_concurrency());
     nt = static_cast<unsigned>(std::min<uint64_t>(nt, n_pools));
@@ -705,7 +715,7 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
     if (e_ != cudaSuccess)                                                                \
       return cleanup(fail(WALLACE_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)));    \
   } while (0)
-  WB_CUDA_C(cudaMalloc(&h->d_pools, pools.size()));
+  WB_CUDA_C(cudaMalloc(&h->d_pools, n_pools * N * h->esize));
   WB_CUDA_C(cudaMalloc(&h->d_state, n_pools * sizeof(PoolState)));
   WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * h->plan_words * sizeof(uint32_t)));
   WB_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -722,10 +732,27 @@ wallace_status wallace_create(const wallace_config* cfg, uint64_t n_pools, const
     h->bulk_ok = cfg->disable_chi2 && cfg->out_sigma == 1.0 && cfg->out_mean == 0.0 &&
                  !std::signbit(cfg->out_mean) && h->pass_type < 2 && !(nb && nb[0] == '1');
   }
-  WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,
-                            h->stream));
-  WB_CUDA_C(cudaMemcpyAsync(h->d_state, states.data(), n_pools * sizeof(PoolState),
-                            cudaMemcpyHostToDevice, h->stream));
+  if (!device_seed) {
+    WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,
+                              h->stream));
+    WB_CUDA_C(cudaMemcpyAsync(h->d_state, states.data(), n_pools * sizeof(PoolState),
+                              cudaMemcpyHostToDevice, h->stream));
+  } else {
+    // the constructor's Polar fill + normalisation on the device (seed_kernel)
+    uint64_t* d_seeds = nullptr;
+    if (seeds) {
+      WB_CUDA_C(cudaMalloc(&d_seeds, n_pools * sizeof(uint64_t)));
+      WB_CUDA_C(cudaMemcpyAsync(d_seeds, seeds, n_pools * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+    }
+    const cudaError_t e = wb::launch_seed(h->dtype, d_seeds, cfg->seed, static_cast<uint32_t>(N), h->d_pools,
+                                          h->d_state, n_pools, h->stream);
+    ++g_launches;
+    if (d_seeds) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(d_seeds);
+    }
+    WB_CUDA_C(e);
+  }
   // warm-up (generator.cpp:329-330)
   if ((st = run_passes(h, 16))) return cleanup(st);
   WB_CUDA_C(cudaStreamSynchronize(h->stream));

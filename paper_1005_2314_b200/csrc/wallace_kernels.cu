@@ -81,6 +81,110 @@ __global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device seeding (WALLACE_CREATE_DEVICE_SEED): the constructor's Polar fill
+// and normalisation (generator.cpp:309-331, baselines.cpp:19-66) for one pool
+// per CTA.  Thread 0 walks the pool's xoshiro256** stream and records the
+// accepted Polar pairs (u, v) -- the integer stream and the acceptance test
+// are exact; all threads then form the values u*f, v*f with
+// f = sqrt(-2 log(s)/s) using CUDA's log (within ~1 ulp of glibc's, so this
+// is NOT a parity path); thread 0 runs the sequential Neumaier normalisation.
+// Shared memory: (N + 2) doubles (pairs, then values in place) + N T values.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) seed_kernel(const uint64_t* seeds, uint64_t seed_base, uint32_t N,
+                                                   T* pools, PoolState* st) {
+  extern __shared__ __align__(16) unsigned char seed_smem[];
+  double* x = reinterpret_cast<double*>(seed_smem);             // N + 2
+  T* t = reinterpret_cast<T*>(seed_smem + (N + 2) * sizeof(double));  // N
+  __shared__ uint64_t s_state[4];
+  __shared__ uint64_t s_draws;
+  __shared__ double s_k;
+  const uint64_t pool = blockIdx.x;
+  const uint64_t seed = seeds ? seeds[pool] : seed_base + pool;
+  const uint32_t pairs = N / 2 + 1;  // N values + the reserved one (N even)
+  if (threadIdx.x == 0) {
+    uint64_t sm = seed, s[4];
+    for (int k = 0; k < 4; ++k) {  // baselines.cpp:19-31 splitmix64 seeding
+      uint64_t z = (sm += 0x9e3779b97f4a7c15ULL);
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      s[k] = z ^ (z >> 31);
+    }
+    uint64_t draws = 0;
+    auto next_u = [&]() -> double {  // uniform_next (baselines.cpp:33-49)
+      const uint64_t w = rotl64(s[1] * 5, 7) * 9;
+      const uint64_t tt = s[1] << 17;
+      s[2] ^= s[0];
+      s[3] ^= s[1];
+      s[1] ^= s[2];
+      s[0] ^= s[3];
+      s[2] ^= tt;
+      s[3] = rotl64(s[3], 45);
+      ++draws;
+      return __dmul_rn(static_cast<double>(w >> 11), 0x1.0p-53);
+    };
+    for (uint32_t i = 0; i < pairs;) {  // polar_next's acceptance loop
+      const double u = __dsub_rn(__dmul_rn(2.0, next_u()), 1.0);
+      const double v = __dsub_rn(__dmul_rn(2.0, next_u()), 1.0);
+      const double s2 = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
+      if (s2 >= 1.0 || s2 == 0.0) continue;
+      x[2 * i] = u;
+      x[2 * i + 1] = v;
+      ++i;
+    }
+    for (int k = 0; k < 4; ++k) s_state[k] = s[k];
+    s_draws = draws;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const double u = x[2 * i], v = x[2 * i + 1];
+    const double s2 = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
+    const double f = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(s2)), s2));
+    x[2 * i] = __dmul_rn(u, f);
+    x[2 * i + 1] = __dmul_rn(v, f);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // generator.cpp:318-327: Neumaier, k = sqrt(n / ss)
+    double sum = 0.0, comp = 0.0;
+    for (uint32_t i = 0; i < N; ++i) {
+      const double term = __dmul_rn(x[i], x[i]);
+      const double tt = __dadd_rn(sum, term);
+      comp = fabs(sum) >= fabs(term) ? __dadd_rn(comp, __dadd_rn(__dsub_rn(sum, tt), term))
+                                     : __dadd_rn(comp, __dadd_rn(__dsub_rn(term, tt), sum));
+      sum = tt;
+    }
+    s_k = __dsqrt_rn(__ddiv_rn(static_cast<double>(N), __dadd_rn(sum, comp)));
+  }
+  __syncthreads();
+  T* dst = pools + pool * N;
+  for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+    const T v = static_cast<T>(__dmul_rn(x[i], s_k));
+    t[i] = v;
+    dst[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0, comp = 0.0;  // recompute_sum_sq over the stored values
+    for (uint32_t i = 0; i < N; ++i) {
+      const double xi = static_cast<double>(t[i]);
+      const double term = __dmul_rn(xi, xi);
+      const double tt = __dadd_rn(sum, term);
+      comp = fabs(sum) >= fabs(term) ? __dadd_rn(comp, __dadd_rn(__dsub_rn(sum, tt), term))
+                                     : __dadd_rn(comp, __dadd_rn(__dsub_rn(term, tt), sum));
+      sum = tt;
+    }
+    PoolState ps{};
+    ps.reserved_prev = x[N];
+    ps.sum_sq = __dadd_rn(sum, comp);
+    for (int k = 0; k < 4; ++k) ps.s[k] = s_state[k];
+    ps.draws = s_draws;
+    ps.cursor = N - 1;
+    ps.seed = seed;
+    st[pool] = ps;
+  }
+}
+
 // Snapshot of the current emission before the pool is advanced outside
 // fill(): Generator::out_ keeps the old values until the next refill.
 template <typename T>
@@ -225,6 +329,21 @@ int pool_kernel_threads(int dtype, int log2n) {
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s) {
   const unsigned blocks = unsigned((a.n_pools + 127) / 128);
   plan_kernel<<<blocks, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
+                        PoolState* st, uint64_t n_pools, cudaStream_t s) {
+  const size_t smem = (N + 2) * sizeof(double) + N * (dtype == 0 ? 4 : 8);
+  if (dtype == 0) {
+    cudaError_t e = cudaFuncSetAttribute(seed_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    seed_kernel<float><<<unsigned(n_pools), 128, smem, s>>>(d_seeds, seed_base, N, static_cast<float*>(pools), st);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(seed_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    seed_kernel<double><<<unsigned(n_pools), 128, smem, s>>>(d_seeds, seed_base, N, static_cast<double*>(pools), st);
+  }
   return cudaGetLastError();
 }
 
