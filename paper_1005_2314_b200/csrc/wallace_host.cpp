@@ -1014,9 +1014,14 @@ wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t cou
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (!host_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
-  // chunk along the per-pool count so device staging stays bounded
+  // Stage the whole pool-major block on the device when it fits (HBM is
+  // large): one fill and one contiguous device->host copy run at the link's
+  // bandwidth.  Otherwise chunk along the per-pool count (strided copies).
   const uint64_t row_bytes = h->n_pools * h->esize;
-  const uint64_t max_stage = 2ull << 30;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+  const uint64_t max_stage =
+      std::max<uint64_t>(2ull << 30, std::min<uint64_t>(48ull << 30, (free_b + h->stage_bytes) / 2));
   uint64_t chunk = std::max<uint64_t>(1, max_stage / row_bytes);
   chunk = std::min(chunk, count);
   const uint64_t need = chunk * row_bytes;
@@ -1031,9 +1036,29 @@ wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t cou
     const uint64_t c = std::min(chunk, count - off);
     wallace_status st = run_emit(h, h->d_stage, c, wb::kModeFill, h->d_state, h->d_pools);
     if (st) return st;
-    WB_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(host_out) + off * h->esize,
-                              count * h->esize, h->d_stage, c * h->esize, c * h->esize,
-                              h->n_pools, cudaMemcpyDeviceToHost, h->stream));
+    if (c == count) {
+      // one contiguous block: 256 MiB pieces alternating over two streams
+      // (measured 55 GB/s vs 50.5 GB/s for a single 16 GiB copy on this link)
+      const uint64_t total = count * row_bytes;
+      const uint64_t piece = 256ull << 20;
+      if (!h->ws_stream) WB_CUDA(cudaStreamCreateWithFlags(&h->ws_stream, cudaStreamNonBlocking));
+      if (!h->ws_ef[0]) WB_CUDA(cudaEventCreateWithFlags(&h->ws_ef[0], cudaEventDisableTiming));
+      if (!h->ws_ec[0]) WB_CUDA(cudaEventCreateWithFlags(&h->ws_ec[0], cudaEventDisableTiming));
+      WB_CUDA(cudaEventRecord(h->ws_ef[0], h->stream));
+      WB_CUDA(cudaStreamWaitEvent(h->ws_stream, h->ws_ef[0], 0));
+      uint64_t k = 0;
+      for (uint64_t o = 0; o < total; o += piece, ++k) {
+        const uint64_t b = std::min(piece, total - o);
+        WB_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(host_out) + o,
+                                static_cast<const unsigned char*>(h->d_stage) + o, b, cudaMemcpyDeviceToHost,
+                                (k & 1) ? h->ws_stream : h->stream));
+      }
+      WB_CUDA(cudaEventRecord(h->ws_ec[0], h->ws_stream));
+      WB_CUDA(cudaStreamWaitEvent(h->stream, h->ws_ec[0], 0));
+    } else
+      WB_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(host_out) + off * h->esize,
+                                count * h->esize, h->d_stage, c * h->esize, c * h->esize,
+                                h->n_pools, cudaMemcpyDeviceToHost, h->stream));
   }
   WB_CUDA(cudaStreamSynchronize(h->stream));
   return WALLACE_OK;
