@@ -154,6 +154,16 @@ def cpu_reference_run(cfg, n_pools, count, threads, seed_base=1):
     return tf.value, ti.value
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_sample_size(cfg, target_values):
     pools = max(1, min(cfg["pools"], target_values // cfg["count"]))
     return pools
@@ -191,7 +201,7 @@ def run_reference(args):
         "data": "synthetic (seeded pools)",
         "config": {"workload": cfg["name"], "sample_pools": n_pools, "threads": threads},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "init_s_per_step": statistics.median(inits),
     }
@@ -359,9 +369,15 @@ def run_ours(args):
                 threads = os.cpu_count() or 1
                 sp = cpu_sample_size(cfg, 1 << 29)
                 tf, ti = cpu_reference_run(cfg, sp, count, threads)
+                # the 1-core rate beside the all-core one, on a
+                # smaller sample of the same job
+                sp1 = max(1, sp // 64)
+                tf1, _ = cpu_reference_run(cfg, sp1, count, 1)
                 cpu = {"value": sp * count / tf, "unit": UNIT, "cores": threads, "kind": "reference",
                        "sample": f"{sp} of {n_pools} pools x {count} variates, fp64 reference "
-                                 f"Generator::fill, construction ({ti:.2f}s) excluded"}
+                                 f"Generator::fill, construction ({ti:.2f}s) excluded",
+                       "value_1core": sp1 * count / tf1, "sample_1core": f"{sp1} pools x {count} variates",
+                       "cpu_model": cpu_model(), "nproc": os.cpu_count()}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "error": str(ex)[:200]}
 
