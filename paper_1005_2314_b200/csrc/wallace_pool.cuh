@@ -117,6 +117,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_CHAINW
 #define WB_CHAINW 0
 #endif
+// chain-warp kernels: nanoseconds a waiting warp sleeps between polls (0: spin)
+#ifndef WB_CHAIN_SLEEP
+#define WB_CHAIN_SLEEP 32
+#endif
 // ABLATION builds only: consumer without histogram (1) / moments (2) / both (3)
 #ifndef WB_CONS_ABLATE
 #define WB_CONS_ABLATE 0
@@ -1178,7 +1182,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   constexpr bool ROT = PT >= 2;
   constexpr uint32_t PFLIP = ROT ? 0u : FLIP;
   constexpr uint32_t PW = ROT ? 2u : 1u;
-  static_assert(!ROT || (G::JC == G::J && !G::CHAINW && !G::INPLACE),
+  static_assert(!ROT || (G::JC == G::J && !G::INPLACE),
                 "rotation passes hold all 4-blocks of a thread across their inner barrier");
   __shared__ __align__(1024) unsigned char s_pool[SM::STATIC ? SM::TOTAL : 16];
   extern __shared__ __align__(1024) unsigned char dsmem[];
@@ -1275,6 +1279,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           else
             run_pass<T, LOG2N, G::JC, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs);
         }
+      } else if constexpr (ROT) {
+        __syncthreads();  // the chain warp joins the rotation pass's inner barrier
       }
       __syncthreads();
       cur_off ^= PFLIP;
@@ -1341,7 +1347,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           // S/r/scale of emission e come from the chain warp: one lane per
           // warp polls (acquire), __syncwarp orders the other lanes' reads
           if (lane == 0)
-            while (ld_acquire_cta(&s.ready) < e) __nanosleep(32);
+            while (ld_acquire_cta(&s.ready) < e) {
+              if (WB_CHAIN_SLEEP) __nanosleep(WB_CHAIN_SLEEP);
+            }
           __syncwarp();
           sc = from_double<T>(*static_cast<volatile double*>(&s.scale[slot]));
         }
@@ -1379,6 +1387,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           }
           x_last = X[JCL - 1][3];
         }
+        if constexpr (ROT && G::CHAINW)
+          if (!compute) __syncthreads();  // the chain warp joins the rotation pass's inner barrier
         if constexpr (MODE == kModeConsume)
           if (do_emit) cons.flush();
         if constexpr (MODE == kModeDefect) {
