@@ -103,6 +103,16 @@ struct FillArgs {
   uint32_t n_probes;      // 0 = no probes
   uint32_t probe_out[32];
   uint32_t probe_in[32];
+  // HBM-resident large pools (wallace_large.cu): second pool buffer, per-pool
+  // chain state, the pass constants and the pass count before this launch
+  void* lg_pool2;
+  void* lg_state;
+  uint64_t lg_stride;     // default_stride(rows) % rows
+  uint64_t lg_alpha;      // default_multipliers(N)
+  uint64_t lg_beta;
+  uint64_t lg_pass0;
+  int32_t lg_log2n;
+  int32_t pad_lg;
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]
@@ -118,6 +128,7 @@ struct PlanArgs {
   uint32_t off_mask;       // rows-1 (stride_transpose) or N-1 (affine)
   int32_t fixed_transform;
   int32_t rotation;        // family: two plan words per pass
+  int32_t large;           // HBM-resident pools: 31-bit offsets, 2 (wallace4) / 3 (rotation) words
 };
 
 }  // namespace wb

@@ -34,6 +34,7 @@ cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t
                                cudaStream_t s);
 int pool_kernel_threads(int dtype, int log2n);
 void affine_multipliers(int log2n, uint32_t* alpha, uint32_t* beta);
+size_t large_state_bytes();
 cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
                         PoolState* st, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
@@ -218,6 +219,10 @@ struct wallace_handle {
   int key = 0;        // kernel key: log2(N) (+16 for the latency kernel)
   int kmode = 0;      // 0 auto, 1 throughput, 2 latency
   bool bulk_ok = false;  // fills may use the bulk-emission kernel
+  // pools above the on-chip limit: HBM-resident executor (wallace_large.cu)
+  bool large = false;
+  void* d_lg_pool2 = nullptr;
+  void* d_lg_state = nullptr;
   // defect suite (wallace_cross_pool_probes / wallace_pool_defect_stats)
   double* d_probe_acc = nullptr;
   uint32_t n_probes = 0;  // active only inside wallace_cross_pool_probes
@@ -316,20 +321,23 @@ wallace_status validate(const wallace_config* c) {
 }
 
 wallace_status check_supported(const wallace_config* c, int dtype) {
-  const uint64_t lim = dtype == WALLACE_F32 ? (1u << 14) : (1u << 13);
-  if (c->pool_size > lim)
-    return fail(WALLACE_ERR_UNSUPPORTED,
-                "pool_size %llu exceeds the on-chip pool limit %llu for this dtype",
-                static_cast<unsigned long long>(c->pool_size),
-                static_cast<unsigned long long>(lim));
-  return WALLACE_OK;
+  (void)c;
+  (void)dtype;
+  return WALLACE_OK;  // pools above the on-chip limit run HBM-resident
 }
+
+// pools above this run on the HBM-resident executor
+uint64_t onchip_limit(int dtype) { return dtype == WALLACE_F32 ? (1u << 14) : (1u << 13); }
 
 // Few pools cannot fill the GPU with the throughput kernel (a few warps per
 // pool): give each pool a CTA of up to 1024 threads instead.
 constexpr uint64_t kLatencyMaxPools = 148;
 
 void select_kernel(wallace_handle* h) {
+  if (h->large) {
+    h->key = 64 + h->log2n;  // launch_pool_kernel -> the HBM-resident executor
+    return;
+  }
   const int lim = h->dtype == WALLACE_F32 ? 14 : 13;
   const bool lat_ok = h->log2n >= 8 && h->log2n <= lim;
   bool lat = false;
@@ -360,6 +368,17 @@ wb::FillArgs base_args(wallace_handle* h) {
   a.def_marks = h->d_def_marks;
   a.def_stride = h->def_stride;
   a.def_threshold = h->def_threshold;
+  if (h->large) {
+    const uint64_t rows = h->N / 4;
+    uint64_t al = 0, be = 0;
+    default_multipliers(h->N, al, be);
+    a.lg_pool2 = h->d_lg_pool2;
+    a.lg_state = h->d_lg_state;
+    a.lg_stride = default_stride(rows) % rows;
+    a.lg_alpha = al;
+    a.lg_beta = be;
+    a.lg_log2n = h->log2n;
+  }
   std::memcpy(a.rot_c, h->rot_c, sizeof(a.rot_c));
   std::memcpy(a.rot_s, h->rot_s, sizeof(a.rot_s));
   return a;
@@ -420,6 +439,7 @@ wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
     p.off_mask = static_cast<uint32_t>(h->cfg.mixing == 0 ? h->N / 4 - 1 : h->N - 1);
     p.fixed_transform = h->cfg.fixed_transform;
     p.rotation = h->cfg.transform_family == 1;
+    p.large = h->large ? 1 : 0;
     WB_CUDA(timed(h, h->ev_plan, h->side, [&] { return wb::launch_plan_kernel(p, h->side); }));
     ++g_launches;
     WB_CUDA(cudaEventRecord(h->ev_planned[k & 1], h->side));
@@ -446,6 +466,7 @@ wallace_status run_passes(wallace_handle* h, uint64_t n) {
   while (n > 0) {
     const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(n, h->plan_cap));
     Launch l{base_args(h)};
+    l.a.lg_pass0 = h->pass_count;
     l.a.mode = wb::kModePasses;
     l.a.n_passes = k;
     l.a.n_emit = 0;
@@ -536,6 +557,7 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     a.n_emit = static_cast<uint32_t>(e);
     a.n_passes = static_cast<uint32_t>(passes);
     a.last_limit = static_cast<uint32_t>(last_limit);
+    a.lg_pass0 = h->pass_count;
     if (a.d != h->cfg.discard_every) {
       // the huge-discard path ran d-1 passes eagerly: keep launch order
       std::vector<Launch> one{Launch{a}};
@@ -649,7 +671,12 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
   h->stream = static_cast<cudaStream_t>(stream);
   h->chi2 = chi2_consts(*cfg);
   h->pass_type = 2 * cfg->transform_family + cfg->mixing;
-  h->plan_words = cfg->transform_family == 1 ? 2 : 1;
+  h->large = cfg->pool_size > onchip_limit(dtype);
+  if (h->large && device_seed) {
+    delete h;
+    return fail(WALLACE_ERR_UNSUPPORTED, "create: device seeding covers on-chip pool sizes only");
+  }
+  h->plan_words = h->large ? (cfg->transform_family == 1 ? 3 : 2) : (cfg->transform_family == 1 ? 2 : 1);
   h->plan_cap = static_cast<uint32_t>(std::max<uint64_t>(
       1, std::min<uint64_t>(kMaxPassesPerLaunch, kPlanBudgetBytes / (4 * h->plan_words * n_pools))));
   rotation_table(h->rot_c, h->rot_s);
@@ -717,6 +744,10 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
   } while (0)
   WB_CUDA_C(cudaMalloc(&h->d_pools, n_pools * N * h->esize));
   WB_CUDA_C(cudaMalloc(&h->d_state, n_pools * sizeof(PoolState)));
+  if (h->large) {
+    WB_CUDA_C(cudaMalloc(&h->d_lg_pool2, n_pools * N * h->esize));
+    WB_CUDA_C(cudaMalloc(&h->d_lg_state, n_pools * wb::large_state_bytes()));
+  }
   WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * h->plan_words * sizeof(uint32_t)));
   WB_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
@@ -779,6 +810,8 @@ wallace_status wallace_destroy(wallace_handle* h) {
   cudaFree(h->d_part_sums);
   cudaFree(h->d_part_hist);
   cudaFree(h->d_stage);
+  cudaFree(h->d_lg_pool2);
+  cudaFree(h->d_lg_state);
   for (int k = 0; k < 2; ++k) {
     cudaFree(h->ws_dev[k]);
     cudaFreeHost(h->ws_host[k]);
@@ -1160,6 +1193,7 @@ wallace_status wallace_cross_pool_probes(wallace_handle* h, uint64_t passes, uin
                                          const uint64_t* out_i, const uint64_t* in_j, double* acc) {
   if (!h || !out_i || !in_j || !acc) return fail(WALLACE_ERR_INVALID_PARAM, "handle/probes/acc must not be NULL");
   if (n_probes < 1 || n_probes > 32) return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_probes: 1..32 probes");
+  if (h->large) return fail(WALLACE_ERR_UNSUPPORTED, "cross_pool_probes: on-chip pool sizes only");
   if (passes < 1) return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_probes: passes must be >= 1");
   for (uint32_t k = 0; k < n_probes; ++k)
     if (out_i[k] >= h->N || in_j[k] >= h->N)
@@ -1191,6 +1225,7 @@ wallace_status wallace_pool_defect_stats(wallace_handle* h, uint64_t emissions, 
                                          double* totals, uint8_t* marks) {
   if (!h || !totals || !marks) return fail(WALLACE_ERR_INVALID_PARAM, "handle/totals/marks must not be NULL");
   if (emissions < 1) return fail(WALLACE_ERR_INVALID_PARAM, "pool_defect_stats: emissions must be >= 1");
+  if (h->large) return fail(WALLACE_ERR_UNSUPPORTED, "pool_defect_stats: on-chip pool sizes only");
   if (!(h->cfg.out_mean == 0.0) || !(h->cfg.out_sigma == 1.0))
     return fail(WALLACE_ERR_INVALID_PARAM,
                 "pool_defect_stats: the handle's config must be standardized (out_mean 0, out_sigma 1)");
@@ -1386,6 +1421,7 @@ static wallace_status finish_consumer(cudaStream_t stream, const double* part_su
 static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sums[4],
                                    uint64_t hist[258], bool from_snapshot) {
   if (!h || !sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "handle/sums/hist must not be NULL");
+  if (h->large) return fail(WALLACE_ERR_UNSUPPORTED, "consume: fused consumers cover on-chip pool sizes only");
   if (from_snapshot && !h->has_snapshot) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (h->part_cap < h->n_pools) {

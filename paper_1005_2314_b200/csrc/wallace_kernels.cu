@@ -30,10 +30,11 @@ __global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
   // plan words of this launch: one per pass (wallace4: offset | variant << 16)
   // or two (rotation: per sweep offset | t_index << 16 | negate << 20;
   // decode_pass_plan, generator.cpp:238-257)
-  const uint32_t pw = a.rotation ? 2u : 1u;
+  const uint32_t pw = a.large ? (a.rotation ? 3u : 2u) : (a.rotation ? 2u : 1u);
   const uint32_t n_words = a.n_passes * pw;
-  for (uint32_t base = 0; base < n_words; base += 32) {
-    const uint32_t cnt = min(32u, n_words - base);
+  const uint32_t step = 32u - 32u % pw;  // whole passes per staged tile
+  for (uint32_t base = 0; base < n_words; base += step) {
+    const uint32_t cnt = min(step, n_words - base);
     for (uint32_t i = 0; i < cnt; i += pw) {
       uint64_t w2[2];
 #pragma unroll
@@ -47,7 +48,22 @@ __global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
         s2 ^= t;
         s3 = rotl64(s3, 45);
       }
-      if (!a.rotation) {
+      if (a.large) {
+        // wallace_large.cu plan words: offsets need up to 31 bits
+        uint32_t o0 = static_cast<uint32_t>(w2[1]) & a.off_mask;
+        uint32_t o1 = static_cast<uint32_t>(w2[1] >> 32) & a.off_mask;
+        uint32_t x = a.rotation ? static_cast<uint32_t>((w2[0] & 15u) | ((w2[0] >> 4) & 1u) << 4 |
+                                                        ((w2[0] >> 5) & 15u) << 8 | ((w2[0] >> 9) & 1u) << 12)
+                                : static_cast<uint32_t>(w2[0] % 384u);
+        if (a.fixed_transform) o0 = o1 = x = 0;
+        tile[w][lane][i] = o0;
+        if (a.rotation) {
+          tile[w][lane][i + 1] = o1;
+          tile[w][lane][i + 2] = x;
+        } else {
+          tile[w][lane][i + 1] = x;
+        }
+      } else if (!a.rotation) {
         uint32_t variant = static_cast<uint32_t>(w2[0] % 384u);
         uint32_t off = static_cast<uint32_t>(w2[1]) & a.off_mask;
         if (a.fixed_transform) variant = off = 0;  // PassPlan{} (generator.cpp:336-338)
@@ -289,8 +305,13 @@ __global__ void __launch_bounds__(128)
   for (int i = tid; i < 258; i += 128) part_hist[blockIdx.x * 258 + i] = hist[i];
 }
 
+cudaError_t launch_pool_large(int dtype, const FillArgs& a, uint64_t n_pools, cudaStream_t s);
+
+size_t large_state_bytes() { return sizeof(SState); }
+
 cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t n_pools,
                                cudaStream_t s) {
+  if (log2n >= 64) return launch_pool_large(dtype, a, n_pools, s);  // HBM-resident pools
   switch (a.pass_type) {
     case 0: return launch_pool_pt<0>(dtype, log2n, a, n_pools, s);
     case 1: return launch_pool_pt<1>(dtype, log2n, a, n_pools, s);

@@ -120,9 +120,18 @@ int main() {
     cfg.out_mean = 0.0;
     cfg.validate();
     CHECK_THROWS_AS(wb::Generator(cfg_of(48, 0)), wb::ConfigError);
-    // the on-chip pool limit (fp64 pools above 2^13) is the one reported
-    // UnsupportedError of the drop-in
-    CHECK_THROWS_AS(wb::Generator(cfg_of(1u << 14, 1)), wb::UnsupportedError);
+  }
+  // a pool above the on-chip limit (fp64 N = 2^14) runs HBM-resident: the
+  // same stream as the reference, across a renormalisation
+  {
+    wb::Generator g(cfg_of(1u << 14, 1));
+    Ref r(cfg_of(1u << 14, 1));
+    CHECK(same_bits(g.fill(250000), r.fill(250000)));
+    for (int i = 0; i < 260; ++i) {
+      g.step_pass();
+      ref_step_pass(r.g);
+    }
+    CHECK(same_bits(g.fill(70000), r.fill(70000)));
   }
   // rotation family and affine mixing (generator.cpp:86-172): the same
   // stream as the reference, through next_normal / fill / step_pass
