@@ -34,8 +34,6 @@ CONFIGS = [
 @pytest.mark.parametrize("fam,mix", FAMILIES, ids=FAM_IDS)
 @pytest.mark.parametrize("kw", CONFIGS, ids=lambda k: "_".join(f"{a}{b}" for a, b in k.items()))
 def test_family_fill_matches_oracle(cuda, kw, fam, mix, dtype, kernel):
-    if dtype == "f64" and kw["pool_size"] > 8192:
-        pytest.skip("f64 on-chip limit")
     n = kw["pool_size"]
     seeds = [11, 12, 1013]
     # several emissions, misaligned pool-major stride, and > 256 passes

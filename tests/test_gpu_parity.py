@@ -65,8 +65,6 @@ CONFIGS = [
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("kw", CONFIGS, ids=lambda k: "_".join(f"{a}{b}" for a, b in k.items()))
 def test_fill_matches_oracle(cuda, dtype, kw, kernel):
-    if dtype == "f64" and kw["pool_size"] > 8192:
-        pytest.skip("f64 on-chip limit")
     n = kw["pool_size"]
     seeds = [11, 12, 1013]
     count = 3 * n + 5  # several emissions, misaligned pool-major stride
