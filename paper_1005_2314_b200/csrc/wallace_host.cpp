@@ -536,15 +536,24 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
       } else {
         // an emission longer than one launch: run d-1 passes first, then a
         // launch with one pass and the emission (emission alignment is
-        // per launch)
-        wallace_status st = WALLACE_OK;
-        if (!first || (st_first == h->d_state && pools_first == h->d_pools)) {
-          st = issue(h, ls);
-          ls.clear();
-          if (!st) st = run_passes(h, d - 1);
-        } else {
-          return fail(WALLACE_ERR_UNSUPPORTED, "discard_every too large for snapshot replay");
+        // per launch).  The passes must not run before the partially
+        // consumed emission is drained (or before the snapshot being
+        // replayed is in the live buffers): a drain-only launch does that.
+        if (first && (lead > 0 || st_first != h->d_state || pools_first != h->d_pools)) {
+          a.lead = static_cast<uint32_t>(lead);
+          a.n_emit = 0;
+          a.n_passes = 0;
+          a.last_limit = 0;
+          a.lg_pass0 = h->pass_count;
+          ls.push_back(Launch{a});
+          h->cursor += static_cast<uint32_t>(lead);
+          produced += lead;
+          first = false;
+          continue;
         }
+        wallace_status st = issue(h, ls);
+        ls.clear();
+        if (!st) st = run_passes(h, d - 1);
         if (st) return st;
         e = 1;
         passes = 1;
@@ -1453,7 +1462,9 @@ static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sum
   while (done < count) {
     // values a single launch produces: the lead plus per_launch_emit emissions
     const uint64_t lead = (h->cursor < n1) ? (n1 - h->cursor) : 0;
-    const uint64_t cap = lead + per_launch_emit * n1;
+    // one launch per run_emit (the partials are per launch): an emission
+    // longer than a launch drains a pending lead in a call of its own
+    const uint64_t cap = (d > h->plan_cap && lead > 0) ? lead : lead + per_launch_emit * n1;
     const uint64_t c = std::min(cap, count - done);
     const bool snap = from_snapshot && first;
     wallace_status st = run_emit(h, nullptr, c, wb::kModeConsume, snap ? h->d_snap_state : h->d_state,

@@ -375,3 +375,51 @@ def test_bulk_disabled_by_nonfinite_pool(cuda):
     # the other pools keep their exact streams
     o1 = OracleGen(ocfg(seed=seeds[1], **kw), "f32")
     assert_same(b.fill(3000).cpu().numpy()[1], (o1.fill(5 * 1023 + 2), o1.fill(3000))[1], "pool 1")
+
+
+@pytest.mark.parametrize("kernel", ["throughput", "latency"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_huge_discard_every(cuda, dtype, kernel):
+    """discard_every above one launch's plan capacity (2048 passes): the host
+    runs d-1 passes, then a launch with the last pass and the emission; a
+    pending partial emission is drained before those passes, and snapshot
+    replay copies the snapshot into the live buffers first."""
+    kw = dict(pool_size=256, discard_every=2500)
+    seeds = [5, 6]
+    b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=seeds, dtype=dtype)
+    b.set_kernel_mode(kernel)
+    o = [OracleGen(ocfg(seed=s, **kw), dtype) for s in seeds]
+    for k in (5, 300, 258, 1):
+        got = b.fill(k).cpu().numpy()
+        for p in range(2):
+            assert_same(got[p], o[p].fill(k), f"fill {k} pool {p}")
+    b.snapshot()
+    first = b.fill(400).cpu().numpy()
+    for p in range(2):
+        assert_same(first[p], o[p].fill(400), f"fill after snapshot pool {p}")
+    import torch
+    t = torch.empty(first.shape, dtype=b.torch_dtype, device="cuda")
+    b.fill_from_snapshot_into(t)
+    assert_same(t.cpu().numpy()[0], first[0], "snapshot replay")
+
+
+def test_huge_discard_every_consume(cuda):
+    """The consumer across a pending lead with an emission longer than one
+    launch: the same values as the fills (histogram exact, sums to rounding)."""
+    kw = dict(pool_size=256, discard_every=2500)
+    seeds = np.array([5, 6], dtype=np.uint64)
+    b = pb.PoolBatch(gcfg(**kw), n_pools=2, seeds=seeds, dtype="f64")
+    b.consume(7)
+    sums, hist = b.consume(600)
+    vals = []
+    for s in seeds:
+        o = OracleGen(ocfg(seed=int(s), **kw), "f64")
+        o.fill(7)
+        vals.append(o.fill(600))
+    v = np.concatenate(vals)
+    want = np.array([np.sum(v), np.sum(v * v), np.sum(v ** 3), np.sum(v ** 4)])
+    assert np.allclose(sums, want, rtol=1e-12, atol=1e-9)
+    bins = np.floor((v + 8.0) * 16.0)
+    assert int(hist[0]) == int(np.sum(bins < 0)) and int(hist[257]) == int(np.sum(bins >= 256))
+    inside = bins[(bins >= 0) & (bins < 256)].astype(int)
+    assert np.array_equal(hist[1:257], np.bincount(inside, minlength=256))
