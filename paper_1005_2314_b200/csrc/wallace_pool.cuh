@@ -121,6 +121,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_CHAIN_SLEEP
 #define WB_CHAIN_SLEEP 32
 #endif
+// 1: the consumer's four power sums as two packed f32x2 FMAs
+#ifndef WB_CONS_PACKED
+#define WB_CONS_PACKED 1
+#endif
 // ABLATION builds only: consumer without histogram (1) / moments (2) / both (3)
 #ifndef WB_CONS_ABLATE
 #define WB_CONS_ABLATE 0
@@ -486,14 +490,25 @@ struct Consumer {
   __device__ __forceinline__ void add(T x) {
     if (WB_CONS_ABLATE != 2 && WB_CONS_ABLATE != 3) {
       const T x2 = mul_rn(x, x);
-      a1 = add_rn(a1, x);
-      a2 = add_rn(a2, x2);
-      a3 = fma_rn(x2, x, a3);
-      a4 = fma_rn(x2, x2, a4);
+      if constexpr (sizeof(T) == 4 && WB_CONS_PACKED) {
+        // (a1, a2) += (x, x^2) and (a3, a4) += (x^2 * x, x^2 * x^2) as two
+        // packed f32x2 FMAs (the add as fma(.., 1, ..): no contraction risk)
+        uint64_t p12 = pk2(a1, a2), p34 = pk2(a3, a4);
+        p12 = fma2_rn(pk2(x, x2), pk2(1.0f, 1.0f), p12);
+        p34 = fma2_rn(pk2(x2, x2), pk2(x, x2), p34);
+        upk2(p12, a1, a2);
+        upk2(p34, a3, a4);
+      } else {
+        a1 = add_rn(a1, x);
+        a2 = add_rn(a2, x2);
+        a3 = fma_rn(x2, x, a3);
+        a4 = fma_rn(x2, x2, a4);
+      }
     }
     if (WB_CONS_ABLATE != 1 && WB_CONS_ABLATE != 3) {
-      // bin = floor((x + 8) * 16) in T, clamped to [-1, 256] (under / over)
-      const T t = mul_rn(add_rn(x, T(8)), T(16));
+      // bin = floor((x + 8) * 16) in T, clamped to [-1, 256] (under / over);
+      // fl(fl(x + 8) * 16) == fma(x, 16, 128): scaling by 16 is exact
+      const T t = fma_rn(x, T(16), T(128));
       int bin = sizeof(T) == 4 ? __float2int_rd(static_cast<float>(t)) : __double2int_rd(static_cast<double>(t));
       bin = max(-1, min(bin, 256));
       atomicAdd(&hist[bin + 1], 1u);
