@@ -57,9 +57,25 @@ __global__ void lg_lead(const FillArgs a, const T* pool_buf, uint64_t N) {
   static_cast<T*>(a.out)[pool * a.out_stride + a.out_offset + i] = v;
 }
 
+// Fused emission (emit_slot >= 0): the pass's outputs x, scaled, are the
+// emission (values i < limit at output offset gofs) -- valid when no
+// renormalisation follows the pass.
+template <typename T>
+__device__ __forceinline__ void lg_emit4(const FillArgs& a, uint64_t pool, uint64_t i0, const T* x, int slot,
+                                         uint64_t gofs, uint32_t limit) {
+  const SState& s = static_cast<const SState*>(a.lg_state)[pool];
+  const T sc = from_double<T>(s.scale[slot]);
+  const T mean = from_double<T>(a.mean);
+  T* o = static_cast<T*>(a.out) + pool * a.out_stride + gofs;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (i0 + k < limit) o[i0 + k] = emit_value(x[k], sc, mean, a.mean_is_zero != 0);
+}
+
 // One wallace4 pass (generator.cpp:52-110), a thread per 4-block.
 template <typename T, int MIX>
-__global__ void lg_pass_wallace(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N) {
+__global__ void lg_pass_wallace(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N, int emit_slot,
+                                uint64_t gofs, uint32_t limit) {
   const uint64_t pool = blockIdx.y;
   const uint64_t rows = N / 4;
   const uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -81,17 +97,21 @@ __global__ void lg_pass_wallace(const FillArgs a, const T* in, T* out, uint32_t 
   const T z[4] = {sub_rn(aa, dd), add_rn(bb, cc), sub_rn(bb, cc), sub_rn(-aa, dd)};
   const int perm = int(variant >> 4);
   T* dst = out + pool * N + 4 * b;
+  T x[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const T h = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
-    dst[k] = mul_rn(h, z[perm_at(perm, k)]);
+    x[k] = mul_rn(h, z[perm_at(perm, k)]);
+    dst[k] = x[k];
   }
+  if (emit_slot >= 0) lg_emit4(a, pool, 4 * b, x, emit_slot, gofs, limit);
 }
 
 // One rotation half-sweep (generator.cpp:113-172), a thread per 4-block of
 // the output; sweep 1 gathers the block's neighbours g[4b-1], g[4b+4] too.
 template <typename T, int MIX, int SWEEP>
-__global__ void lg_pass_rotation(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N) {
+__global__ void lg_pass_rotation(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N, int emit_slot,
+                                 uint64_t gofs, uint32_t limit) {
   const uint64_t pool = blockIdx.y;
   const uint64_t rows = N / 4;
   const uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -124,10 +144,14 @@ __global__ void lg_pass_rotation(const FillArgs a, const T* in, T* out, uint32_t
   } else {
     const T hm = g(4 * b + N - 1), h0 = g(4 * b), h1 = g(4 * b + 1), h2 = g(4 * b + 2), h3 = g(4 * b + 3),
             hp = g(4 * b + 4);
-    dst[0] = add_rn(mul_rn(nse, hm), mul_rn(ce, h0));
-    dst[1] = add_rn(mul_rn(ce, h1), mul_rn(se, h2));
-    dst[2] = add_rn(mul_rn(nse, h1), mul_rn(ce, h2));
-    dst[3] = add_rn(mul_rn(ce, h3), mul_rn(se, hp));
+    T x[4];
+    x[0] = add_rn(mul_rn(nse, hm), mul_rn(ce, h0));
+    x[1] = add_rn(mul_rn(ce, h1), mul_rn(se, h2));
+    x[2] = add_rn(mul_rn(nse, h1), mul_rn(ce, h2));
+    x[3] = add_rn(mul_rn(ce, h3), mul_rn(se, hp));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k] = x[k];
+    if (emit_slot >= 0) lg_emit4(a, pool, 4 * b, x, emit_slot, gofs, limit);
   }
 }
 
@@ -252,16 +276,17 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
     const dim3 g(unsigned((a.lead + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
     lg_lead<T><<<g, kLgThreads, 0, st>>>(a, w[0], N);
   }
-  auto pass = [&](uint32_t p) {
+  // one pass; emit_slot >= 0 fuses the emission (values i < limit at gofs)
+  auto pass = [&](uint32_t p, int es = -1, uint64_t go = 0, uint32_t lim = 0) {
     if (!rot) {
-      if (pt == 0) lg_pass_wallace<T, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N);
-      else lg_pass_wallace<T, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N);
+      if (pt == 0) lg_pass_wallace<T, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, es, go, lim);
+      else lg_pass_wallace<T, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, es, go, lim);
     } else if (pt == 2) {
-      lg_pass_rotation<T, 0, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N);
-      lg_pass_rotation<T, 0, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur ^ 1], w[cur], p, N);
+      lg_pass_rotation<T, 0, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, -1, 0, 0);
+      lg_pass_rotation<T, 0, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur ^ 1], w[cur], p, N, es, go, lim);
     } else {
-      lg_pass_rotation<T, 1, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N);
-      lg_pass_rotation<T, 1, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur ^ 1], w[cur], p, N);
+      lg_pass_rotation<T, 1, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, -1, 0, 0);
+      lg_pass_rotation<T, 1, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur ^ 1], w[cur], p, N, es, go, lim);
     }
     if (!rot) cur ^= 1;
   };
@@ -284,11 +309,16 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
       const int slot = e & 1;
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
       for (uint32_t q = 1; q <= a.d; ++q, ++p) {
-        pass(p);
+        const bool emit = q == a.d;
+        const bool fuse = emit && pc != 0;  // no renormalisation between the pass and its emission
+        if (fuse) pass(p, slot, gofs, limit);
+        else pass(p);
         if (pc == 0) renorm(slot, 1);
-        if (q == a.d) {
-          const dim3 g(unsigned((limit + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
-          lg_emit<T><<<g, kLgThreads, 0, st>>>(a, w[cur], N, gofs, limit, slot);
+        if (emit) {
+          if (!fuse) {
+            const dim3 g(unsigned((limit + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
+            lg_emit<T><<<g, kLgThreads, 0, st>>>(a, w[cur], N, gofs, limit, slot);
+          }
           lg_chain<T><<<pool_blocks, 128, 0, st>>>(a, w[cur], N, slot, e + 1 < a.n_emit ? 1 : 0, n_pools);
         }
         pc = (pc + 1) & 255u;
