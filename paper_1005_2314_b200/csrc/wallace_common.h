@@ -113,6 +113,8 @@ struct FillArgs {
   uint64_t lg_pass0;
   int32_t lg_log2n;
   int32_t pad_lg;
+  double* lg_aux;         // per pool: consumer totals, defect mark, probe x, block partials
+  uint64_t lg_aux_stride; // doubles per pool
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]

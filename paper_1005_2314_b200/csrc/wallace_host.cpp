@@ -35,6 +35,7 @@ cudaError_t launch_pool_kernel(int dtype, int log2n, const FillArgs& a, uint64_t
 int pool_kernel_threads(int dtype, int log2n);
 void affine_multipliers(int log2n, uint32_t* alpha, uint32_t* beta);
 size_t large_state_bytes();
+uint64_t large_aux_stride(uint64_t N);
 cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
                         PoolState* st, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
@@ -223,6 +224,7 @@ struct wallace_handle {
   bool large = false;
   void* d_lg_pool2 = nullptr;
   void* d_lg_state = nullptr;
+  double* d_lg_aux = nullptr;
   // defect suite (wallace_cross_pool_probes / wallace_pool_defect_stats)
   double* d_probe_acc = nullptr;
   uint32_t n_probes = 0;  // active only inside wallace_cross_pool_probes
@@ -374,6 +376,8 @@ wb::FillArgs base_args(wallace_handle* h) {
     default_multipliers(h->N, al, be);
     a.lg_pool2 = h->d_lg_pool2;
     a.lg_state = h->d_lg_state;
+    a.lg_aux = h->d_lg_aux;
+    a.lg_aux_stride = wb::large_aux_stride(h->N);
     a.lg_stride = default_stride(rows) % rows;
     a.lg_alpha = al;
     a.lg_beta = be;
@@ -756,6 +760,7 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
   if (h->large) {
     WB_CUDA_C(cudaMalloc(&h->d_lg_pool2, n_pools * N * h->esize));
     WB_CUDA_C(cudaMalloc(&h->d_lg_state, n_pools * wb::large_state_bytes()));
+    WB_CUDA_C(cudaMalloc(&h->d_lg_aux, n_pools * wb::large_aux_stride(N) * sizeof(double)));
   }
   WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * h->plan_words * sizeof(uint32_t)));
   WB_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -821,6 +826,7 @@ wallace_status wallace_destroy(wallace_handle* h) {
   cudaFree(h->d_stage);
   cudaFree(h->d_lg_pool2);
   cudaFree(h->d_lg_state);
+  cudaFree(h->d_lg_aux);
   for (int k = 0; k < 2; ++k) {
     cudaFree(h->ws_dev[k]);
     cudaFreeHost(h->ws_host[k]);
@@ -1202,7 +1208,6 @@ wallace_status wallace_cross_pool_probes(wallace_handle* h, uint64_t passes, uin
                                          const uint64_t* out_i, const uint64_t* in_j, double* acc) {
   if (!h || !out_i || !in_j || !acc) return fail(WALLACE_ERR_INVALID_PARAM, "handle/probes/acc must not be NULL");
   if (n_probes < 1 || n_probes > 32) return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_probes: 1..32 probes");
-  if (h->large) return fail(WALLACE_ERR_UNSUPPORTED, "cross_pool_probes: on-chip pool sizes only");
   if (passes < 1) return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_probes: passes must be >= 1");
   for (uint32_t k = 0; k < n_probes; ++k)
     if (out_i[k] >= h->N || in_j[k] >= h->N)
@@ -1234,7 +1239,6 @@ wallace_status wallace_pool_defect_stats(wallace_handle* h, uint64_t emissions, 
                                          double* totals, uint8_t* marks) {
   if (!h || !totals || !marks) return fail(WALLACE_ERR_INVALID_PARAM, "handle/totals/marks must not be NULL");
   if (emissions < 1) return fail(WALLACE_ERR_INVALID_PARAM, "pool_defect_stats: emissions must be >= 1");
-  if (h->large) return fail(WALLACE_ERR_UNSUPPORTED, "pool_defect_stats: on-chip pool sizes only");
   if (!(h->cfg.out_mean == 0.0) || !(h->cfg.out_sigma == 1.0))
     return fail(WALLACE_ERR_INVALID_PARAM,
                 "pool_defect_stats: the handle's config must be standardized (out_mean 0, out_sigma 1)");
@@ -1430,7 +1434,6 @@ static wallace_status finish_consumer(cudaStream_t stream, const double* part_su
 static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sums[4],
                                    uint64_t hist[258], bool from_snapshot) {
   if (!h || !sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "handle/sums/hist must not be NULL");
-  if (h->large) return fail(WALLACE_ERR_UNSUPPORTED, "consume: fused consumers cover on-chip pool sizes only");
   if (from_snapshot && !h->has_snapshot) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (h->part_cap < h->n_pools) {

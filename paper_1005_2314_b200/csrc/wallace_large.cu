@@ -258,6 +258,132 @@ __global__ void lg_epilogue(const FillArgs a, uint64_t n_pools) {
   }
 }
 
+// ---- fused consumers (kModeConsume, kModeDefect) and probes on the large path
+// aux layout per pool (doubles): [0..3] consumer totals, [4] defect mark,
+// [8..39] probe x, [40...] per-block partials (4 per block).
+constexpr int kAuxTotals = 0, kAuxMark = 4, kAuxProbe = 8, kAuxPart = 40;
+constexpr int kLgVpt = 16;                     // values per thread in the consumer kernels
+constexpr int kLgBlockVals = kLgThreads * kLgVpt;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum_f64(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kLgThreads / 32; ++w) t = __dadd_rn(t, red[w]);
+  return t;
+}
+
+// values [i0, i0 + n) of pool `pool`: emitted (scale sc) from the pool or the
+// materialized leftover, fed to the consumer (moments + histogram) or the
+// defect statistics (sum of squares + rare-event mark); one block partial
+template <typename T, int MODE>
+__global__ void lg_consume(const FillArgs a, const T* src, uint64_t src_stride, uint64_t n, int use_cur_scale,
+                           int slot) {
+  __shared__ double red[kLgThreads / 32];
+  const uint64_t pool = blockIdx.y, blk = blockIdx.x;
+  const SState& s = static_cast<const SState*>(a.lg_state)[pool];
+  const T sc = from_double<T>(use_cur_scale ? s.cur_scale : s.scale[slot]);
+  const T mean = from_double<T>(a.mean);
+  const bool mz = a.mean_is_zero != 0, raw = use_cur_scale == 2;  // 2: leftover values are already emitted
+  double m[4] = {0.0, 0.0, 0.0, 0.0};
+  bool mark = false;
+  for (int k = 0; k < kLgVpt; ++k) {
+    const uint64_t i = blk * kLgBlockVals + uint64_t(k) * kLgThreads + threadIdx.x;
+    if (i >= n) break;
+    const T x = src[pool * src_stride + i];
+    const T y = raw ? x : emit_value(x, sc, mean, mz);
+    const double v = static_cast<double>(y);
+    if (MODE == kModeConsume) {
+      const double v2 = __dmul_rn(v, v);
+      m[0] = __dadd_rn(m[0], v);
+      m[1] = __dadd_rn(m[1], v2);
+      m[2] = __dadd_rn(m[2], __dmul_rn(v2, v));
+      m[3] = __dadd_rn(m[3], __dmul_rn(v2, v2));
+      const T t = fma_rn(y, T(16), T(128));  // floor((y + 8) * 16), as the on-chip consumer
+      int bin = sizeof(T) == 4 ? __float2int_rd(static_cast<float>(t)) : __double2int_rd(static_cast<double>(t));
+      bin = max(-1, min(bin, 256));
+      atomicAdd(&a.part_hist[pool * 258 + bin + 1], 1u);
+    } else {
+      m[0] = __dadd_rn(m[0], __dmul_rn(v, v));
+      mark |= fabs(v) > a.def_threshold;
+    }
+  }
+  double* part = a.lg_aux + pool * a.lg_aux_stride + kAuxPart + blk * 4;
+  for (int q = 0; q < (MODE == kModeConsume ? 4 : 1); ++q) {
+    const double t = block_sum(m[q], red);
+    if (threadIdx.x == 0) part[q] = t;
+  }
+  if (MODE == kModeDefect && __syncthreads_or(mark) && threadIdx.x == 0)
+    a.lg_aux[pool * a.lg_aux_stride + kAuxMark] = 1.0;
+}
+
+// fold the block partials of one emission (or of the lead) in block order
+template <int MODE>
+__global__ void lg_fold(const FillArgs a, uint64_t nblk, uint64_t e, uint64_t n_pools) {
+  const uint64_t pool = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pool >= n_pools) return;
+  double* aux = a.lg_aux + pool * a.lg_aux_stride;
+  if (MODE == kModeConsume) {
+    for (int q = 0; q < 4; ++q) {
+      double t = aux[kAuxTotals + q];
+      for (uint64_t b = 0; b < nblk; ++b) t = __dadd_rn(t, aux[kAuxPart + b * 4 + q]);
+      aux[kAuxTotals + q] = t;
+    }
+  } else {
+    // pool_sum_squares_test's total: reserved^2 (chain_close ran) + sum v^2
+    const SState& s = static_cast<const SState*>(a.lg_state)[pool];
+    double t = __dmul_rn(s.reserved_prev, s.reserved_prev);
+    for (uint64_t b = 0; b < nblk; ++b) t = __dadd_rn(t, aux[kAuxPart + b * 4]);
+    a.def_totals[pool * a.def_stride + a.def_e0 + e] = t;
+    a.def_marks[pool * a.def_stride + a.def_e0 + e] = aux[kAuxMark] != 0.0 ? 1 : 0;
+    aux[kAuxMark] = 0.0;
+  }
+}
+
+__global__ void lg_consume_begin(const FillArgs a, uint64_t n_pools) {
+  const uint64_t pool = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pool >= n_pools) return;
+  double* aux = a.lg_aux + pool * a.lg_aux_stride;
+  for (int q = 0; q < 5; ++q) aux[q] = 0.0;
+  if (a.mode == kModeConsume)
+    for (int i = 0; i < 258; ++i) a.part_hist[pool * 258 + i] = 0;
+}
+__global__ void lg_consume_end(const FillArgs a, uint64_t n_pools) {
+  const uint64_t pool = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pool >= n_pools) return;
+  for (int q = 0; q < 4; ++q) a.part_sums[pool * 4 + q] = a.lg_aux[pool * a.lg_aux_stride + kAuxTotals + q];
+}
+
+// cross-pool probes (stats.cpp:310-338): x before the pass, y after it (and
+// after a renormalisation), ProbeAccumulator sums in pass order
+template <typename T>
+__global__ void lg_probe_x(const FillArgs a, const T* pool_buf, uint64_t N, uint64_t n_pools) {
+  const uint64_t pool = blockIdx.x;
+  const uint32_t k = threadIdx.x;
+  if (pool >= n_pools || k >= a.n_probes) return;
+  a.lg_aux[pool * a.lg_aux_stride + kAuxProbe + k] = static_cast<double>(pool_buf[pool * N + a.probe_in[k]]);
+}
+template <typename T>
+__global__ void lg_probe_y(const FillArgs a, const T* pool_buf, uint64_t N, uint64_t n_pools) {
+  const uint64_t pool = blockIdx.x;
+  const uint32_t k = threadIdx.x;
+  if (pool >= n_pools || k >= a.n_probes) return;
+  const double x = a.lg_aux[pool * a.lg_aux_stride + kAuxProbe + k];
+  const double y = static_cast<double>(pool_buf[pool * N + a.probe_out[k]]);
+  double* pa = a.probe_acc + (pool * a.n_probes + k) * 6;
+  pa[0] = __dadd_rn(pa[0], x);
+  pa[1] = __dadd_rn(pa[1], __dmul_rn(x, x));
+  pa[2] = __dadd_rn(pa[2], y);
+  pa[3] = __dadd_rn(pa[3], __dmul_rn(y, y));
+  const double w = __dmul_rn(x, y);
+  pa[4] = __dadd_rn(pa[4], w);
+  pa[5] = __dadd_rn(pa[5], __dmul_rn(w, w));
+}
+
 template <typename T>
 cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
   const uint64_t N = uint64_t(1) << a.lg_log2n;
@@ -272,7 +398,25 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
   if (a.pools_in != a.pools_out)
     cudaMemcpyAsync(w[0], a.pools_in, n_pools * N * sizeof(T), cudaMemcpyDeviceToDevice, st);
   lg_prologue<T><<<pool_blocks, 128, 0, st>>>(a, n_pools);
-  if (a.mode != kModePasses && a.lead > 0) {
+  const bool cons = a.mode == kModeConsume || a.mode == kModeDefect;
+  if (cons) lg_consume_begin<<<pool_blocks, 128, 0, st>>>(a, n_pools);
+  if (a.mode == kModeConsume && a.lead > 0) {
+    // the lead: from the materialized leftover (already emitted values) or the
+    // pool with the current emission's scale; pools agree on both (uniform cursor)
+    cudaError_t e0 = cudaSuccess;
+    PoolState st0{};
+    e0 = cudaMemcpyAsync(&st0, a.st_in, sizeof(st0), cudaMemcpyDeviceToHost, st);
+    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize(st);
+    if (e0 != cudaSuccess) return e0;
+    const uint64_t nb = (a.lead + kLgBlockVals - 1) / kLgBlockVals;
+    const dim3 g{unsigned(nb), unsigned(n_pools)};
+    if (st0.flags & kFlagLeftover)
+      lg_consume<T, kModeConsume><<<g, kLgThreads, 0, st>>>(
+          a, static_cast<const T*>(a.leftover) + st0.cursor, N - 1, a.lead, 2, 0);
+    else
+      lg_consume<T, kModeConsume><<<g, kLgThreads, 0, st>>>(a, w[0] + st0.cursor, N, a.lead, 1, 0);
+    lg_fold<kModeConsume><<<pool_blocks, 128, 0, st>>>(a, nb, 0, n_pools);
+  } else if (a.mode != kModePasses && a.lead > 0 && !cons) {
     const dim3 g(unsigned((a.lead + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
     lg_lead<T><<<g, kLgThreads, 0, st>>>(a, w[0], N);
   }
@@ -299,8 +443,10 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
   uint32_t p = 0;
   if (a.mode == kModePasses) {
     for (; p < a.n_passes; ++p) {
+      if (a.n_probes) lg_probe_x<T><<<unsigned(n_pools), 32, 0, st>>>(a, w[cur], N, n_pools);
       pass(p);
       if (pc == 0) renorm(0, 0);
+      if (a.n_probes) lg_probe_y<T><<<unsigned(n_pools), 32, 0, st>>>(a, w[cur], N, n_pools);
       pc = (pc + 1) & 255u;
     }
   } else {
@@ -310,30 +456,42 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
       for (uint32_t q = 1; q <= a.d; ++q, ++p) {
         const bool emit = q == a.d;
-        const bool fuse = emit && pc != 0;  // no renormalisation between the pass and its emission
+        // the emission fused into the pass when no renormalisation intervenes
+        const bool fuse = emit && pc != 0 && !cons;
         if (fuse) pass(p, slot, gofs, limit);
         else pass(p);
         if (pc == 0) renorm(slot, 1);
         if (emit) {
-          if (!fuse) {
+          const uint64_t nb = (limit + kLgBlockVals - 1) / kLgBlockVals;
+          const dim3 gc{unsigned(nb), unsigned(n_pools)};
+          if (a.mode == kModeConsume) {
+            lg_consume<T, kModeConsume><<<gc, kLgThreads, 0, st>>>(a, w[cur], N, limit, 0, slot);
+            lg_fold<kModeConsume><<<pool_blocks, 128, 0, st>>>(a, nb, e, n_pools);
+          } else if (a.mode == kModeDefect) {
+            lg_consume<T, kModeDefect><<<gc, kLgThreads, 0, st>>>(a, w[cur], N, limit, 0, slot);
+          } else if (!fuse) {
             const dim3 g(unsigned((limit + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
             lg_emit<T><<<g, kLgThreads, 0, st>>>(a, w[cur], N, gofs, limit, slot);
           }
           lg_chain<T><<<pool_blocks, 128, 0, st>>>(a, w[cur], N, slot, e + 1 < a.n_emit ? 1 : 0, n_pools);
+          if (a.mode == kModeDefect) lg_fold<kModeDefect><<<pool_blocks, 128, 0, st>>>(a, nb, e, n_pools);
         }
         pc = (pc + 1) & 255u;
       }
     }
   }
   if (cur != 0) cudaMemcpyAsync(w[0], w[1], n_pools * N * sizeof(T), cudaMemcpyDeviceToDevice, st);
+  if (a.mode == kModeConsume) lg_consume_end<<<pool_blocks, 128, 0, st>>>(a, n_pools);
   lg_epilogue<T><<<pool_blocks, 128, 0, st>>>(a, n_pools);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+// doubles of aux scratch per pool for pool size N
+uint64_t large_aux_stride(uint64_t N) { return kAuxPart + 4 * ((N + kLgBlockVals - 1) / kLgBlockVals); }
+
 cudaError_t launch_pool_large(int dtype, const FillArgs& a, uint64_t n_pools, cudaStream_t s) {
-  if (a.mode != kModeFill && a.mode != kModePasses) return cudaErrorNotSupported;
   return dtype == 0 ? run_large<float>(a, n_pools, s) : run_large<double>(a, n_pools, s);
 }
 
