@@ -261,6 +261,24 @@ typedef struct wallace_pass_plan {
 } wallace_pass_plan;
 wallace_status wallace_decode_pass_plan_ex(const wallace_config* cfg, uint64_t transform_word,
                                            uint64_t offset_word, wallace_pass_plan* out);
+/* maxent::run_pass (generator.cpp:259-271): one pass of the configured family
+ * and mixing with an explicit plan over one fp64 pool (host buffers of
+ * pool_size doubles, run on the device). */
+wallace_status wallace_run_pass(const wallace_config* cfg, const wallace_pass_plan* plan, const double* in,
+                                double* out);
+/* maxent::pass_coefficient (generator.cpp:273-284): entry (out_i, in_j) of
+ * the composed pass matrix, from the permutation and block structure. */
+wallace_status wallace_pass_coefficient(const wallace_config* cfg, const wallace_pass_plan* plan, uint64_t out_i,
+                                        uint64_t in_j, double* out);
+/* maxent::default_multipliers (generator.cpp:286-294). */
+void wallace_default_multipliers(uint64_t n, uint64_t* alpha, uint64_t* beta);
+/* cross_pool_correlation's fixed-transform mode (stats.cpp:284-299): `pairs`
+ * fresh Polar pools from BaselineState(cfg->seed), one pinned pass
+ * (PassPlan{}) each on the device; ProbeAccumulator sums in pair order,
+ * acc[k * 6 + {0..5}] = {sx, sxx, sy, syy, sxy, sxy2}. */
+wallace_status wallace_cross_pool_fixed(const wallace_config* cfg, uint64_t pairs, uint32_t n_probes,
+                                        const uint64_t* out_i, const uint64_t* in_j, double* acc);
+
 /* rotation_t_table() and rotation_from_t (transforms.cpp:39-70): t, c = cos,
  * s = sin of the 16 table entries (any pointer may be NULL). */
 void wallace_rotation_table(double t[16], double c[16], double s[16]);

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -108,6 +109,62 @@ struct NormalPool {
   std::uint64_t pass_count = 0;
   double sum_sq = 0.0;
 };
+
+// maxent::PassPlan (generator.hpp:50-55)
+struct PassPlan {
+  int wallace_variant = 0;
+  std::array<int, 2> t_index{0, 0};
+  std::array<bool, 2> negate{false, false};
+  std::array<std::uint64_t, 2> offset{0, 0};
+  wallace_pass_plan to_c() const {
+    wallace_pass_plan p{};
+    p.wallace_variant = wallace_variant;
+    for (int s = 0; s < 2; ++s) {
+      p.t_index[s] = t_index[static_cast<std::size_t>(s)];
+      p.negate[s] = negate[static_cast<std::size_t>(s)] ? 1 : 0;
+      p.offset[s] = offset[static_cast<std::size_t>(s)];
+    }
+    return p;
+  }
+};
+
+// maxent::decode_pass_plan / run_pass / pass_coefficient / default_multipliers
+// (generator.hpp:56-77); run_pass executes on the device.
+inline PassPlan decode_pass_plan(const GeneratorConfig& cfg, std::uint64_t transform_word,
+                                 std::uint64_t offset_word) {
+  const wallace_config c = cfg.to_c();
+  wallace_pass_plan p{};
+  check(wallace_decode_pass_plan_ex(&c, transform_word, offset_word, &p));
+  PassPlan out;
+  out.wallace_variant = p.wallace_variant;
+  for (int s = 0; s < 2; ++s) {
+    out.t_index[static_cast<std::size_t>(s)] = p.t_index[s];
+    out.negate[static_cast<std::size_t>(s)] = p.negate[s] != 0;
+    out.offset[static_cast<std::size_t>(s)] = p.offset[s];
+  }
+  return out;
+}
+inline void run_pass(const GeneratorConfig& cfg, const PassPlan& plan, std::span<const double> in,
+                     std::span<double> out) {
+  if (in.size() != cfg.pool_size || out.size() != cfg.pool_size)
+    throw InvalidParameterError("run_pass: buffers must match pool_size");
+  const wallace_config c = cfg.to_c();
+  const wallace_pass_plan p = plan.to_c();
+  check(wallace_run_pass(&c, &p, in.data(), out.data()));
+}
+inline double pass_coefficient(const GeneratorConfig& cfg, const PassPlan& plan, std::size_t out_i,
+                               std::size_t in_j) {
+  const wallace_config c = cfg.to_c();
+  const wallace_pass_plan p = plan.to_c();
+  double v = 0.0;
+  check(wallace_pass_coefficient(&c, &p, out_i, in_j, &v));
+  return v;
+}
+inline std::pair<std::uint64_t, std::uint64_t> default_multipliers(std::size_t n) {
+  std::uint64_t a = 0, b = 0;
+  wallace_default_multipliers(n, &a, &b);
+  return {a, b};
+}
 
 // maxent::ProbePair (stats.hpp:78-81)
 struct ProbePair {
@@ -347,6 +404,8 @@ inline MomentSummary moments(std::span<const double> samples) {
 struct CrossPoolOptions {
   std::size_t pool_pairs = 100000;  // >= 1e3
   std::vector<ProbePair> probes;    // empty -> default spread of 8 probes
+  bool fixed_transform = false;     // fresh Polar pool per pair, one pinned pass
+  bool expect_composed_q = false;   // report against q_{i,j} instead of 0
 };
 
 // stats.cpp:310-338 on a streaming generator: the probe sums are accumulated
@@ -377,6 +436,55 @@ inline std::vector<TestReport> cross_pool_correlation(Generator& gen, const Cros
     const double var_xy = a[5] / nn - mean_xy * mean_xy;
     const double se = std::sqrt(var_xy / nn) / denom;
     reports.push_back(TestReport::make(name, cov / denom, 0.0, se));
+  }
+  return reports;
+}
+
+// stats.cpp:260-307 cross_pool_correlation(cfg, opts): the streaming
+// generator, or with fixed_transform fresh Polar pools pushed through one
+// pinned pass each (device batch), reported against 0 or q_{i,j}.
+inline std::vector<TestReport> cross_pool_correlation(const GeneratorConfig& cfg, const CrossPoolOptions& opts) {
+  cfg.validate();
+  if (opts.pool_pairs < 1000) throw InvalidParameterError("cross_pool_correlation: pool_pairs must be >= 1000");
+  if (!opts.fixed_transform) {
+    GeneratorConfig streaming = cfg;
+    streaming.diag.fixed_transform = false;
+    Generator gen(streaming);
+    return cross_pool_correlation(gen, opts);
+  }
+  const std::size_t n = cfg.pool_size;
+  std::vector<ProbePair> probes = opts.probes;
+  if (probes.empty())
+    for (std::size_t k = 0; k < 8; ++k) probes.push_back({(5 * k) % n, (11 * k + 3) % n});
+  std::vector<std::uint64_t> oi, ij;
+  for (const auto& p : probes) {
+    if (p.out_i >= n || p.in_j >= n) throw InvalidParameterError("cross_pool_correlation: probe index out of range");
+    oi.push_back(p.out_i);
+    ij.push_back(p.in_j);
+  }
+  const wallace_config c = cfg.to_c();
+  std::vector<double> acc(probes.size() * 6);
+  check(wallace_cross_pool_fixed(&c, opts.pool_pairs, static_cast<std::uint32_t>(probes.size()), oi.data(),
+                                 ij.data(), acc.data()));
+  std::vector<TestReport> reports;
+  const double nn = static_cast<double>(opts.pool_pairs);
+  const PassPlan plan{};
+  for (std::size_t k = 0; k < probes.size(); ++k) {
+    const double* a = acc.data() + k * 6;
+    const std::string name =
+        "cross_pool_corr.i" + std::to_string(probes[k].out_i) + ".j" + std::to_string(probes[k].in_j);
+    const double mx = a[0] / nn, my = a[2] / nn;
+    const double vx = a[1] / nn - mx * mx, vy = a[3] / nn - my * my;
+    if (!(vx > 0.0) || !(vy > 0.0))
+      throw InvalidParameterError("cross_pool_correlation: zero-variance pool values at probe " + name);
+    const double denom = std::sqrt(vx * vy);
+    const double cov = a[4] / nn - mx * my;
+    const double mean_xy = a[4] / nn;
+    const double var_xy = a[5] / nn - mean_xy * mean_xy;
+    const double se = std::sqrt(var_xy / nn) / denom;
+    const double expected =
+        opts.expect_composed_q ? pass_coefficient(cfg, plan, probes[k].out_i, probes[k].in_j) : 0.0;
+    reports.push_back(TestReport::make(name, cov / denom, expected, se));
   }
   return reports;
 }

@@ -142,6 +142,13 @@ def ref_lib():
         L.ref_pool_sum_squares.restype = C.c_int
         L.ref_rare_event_adjacency.argtypes = [u64, C.c_int, u64, u64, C.c_int, u64, f64, P(f64)]
         L.ref_rare_event_adjacency.restype = C.c_int
+        L.ref_run_pass.argtypes = [u64, C.c_int, C.c_int, P(C.c_int32), P(u64), P(f64), P(f64)]
+        L.ref_run_pass.restype = C.c_int
+        L.ref_pass_coefficient.argtypes = [u64, C.c_int, C.c_int, P(C.c_int32), P(u64), u64, u64]
+        L.ref_pass_coefficient.restype = f64
+        L.ref_cross_pool_fixed.argtypes = [u64, C.c_int, C.c_int, u64, u64, C.c_uint32, P(u64), P(u64), C.c_int,
+                                           P(f64)]
+        L.ref_cross_pool_fixed.restype = C.c_int
         L.ref_last_error.restype = C.c_char_p
         L.ref_destroy.argtypes = [vp]
         L.ref_fill.argtypes = [vp, P(f64), u64]

@@ -256,6 +256,54 @@ int ref_rare_event_adjacency(uint64_t pool_size, int chi2_method, uint64_t disca
   }
 }
 
+// run_pass / pass_coefficient with an explicit plan {variant, t0, t1, neg0, neg1}, {off0, off1}
+static maxent::PassPlan plan_of(const int32_t* ints, const uint64_t* offs) {
+  maxent::PassPlan p;
+  p.wallace_variant = ints[0];
+  p.t_index = {ints[1], ints[2]};
+  p.negate = {ints[3] != 0, ints[4] != 0};
+  p.offset = {offs[0], offs[1]};
+  return p;
+}
+int ref_run_pass(uint64_t n, int family, int mixing, const int32_t* ints, const uint64_t* offs, const double* in,
+                 double* out) {
+  try {
+    maxent::run_pass(to_cfg(n, 2, 1, 0.0, 1.0, 0, 0, 0, family, mixing), plan_of(ints, offs),
+                     std::span<const double>(in, n), std::span<double>(out, n));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+double ref_pass_coefficient(uint64_t n, int family, int mixing, const int32_t* ints, const uint64_t* offs,
+                            uint64_t i, uint64_t j) {
+  return maxent::pass_coefficient(to_cfg(n, 2, 1, 0.0, 1.0, 0, 0, 0, family, mixing), plan_of(ints, offs), i, j);
+}
+// cross_pool_correlation(cfg, opts) with fixed_transform (and expect_composed_q)
+int ref_cross_pool_fixed(uint64_t n, int family, int mixing, uint64_t seed, uint64_t pairs, uint32_t n_probes,
+                         const uint64_t* out_i, const uint64_t* in_j, int expect_q, double* out) {
+  try {
+    maxent::CrossPoolOptions o;
+    o.pool_pairs = pairs;
+    o.fixed_transform = true;
+    o.expect_composed_q = expect_q != 0;
+    for (uint32_t k = 0; k < n_probes; ++k) o.probes.push_back({out_i[k], in_j[k]});
+    const auto reps =
+        maxent::cross_pool_correlation(to_cfg(n, 2, 1, 0.0, 1.0, seed, 0, 0, family, mixing), o);
+    for (size_t k = 0; k < reps.size(); ++k) {
+      out[k * 4 + 0] = reps[k].statistic;
+      out[k * 4 + 1] = reps[k].expected;
+      out[k * 4 + 2] = reps[k].std_error;
+      out[k * 4 + 3] = reps[k].z_score;
+    }
+    return static_cast<int>(reps.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 void ref_polar(uint64_t seed, uint64_t n, double* out) {
   maxent::BaselineState s(seed);
   for (uint64_t i = 0; i < n; ++i) out[i] = maxent::polar_next(s);

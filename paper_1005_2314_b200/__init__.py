@@ -315,6 +315,50 @@ class PoolBatch:
                                                 marks.ctypes.data_as(C.POINTER(C.c_uint8))))
         return totals, marks.astype(bool)
 
+def pass_plan(wallace_variant: int = 0, t_index=(0, 0), negate=(0, 0), offset=(0, 0)):
+    """maxent::PassPlan (generator.hpp:50-55); the default is PassPlan{}."""
+    p = _capi.wallace_pass_plan()
+    p.wallace_variant = int(wallace_variant)
+    p.t_index[0], p.t_index[1] = (int(t) for t in t_index)
+    p.negate[0], p.negate[1] = (int(bool(g)) for g in negate)
+    p.offset[0], p.offset[1] = (int(o) for o in offset)
+    return p
+
+
+def run_pass(cfg: GeneratorConfig, plan, values) -> np.ndarray:
+    """maxent::run_pass (generator.cpp:259-271): one pass with an explicit
+    plan over one fp64 pool, on the device."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if v.size != cfg.pool_size:
+        raise InvalidParameterError("run_pass: buffers must match pool_size")
+    out = np.empty_like(v)
+    dp = C.POINTER(C.c_double)
+    _check(_capi.load().wallace_run_pass(C.byref(cfg.to_c()), C.byref(plan), v.ctypes.data_as(dp),
+                                         out.ctypes.data_as(dp)))
+    return out
+
+
+def pass_coefficient(cfg: GeneratorConfig, plan, out_i: int, in_j: int) -> float:
+    """maxent::pass_coefficient (generator.cpp:273-284)."""
+    r = C.c_double()
+    _check(_capi.load().wallace_pass_coefficient(C.byref(cfg.to_c()), C.byref(plan), int(out_i), int(in_j),
+                                                 C.byref(r)))
+    return r.value
+
+
+def cross_pool_fixed_sums(cfg: GeneratorConfig, pairs: int, probes) -> np.ndarray:
+    """cross_pool_correlation's fixed-transform mode (stats.cpp:284-299):
+    ProbeAccumulator sums [n_probes, 6] over `pairs` fresh Polar pools, one
+    pinned pass each (on the device)."""
+    k = len(probes)
+    oi = (C.c_uint64 * k)(*[int(p[0]) for p in probes])
+    ij = (C.c_uint64 * k)(*[int(p[1]) for p in probes])
+    acc = np.zeros((k, 6), dtype=np.float64)
+    _check(_capi.load().wallace_cross_pool_fixed(C.byref(cfg.to_c()), int(pairs), k, oi, ij,
+                                                 acc.ctypes.data_as(C.POINTER(C.c_double))))
+    return acc
+
+
 def boxmuller_consume(n_streams: int, count: int, seed_base: int = 1, seeds=None, stream=None):
     """Box-Muller comparator on UniformState(seed) streams (baselines.cpp:80-92)."""
     L = _capi.load()

@@ -101,6 +101,10 @@ SYMBOLS = [
     ("wallace_rotation_table", None, [P(C.c_double), P(C.c_double), P(C.c_double)]),
     ("wallace_cross_pool_probes", i32, [vp, u64, C.c_uint32, P(u64), P(u64), P(C.c_double)]),
     ("wallace_write_stream", i32, [vp, u64, i32, i32]),
+    ("wallace_run_pass", i32, [P(wallace_config), P(wallace_pass_plan), P(C.c_double), P(C.c_double)]),
+    ("wallace_pass_coefficient", i32, [P(wallace_config), P(wallace_pass_plan), u64, u64, P(C.c_double)]),
+    ("wallace_default_multipliers", None, [u64, P(u64), P(u64)]),
+    ("wallace_cross_pool_fixed", i32, [P(wallace_config), u64, C.c_uint32, P(u64), P(u64), P(C.c_double)]),
     ("wallace_create_ex", i32, [P(wallace_config), u64, P(u64), i32, vp, C.c_uint32, P(vp)]),
     ("wallace_pool_defect_stats", i32, [vp, u64, C.c_double, P(C.c_double), P(C.c_uint8)]),
 ]

@@ -115,6 +115,7 @@ struct FillArgs {
   int32_t pad_lg;
   double* lg_aux;         // per pool: consumer totals, defect mark, probe x, block partials
   uint64_t lg_aux_stride; // doubles per pool
+  uint64_t lg_npools;     // pools of the launch (pool index = blockIdx.y + 65535 * blockIdx.z)
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]

@@ -36,6 +36,8 @@ int pool_kernel_threads(int dtype, int log2n);
 void affine_multipliers(int log2n, uint32_t* alpha, uint32_t* beta);
 size_t large_state_bytes();
 uint64_t large_aux_stride(uint64_t N);
+cudaError_t launch_single_pass(int dtype, const FillArgs& a, void* buf_a, void* buf_b, uint64_t n_pools,
+                               cudaStream_t st, int* in_b);
 cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
                         PoolState* st, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
@@ -1202,6 +1204,224 @@ wallace_status wallace_step_pass(wallace_handle* h, uint64_t n_passes) {
   wallace_status st = materialize(h);
   if (st) return st;
   return run_passes(h, n_passes);
+}
+
+// ---- pass structure: pass_coefficient, run_pass (generator.cpp) -------------
+namespace {
+
+// transforms.cpp:24-35: element k of the p-th permutation of {0,1,2,3} in
+// lexicographic order
+int perm_elem(int p, int k) {
+  int avail[4] = {0, 1, 2, 3}, n = 4;
+  const int fact[4] = {6, 2, 1, 1};
+  int out = 0;
+  for (int pos = 0; pos <= k; ++pos) {
+    const int q = p / fact[pos];
+    p %= fact[pos];
+    out = avail[q];
+    for (int j = q; j + 1 < n; ++j) avail[j] = avail[j + 1];
+    --n;
+  }
+  return out;
+}
+
+// generator.cpp:36-50 mix_index
+uint64_t mix_index(const wallace_config& c, int sweep, uint64_t offset, uint64_t j) {
+  const uint64_t n = c.pool_size;
+  if (c.mixing == 0) {
+    const uint64_t rows = n / 4;
+    return (j % 4) * rows + (default_stride(rows) * (j / 4) + offset) % rows;
+  }
+  uint64_t al = 0, be = 0;
+  default_multipliers(n, al, be);
+  const uint64_t mult = sweep == 0 ? al : be;
+  return (mult % n * j + offset) % n;
+}
+
+// generator.cpp:174-217 sweep_row: the two nonzero entries of a half-sweep row
+void sweep_row(const wallace_config& c, const wallace_pass_plan& plan, int sweep, uint64_t w, uint64_t col[2],
+               double coef[2]) {
+  const uint64_t n = c.pool_size;
+  double rc = 0.0, rs = 0.0;
+  rotation_from_t(rotation_t(plan.t_index[sweep]), rc, rs);
+  const double g = plan.negate[sweep] ? -1.0 : 1.0;
+  const double ce = g * rc, se = g * rs;
+  const uint64_t off = plan.offset[sweep];
+  uint64_t p1, p2;
+  bool is_first;
+  if (sweep == 0) {
+    p1 = w & ~uint64_t{1};
+    p2 = p1 + 1;
+    is_first = w == p1;
+  } else if (w == 0) {
+    p1 = n - 1;
+    p2 = 0;
+    is_first = false;
+  } else if (w % 2 == 1) {
+    p1 = w;
+    p2 = (w + 1) % n;
+    is_first = true;
+  } else {
+    p1 = w - 1;
+    p2 = w;
+    is_first = false;
+  }
+  col[0] = mix_index(c, sweep, off, p1);
+  col[1] = mix_index(c, sweep, off, p2);
+  coef[0] = is_first ? ce : -se;
+  coef[1] = is_first ? se : ce;
+}
+
+// plan words of the HBM-resident pass kernels (wallace_large.cu)
+std::vector<uint32_t> large_plan_words(const wallace_config& c, const wallace_pass_plan& plan) {
+  if (c.transform_family == 0)
+    return {static_cast<uint32_t>(plan.offset[0]), static_cast<uint32_t>(plan.wallace_variant)};
+  return {static_cast<uint32_t>(plan.offset[0]), static_cast<uint32_t>(plan.offset[1]),
+          static_cast<uint32_t>((plan.t_index[0] & 15) | (plan.negate[0] & 1) << 4 | (plan.t_index[1] & 15) << 8 |
+                                (plan.negate[1] & 1) << 12)};
+}
+
+wb::FillArgs single_pass_args(const wallace_config& c, const uint32_t* d_plans) {
+  wb::FillArgs a{};
+  const uint64_t n = c.pool_size, rows = n / 4;
+  uint64_t al = 0, be = 0;
+  default_multipliers(n, al, be);
+  a.plans = d_plans;
+  a.plan_stride = 0;  // one plan for every pool of the batch
+  a.pass_type = 2 * c.transform_family + c.mixing;
+  rotation_table(a.rot_c, a.rot_s);
+  a.lg_stride = default_stride(rows) % rows;
+  a.lg_alpha = al;
+  a.lg_beta = be;
+  a.lg_log2n = ilog2(n);
+  return a;
+}
+
+}  // namespace
+
+void wallace_default_multipliers(uint64_t n, uint64_t* alpha, uint64_t* beta) {
+  uint64_t a = 0, b = 0;
+  default_multipliers(n, a, b);
+  if (alpha) *alpha = a;
+  if (beta) *beta = b;
+}
+
+wallace_status wallace_pass_coefficient(const wallace_config* cfg, const wallace_pass_plan* plan, uint64_t out_i,
+                                        uint64_t in_j, double* out) {
+  wallace_status st = validate(cfg);
+  if (st) return st;
+  if (!plan || !out) return fail(WALLACE_ERR_INVALID_PARAM, "plan/out must not be NULL");
+  const uint64_t n = cfg->pool_size;
+  if (out_i >= n || in_j >= n) return fail(WALLACE_ERR_INVALID_PARAM, "pass_coefficient: index out of range");
+  if (cfg->transform_family == 0) {
+    // generator.cpp:273-284: entries[k][col] = row_sign[k] * 0.5 * A1[src[k]][col]
+    // (A1's signs are the butterfly's: z0 = v0+v1-v2+v3, z1 = v0-v1+v2+v3,
+    // z2 = v0-v1-v2-v3, z3 = -v0-v1-v2+v3)
+    static const int a1[4][4] = {{1, 1, -1, 1}, {1, -1, 1, 1}, {1, -1, -1, -1}, {-1, -1, -1, 1}};
+    const int variant = plan->wallace_variant;
+    const uint64_t b = out_i / 4;
+    const int k = static_cast<int>(out_i % 4);
+    const double row_sign = ((variant & 15) >> k) & 1 ? -1.0 : 1.0;
+    const int src = perm_elem(variant >> 4, k);
+    *out = 0.0;
+    for (int col = 0; col < 4; ++col)
+      if (mix_index(*cfg, 0, plan->offset[0], 4 * b + col) == in_j) {
+        *out = row_sign * 0.5 * a1[src][col];
+        break;
+      }
+    return WALLACE_OK;
+  }
+  double total = 0.0;
+  uint64_t mid[2], col[2];
+  double c2[2], c1[2];
+  sweep_row(*cfg, *plan, 1, out_i, mid, c2);
+  for (int u = 0; u < 2; ++u) {
+    sweep_row(*cfg, *plan, 0, mid[u], col, c1);
+    for (int v = 0; v < 2; ++v)
+      if (col[v] == in_j) total += c2[u] * c1[v];
+  }
+  *out = total;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_run_pass(const wallace_config* cfg, const wallace_pass_plan* plan, const double* in,
+                                double* out) {
+  wallace_status st = validate(cfg);
+  if (st) return st;
+  if (!plan || !in || !out) return fail(WALLACE_ERR_INVALID_PARAM, "run_pass: buffers must match pool_size");
+  const uint64_t n = cfg->pool_size;
+  const std::vector<uint32_t> words = large_plan_words(*cfg, *plan);
+  double *A = nullptr, *B = nullptr;
+  uint32_t* P = nullptr;
+  cudaError_t e = cudaMalloc(&A, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&B, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&P, words.size() * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(P, words.data(), words.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(A, in, n * 8, cudaMemcpyHostToDevice);
+  int in_b = 0;
+  if (e == cudaSuccess) e = wb::launch_single_pass(1, single_pass_args(*cfg, P), A, B, 1, nullptr, &in_b);
+  ++g_launches;
+  if (e == cudaSuccess) e = cudaMemcpy(out, in_b ? B : A, n * 8, cudaMemcpyDeviceToHost);
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(P);
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "run_pass: %s", cudaGetErrorString(e));
+  return WALLACE_OK;
+}
+
+wallace_status wallace_cross_pool_fixed(const wallace_config* cfg, uint64_t pairs, uint32_t n_probes,
+                                        const uint64_t* out_i, const uint64_t* in_j, double* acc) {
+  wallace_status st = validate(cfg);
+  if (st) return st;
+  if (!out_i || !in_j || !acc || n_probes < 1)
+    return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_fixed: probes/acc must not be NULL");
+  const uint64_t n = cfg->pool_size;
+  for (uint32_t k = 0; k < n_probes; ++k)
+    if (out_i[k] >= n || in_j[k] >= n)
+      return fail(WALLACE_ERR_INVALID_PARAM, "cross_pool_correlation: probe index out of range");
+  // stats.cpp:284-299: fresh Polar pools from one BaselineState(seed), one
+  // pinned pass (PassPlan{}) each; the passes run on the device in batches,
+  // the ProbeAccumulator sums are formed in pair order
+  const wallace_pass_plan plan{};
+  const std::vector<uint32_t> words = large_plan_words(*cfg, plan);
+  const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(pairs, (uint64_t(1) << 24) / n));
+  std::vector<double> x(batch * n), y(batch * n);
+  double *A = nullptr, *B = nullptr;
+  uint32_t* P = nullptr;
+  cudaError_t e = cudaMalloc(&A, batch * n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&B, batch * n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&P, words.size() * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(P, words.data(), words.size() * 4, cudaMemcpyHostToDevice);
+  for (uint32_t k = 0; k < n_probes; ++k)
+    for (int q = 0; q < 6; ++q) acc[k * 6 + q] = 0.0;
+  Polar src(cfg->seed);
+  const wb::FillArgs a = single_pass_args(*cfg, P);
+  for (uint64_t p0 = 0; p0 < pairs && e == cudaSuccess; p0 += batch) {
+    const uint64_t m = std::min(batch, pairs - p0);
+    for (uint64_t i = 0; i < m * n; ++i) x[i] = src.next();
+    e = cudaMemcpy(A, x.data(), m * n * 8, cudaMemcpyHostToDevice);
+    int in_b = 0;
+    if (e == cudaSuccess) e = wb::launch_single_pass(1, a, A, B, m, nullptr, &in_b);
+    ++g_launches;
+    if (e == cudaSuccess) e = cudaMemcpy(y.data(), in_b ? B : A, m * n * 8, cudaMemcpyDeviceToHost);
+    for (uint64_t q = 0; q < m && e == cudaSuccess; ++q)
+      for (uint32_t k = 0; k < n_probes; ++k) {
+        const double xv = x[q * n + in_j[k]], yv = y[q * n + out_i[k]];
+        double* r = acc + k * 6;
+        r[0] += xv;
+        r[1] += xv * xv;
+        r[2] += yv;
+        r[3] += yv * yv;
+        const double w = xv * yv;
+        r[4] += w;
+        r[5] += w * w;
+      }
+  }
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(P);
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "cross_pool_fixed: %s", cudaGetErrorString(e));
+  return WALLACE_OK;
 }
 
 wallace_status wallace_cross_pool_probes(wallace_handle* h, uint64_t passes, uint32_t n_probes,

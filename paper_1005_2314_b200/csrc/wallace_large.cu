@@ -20,6 +20,14 @@ namespace {
 
 constexpr int kLgThreads = 256;
 
+// 2-D launches over (blocks of a pool) x (pools): gridDim.y/z are limited to
+// 65535, so the pool index spans y and z
+__device__ __forceinline__ uint64_t lg_pool_index() { return blockIdx.y + uint64_t(blockIdx.z) * 65535u; }
+inline dim3 lg_grid(uint64_t bx, uint64_t n_pools) {
+  const uint64_t y = n_pools < 65535 ? n_pools : 65535;
+  return dim3{unsigned(bx), unsigned(y), unsigned((n_pools + 65534) / 65535)};
+}
+
 __device__ __forceinline__ const uint32_t* plan_at(const FillArgs& a, uint64_t pool, uint32_t p, uint32_t pw) {
   return a.plans + pool * a.plan_stride + uint64_t(p) * pw;
 }
@@ -44,7 +52,8 @@ __global__ void lg_prologue(const FillArgs a, uint64_t n_pools) {
 // drain the partially consumed emission (pool_kernel's lead)
 template <typename T>
 __global__ void lg_lead(const FillArgs a, const T* pool_buf, uint64_t N) {
-  const uint64_t pool = blockIdx.y;
+  const uint64_t pool = lg_pool_index();
+  if (pool >= a.lg_npools) return;
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.lead) return;
   const SState& s = static_cast<const SState*>(a.lg_state)[pool];
@@ -76,7 +85,8 @@ __device__ __forceinline__ void lg_emit4(const FillArgs& a, uint64_t pool, uint6
 template <typename T, int MIX>
 __global__ void lg_pass_wallace(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N, int emit_slot,
                                 uint64_t gofs, uint32_t limit) {
-  const uint64_t pool = blockIdx.y;
+  const uint64_t pool = lg_pool_index();
+  if (pool >= a.lg_npools) return;
   const uint64_t rows = N / 4;
   const uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= rows) return;
@@ -112,7 +122,8 @@ __global__ void lg_pass_wallace(const FillArgs a, const T* in, T* out, uint32_t 
 template <typename T, int MIX, int SWEEP>
 __global__ void lg_pass_rotation(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N, int emit_slot,
                                  uint64_t gofs, uint32_t limit) {
-  const uint64_t pool = blockIdx.y;
+  const uint64_t pool = lg_pool_index();
+  if (pool >= a.lg_npools) return;
   const uint64_t rows = N / 4;
   const uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= rows) return;
@@ -186,7 +197,8 @@ __global__ void lg_renorm_begin(const FillArgs a, const T* pool_buf, uint64_t N)
 }
 template <typename T>
 __global__ void lg_renorm_scale(const FillArgs a, T* pool_buf, uint64_t N) {
-  const uint64_t pool = blockIdx.y;
+  const uint64_t pool = lg_pool_index();
+  if (pool >= a.lg_npools) return;
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const SState& s = static_cast<const SState*>(a.lg_state)[pool];
   if (i >= N || !s.renorm_ok) return;
@@ -212,7 +224,8 @@ __global__ void lg_renorm_end(const FillArgs a, const T* pool_buf, uint64_t N, i
 
 template <typename T>
 __global__ void lg_emit(const FillArgs a, const T* pool_buf, uint64_t N, uint64_t gofs, uint32_t limit, int slot) {
-  const uint64_t pool = blockIdx.y;
+  const uint64_t pool = lg_pool_index();
+  if (pool >= a.lg_npools) return;
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= limit) return;
   const SState& s = static_cast<const SState*>(a.lg_state)[pool];
@@ -284,7 +297,8 @@ template <typename T, int MODE>
 __global__ void lg_consume(const FillArgs a, const T* src, uint64_t src_stride, uint64_t n, int use_cur_scale,
                            int slot) {
   __shared__ double red[kLgThreads / 32];
-  const uint64_t pool = blockIdx.y, blk = blockIdx.x;
+  const uint64_t pool = lg_pool_index(), blk = blockIdx.x;
+  if (pool >= a.lg_npools) return;
   const SState& s = static_cast<const SState*>(a.lg_state)[pool];
   const T sc = from_double<T>(use_cur_scale ? s.cur_scale : s.scale[slot]);
   const T mean = from_double<T>(a.mean);
@@ -385,14 +399,16 @@ __global__ void lg_probe_y(const FillArgs a, const T* pool_buf, uint64_t N, uint
 }
 
 template <typename T>
-cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
+cudaError_t run_large(const FillArgs& args, uint64_t n_pools, cudaStream_t st) {
+  FillArgs a = args;
+  a.lg_npools = n_pools;
   const uint64_t N = uint64_t(1) << a.lg_log2n;
   const uint64_t rows = N / 4;
   const int pt = a.pass_type;
   const bool rot = pt >= 2;
   const unsigned pool_blocks = unsigned((n_pools + 127) / 128);
-  const dim3 grid_rows(unsigned((rows + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
-  const dim3 grid_vals(unsigned((N + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
+  const dim3 grid_rows = lg_grid((rows + kLgThreads - 1) / kLgThreads, n_pools);
+  const dim3 grid_vals = lg_grid((N + kLgThreads - 1) / kLgThreads, n_pools);
   T* w[2] = {static_cast<T*>(a.pools_out), static_cast<T*>(a.lg_pool2)};
   int cur = 0;
   if (a.pools_in != a.pools_out)
@@ -409,7 +425,7 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
     if (e0 == cudaSuccess) e0 = cudaStreamSynchronize(st);
     if (e0 != cudaSuccess) return e0;
     const uint64_t nb = (a.lead + kLgBlockVals - 1) / kLgBlockVals;
-    const dim3 g{unsigned(nb), unsigned(n_pools)};
+    const dim3 g = lg_grid(nb, n_pools);
     if (st0.flags & kFlagLeftover)
       lg_consume<T, kModeConsume><<<g, kLgThreads, 0, st>>>(
           a, static_cast<const T*>(a.leftover) + st0.cursor, N - 1, a.lead, 2, 0);
@@ -417,7 +433,7 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
       lg_consume<T, kModeConsume><<<g, kLgThreads, 0, st>>>(a, w[0] + st0.cursor, N, a.lead, 1, 0);
     lg_fold<kModeConsume><<<pool_blocks, 128, 0, st>>>(a, nb, 0, n_pools);
   } else if (a.mode != kModePasses && a.lead > 0 && !cons) {
-    const dim3 g(unsigned((a.lead + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
+    const dim3 g = lg_grid((a.lead + kLgThreads - 1) / kLgThreads, n_pools);
     lg_lead<T><<<g, kLgThreads, 0, st>>>(a, w[0], N);
   }
   // one pass; emit_slot >= 0 fuses the emission (values i < limit at gofs)
@@ -463,14 +479,14 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
         if (pc == 0) renorm(slot, 1);
         if (emit) {
           const uint64_t nb = (limit + kLgBlockVals - 1) / kLgBlockVals;
-          const dim3 gc{unsigned(nb), unsigned(n_pools)};
+          const dim3 gc = lg_grid(nb, n_pools);
           if (a.mode == kModeConsume) {
             lg_consume<T, kModeConsume><<<gc, kLgThreads, 0, st>>>(a, w[cur], N, limit, 0, slot);
             lg_fold<kModeConsume><<<pool_blocks, 128, 0, st>>>(a, nb, e, n_pools);
           } else if (a.mode == kModeDefect) {
             lg_consume<T, kModeDefect><<<gc, kLgThreads, 0, st>>>(a, w[cur], N, limit, 0, slot);
           } else if (!fuse) {
-            const dim3 g(unsigned((limit + kLgThreads - 1) / kLgThreads), unsigned(n_pools));
+            const dim3 g = lg_grid((limit + kLgThreads - 1) / kLgThreads, n_pools);
             lg_emit<T><<<g, kLgThreads, 0, st>>>(a, w[cur], N, gofs, limit, slot);
           }
           lg_chain<T><<<pool_blocks, 128, 0, st>>>(a, w[cur], N, slot, e + 1 < a.n_emit ? 1 : 0, n_pools);
@@ -487,6 +503,38 @@ cudaError_t run_large(const FillArgs& a, uint64_t n_pools, cudaStream_t st) {
 }
 
 }  // namespace
+
+// One pass (generator.cpp:259-271 run_pass) over n_pools pools in buf_a with
+// the plan words in a.plans (large format, p = 0), scratch buf_b.  Returns
+// through *in_b whether the result sits in buf_b (wallace4) or buf_a
+// (rotation ends where it started).
+cudaError_t launch_single_pass(int dtype, const FillArgs& a, void* buf_a, void* buf_b, uint64_t n_pools,
+                               cudaStream_t st, int* in_b) {
+  const uint64_t N = uint64_t(1) << a.lg_log2n;
+  const dim3 grid = lg_grid((N / 4 + kLgThreads - 1) / kLgThreads, n_pools);
+  FillArgs b = a;
+  b.lg_npools = n_pools;
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    T* A = static_cast<T*>(buf_a);
+    T* B = static_cast<T*>(buf_b);
+    switch (a.pass_type) {
+      case 0: lg_pass_wallace<T, 0><<<grid, kLgThreads, 0, st>>>(b, A, B, 0, N, -1, 0, 0); break;
+      case 1: lg_pass_wallace<T, 1><<<grid, kLgThreads, 0, st>>>(b, A, B, 0, N, -1, 0, 0); break;
+      case 2:
+        lg_pass_rotation<T, 0, 0><<<grid, kLgThreads, 0, st>>>(b, A, B, 0, N, -1, 0, 0);
+        lg_pass_rotation<T, 0, 1><<<grid, kLgThreads, 0, st>>>(b, B, A, 0, N, -1, 0, 0);
+        break;
+      default:
+        lg_pass_rotation<T, 1, 0><<<grid, kLgThreads, 0, st>>>(b, A, B, 0, N, -1, 0, 0);
+        lg_pass_rotation<T, 1, 1><<<grid, kLgThreads, 0, st>>>(b, B, A, 0, N, -1, 0, 0);
+    }
+  };
+  if (dtype == 0) go(float{});
+  else go(double{});
+  *in_b = a.pass_type < 2 ? 1 : 0;
+  return cudaGetLastError();
+}
 
 // doubles of aux scratch per pool for pool size N
 uint64_t large_aux_stride(uint64_t N) { return kAuxPart + 4 * ((N + kLgBlockVals - 1) / kLgBlockVals); }

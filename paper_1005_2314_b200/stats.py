@@ -142,3 +142,19 @@ def rare_event_adjacency_report(marks, pool_size: int) -> TestReport:
     c = cond / cond_pop
     se_cond = math.sqrt(b * (1.0 - b) / cond_pop)
     return TestReport.make(name, c / b, 1.0, se_cond / b)
+
+
+def cross_pool_correlation_fixed(cfg, pairs: int, probes=None, expect_composed_q: bool = False):
+    """stats.cpp:260-307 with opts.fixed_transform: fresh Polar pools, one
+    pinned pass each (device), reports against 0 or the composed q_{i,j}."""
+    import paper_1005_2314_b200 as pb
+    if pairs < 1000:
+        raise ValueError("cross_pool_correlation: pool_pairs must be >= 1000")
+    probes = default_probes(cfg.pool_size) if probes is None else list(probes)
+    acc = pb.cross_pool_fixed_sums(cfg, pairs, probes)
+    plan = pb.pass_plan()
+    out = []
+    for k, (oi, ij) in enumerate(probes):
+        exp = pb.pass_coefficient(cfg, plan, oi, ij) if expect_composed_q else 0.0
+        out.append(probe_report(acc[k], pairs, probe_name(oi, ij), exp))
+    return out

@@ -33,6 +33,12 @@ int ref_pool_sum_squares(uint64_t pool_size, int chi2_method, uint64_t discard_e
                          int disable_chi2, int family, int mixing, uint64_t pools, double* out);
 int ref_rare_event_adjacency(uint64_t pool_size, int chi2_method, uint64_t discard_every, uint64_t seed,
                              int disable_chi2, uint64_t samples, double threshold, double* out);
+int ref_run_pass(uint64_t n, int family, int mixing, const int32_t* ints, const uint64_t* offs, const double* in,
+                 double* out);
+double ref_pass_coefficient(uint64_t n, int family, int mixing, const int32_t* ints, const uint64_t* offs,
+                            uint64_t i, uint64_t j);
+int ref_cross_pool_fixed(uint64_t n, int family, int mixing, uint64_t seed, uint64_t pairs, uint32_t n_probes,
+                         const uint64_t* out_i, const uint64_t* in_j, int expect_q, double* out);
 }
 
 namespace wb = wallace_b200;
@@ -395,6 +401,53 @@ int main() {
     CHECK(std::abs(ps.mean_report.statistic - po[0]) <= 1e-9 * po[0]);
     CHECK(std::abs(ps.variance_report.statistic - po[4]) <= 1e-9 * po[4]);
     CHECK(ps.mean_report.pass && ps.variance_report.pass);
+  }
+  // generator.hpp free functions: run_pass / pass_coefficient, and the
+  // fixed-transform cross-pool test (criterion 4's second half)
+  {
+    wb::GeneratorConfig c = cfg_of(64, 20260808);
+    c.transform_family = wb::TransformFamily::rotation;
+    c.mixing = wb::MixingScheme::affine;
+    wb::PassPlan plan;
+    plan.t_index = {3, 11};
+    plan.negate = {true, false};
+    plan.offset = {17, 40};
+    const int32_t ints[5] = {0, 3, 11, 1, 0};
+    const uint64_t offs[2] = {17, 40};
+    std::vector<double> in(64), out(64), ref_out(64);
+    for (int k = 0; k < 64; ++k) in[static_cast<std::size_t>(k)] = std::sin(0.37 * k + 1.0);
+    wb::run_pass(c, plan, in, out);
+    CHECK(ref_run_pass(64, 1, 1, ints, offs, in.data(), ref_out.data()) == 0);
+    CHECK(same_bits(out, ref_out));
+    bool q_same = true;
+    for (std::size_t i = 0; i < 64 && q_same; ++i)
+      for (std::size_t j = 0; j < 64; ++j)
+        q_same = q_same && wb::pass_coefficient(c, plan, i, j) == ref_pass_coefficient(64, 1, 1, ints, offs, i, j);
+    CHECK(q_same);
+    wb::GeneratorConfig c4 = cfg_of(64, 20260808);
+    wb::CrossPoolOptions fixed;
+    fixed.pool_pairs = 20000;
+    fixed.fixed_transform = true;
+    fixed.expect_composed_q = true;
+    for (std::size_t i = 0; i < 64 && fixed.probes.size() < 4; ++i)
+      for (std::size_t j = 0; j < 64; ++j)
+        if (std::abs(wb::pass_coefficient(c4, wb::PassPlan{}, i, j)) == 0.5) {
+          fixed.probes.push_back({i, j});
+          break;
+        }
+    const auto mine = wb::cross_pool_correlation(c4, fixed);
+    std::vector<uint64_t> oi, ij;
+    for (const auto& p : fixed.probes) {
+      oi.push_back(p.out_i);
+      ij.push_back(p.in_j);
+    }
+    double out4[16];
+    CHECK(ref_cross_pool_fixed(64, 0, 0, 20260808, 20000, 4, oi.data(), ij.data(), 1, out4) == 4);
+    bool same = mine.size() == 4;
+    for (std::size_t k = 0; k < mine.size() && same; ++k)
+      same = mine[k].statistic == out4[4 * k] && mine[k].expected == out4[4 * k + 1] &&
+             mine[k].std_error == out4[4 * k + 2] && mine[k].z_score == out4[4 * k + 3];
+    CHECK(same);
   }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

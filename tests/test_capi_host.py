@@ -127,3 +127,23 @@ def test_plan_decode_ex_vs_reference(ref, fam, mix):
             assert (got.wallace_variant, got.t_index[0], got.t_index[1], got.negate[0],
                     got.negate[1]) == tuple(ints)
             assert (got.offset[0], got.offset[1]) == tuple(offs)
+
+
+@pytest.mark.parametrize("fam,mix", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_pass_coefficient_vs_reference(ref, fam, mix):
+    """generator.cpp:273-284 over every (i, j) of small pools, random plans."""
+    L, R = _capi.load(), ref.ref_lib()
+    rng = np.random.default_rng(11)
+    for n in (32, 64):
+        cfg = pb.GeneratorConfig(pool_size=n, transform_family=fam, mixing=mix)
+        mask = n // 4 - 1 if mix == 0 else n - 1
+        for _ in range(3):
+            ints = [int(rng.integers(384)), int(rng.integers(16)), int(rng.integers(16)),
+                    int(rng.integers(2)), int(rng.integers(2))]
+            offs = [int(rng.integers(mask + 1)), int(rng.integers(mask + 1))]
+            plan = pb.pass_plan(ints[0], ints[1:3], ints[3:5], offs)
+            ci = (C.c_int32 * 5)(*ints)
+            co = (C.c_uint64 * 2)(*offs)
+            for i in range(n):
+                for j in range(n):
+                    assert pb.pass_coefficient(cfg, plan, i, j) == R.ref_pass_coefficient(n, fam, mix, ci, co, i, j)
