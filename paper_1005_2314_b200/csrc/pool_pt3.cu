@@ -1,4 +1,8 @@
 // Pool-kernel instantiations for pass type 3 (rotation + affine).
+// rotation passes are ping-pong only (measurement variants may set the
+// in-place knobs for the wallace4 pass types)
+#undef WB_INPLACE_F32
+#undef WB_INPLACE_F64
 #include "wallace_pool.cuh"
 
 namespace wb {

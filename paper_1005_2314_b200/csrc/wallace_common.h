@@ -62,6 +62,10 @@ enum Mode : int32_t {
                      // itself (scale 1, mean +0): bulk copies from shared memory
   kModeDefect = 4,   // emit into the defect-suite consumer: per-emission sum
                      // of squares (+ reserved^2) and rare-event mark
+  kModeFillStaged = 5, // emit into the caller's buffer, any scale: after the
+                     // emission pass's barrier the scaled values are staged
+                     // in the dead source buffer and each warp sends its
+                     // segment with one bulk copy
 };
 
 struct FillArgs {

@@ -222,6 +222,7 @@ struct wallace_handle {
   int key = 0;        // kernel key: log2(N) (+16 for the latency kernel)
   int kmode = 0;      // 0 auto, 1 throughput, 2 latency
   bool bulk_ok = false;  // fills may use the bulk-emission kernel
+  bool staged_ok = false;  // other fills may use the staged-emission kernel
   // pools above the on-chip limit: HBM-resident executor (wallace_large.cu)
   bool large = false;
   void* d_lg_pool2 = nullptr;
@@ -520,6 +521,8 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     // every emission is the pool itself (scale exactly 1, mean +0): the
     // bulk-emission kernel (throughput geometry, wallace4 passes)
     if (mode == wb::kModeFill && h->bulk_ok && h->key < 16 && h->log2n >= 7) a.mode = wb::kModeFillBulk;
+    else if (mode == wb::kModeFill && h->staged_ok && h->key < 16 && h->log2n >= 7)
+      a.mode = wb::kModeFillStaged;
     if (mode == wb::kModeDefect) a.def_e0 = produced / (h->N - 1);  // defect runs start at an emission
     a.out = out;
     a.out_stride = count;
@@ -778,6 +781,10 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
     const char* nb = std::getenv("WALLACE_B200_NO_BULK");
     h->bulk_ok = cfg->disable_chi2 && cfg->out_sigma == 1.0 && cfg->out_mean == 0.0 &&
                  !std::signbit(cfg->out_mean) && h->pass_type < 2 && !(nb && nb[0] == '1');
+    // any other wallace4 fill: scaled values staged in shared memory and
+    // sent by bulk copies (WALLACE_B200_NO_STAGED=1: register emission)
+    const char* ns = std::getenv("WALLACE_B200_NO_STAGED");
+    h->staged_ok = h->pass_type < 2 && !(ns && ns[0] == '1');
   }
   if (!device_seed) {
     WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,

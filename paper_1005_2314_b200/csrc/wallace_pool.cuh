@@ -82,7 +82,9 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #define WB_REGS_INPLACE 56
 #endif
 // ABLATION builds only (timing experiments, wrong output): 1 = skip the
-// fast emission, 2 = skip its global stores, 3 = skip the scalar chain
+// fast emission, 2 = skip its global stores, 3 = skip the scalar chain,
+// 7 = staged emission without the wait for the bulk copy's read, 8 = staged
+// emission without its shared stores
 #ifndef WB_ABLATE
 #define WB_ABLATE 0
 #endif
@@ -144,6 +146,14 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #endif
 #ifndef WB_JC_F64
 #define WB_JC_F64 8
+#endif
+// staged emission: 1 = the owner's per-emission chain runs after the
+// emission's barrier (off its critical path) instead of before it
+#ifndef WB_DEFER_F32
+#define WB_DEFER_F32 0
+#endif
+#ifndef WB_DEFER_F64
+#define WB_DEFER_F64 1
 #endif
 #ifndef WB_HS_LUT
 #define WB_HS_LUT 1
@@ -558,12 +568,20 @@ __device__ __forceinline__ bool is_neg_zero(T x) {
 // N-1 included -- into a shared buffer whose layout is shifted by the
 // emission's misalignment (see "Bulk emission"); zf collects whether any
 // value is an exact -0 (which the emission must turn into +0).
-template <typename T, int LOG2N, int DELTA, bool MZ, bool SMD = false>
+//
+// STAGED (staged emission): the scaled values y go to a shared buffer in the
+// same shifted layout (gbase is then that buffer's element 0), except the
+// scalar head/tail values at the warp's ends, which go straight to global
+// memory at g1 (the emission's element 0 there).  Every 16-byte vector a warp
+// writes lies inside its own segment, so each warp can send its segment with
+// one bulk copy (staged_range).
+template <typename T, int LOG2N, int DELTA, bool MZ, bool SMD = false, bool STAGED = false>
 __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], int c0, T (&prev)[4],
                                            T* gbase, T sc, T mean, int lane, int warp,
-                                           int jfirst = 0, uint32_t* zf = nullptr) {
+                                           int jfirst = 0, uint32_t* zf = nullptr, T* g1 = nullptr) {
   using G = Geo<T, LOG2N>;
   constexpr int J = G::J, JC = G::JC, VEC = G::VEC;
+  static_assert(!(SMD && STAGED), "one destination kind");
   constexpr uint32_t NLIM = SMD ? G::N : G::N - 1;  // elements written
   static_assert(DELTA < VEC, "shift");
 #if WB_ABLATE == 6
@@ -576,7 +594,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
   } ablate_flush{ablate_x};
 #endif
   auto put_vec = [&](T* p, const T* v) {
-    if constexpr (SMD) {
+    if constexpr (SMD || STAGED) {
       if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
       else *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
     } else {
@@ -585,6 +603,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
   };
   auto put1 = [&](T* p, T v) {
     if constexpr (SMD) *p = v;
+    else if constexpr (STAGED) stg1(g1 + (p - gbase), v);
     else stg1(p, v);
   };
   const bool l31 = lane == 31;
@@ -618,7 +637,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         y[k] = X[jj][k];
         z |= is_neg_zero(y[k]) ? 1u : 0u;
       }
-    } else if constexpr ((WB_PACKED & 2) && MZ && sizeof(T) == 4) {
+    } else if constexpr ((WB_PACKED & 2) && MZ && sizeof(T) == 4 && !STAGED) {
       // (only the mean-zero form: ptxas contracts a packed mul.rn + add.rn
       // pair into one FFMA2 despite the explicit rounding modifiers)
       const uint64_t s2 = pk2(sc, sc);
@@ -629,7 +648,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
 #pragma unroll
       for (int k = 0; k < 4; ++k) y[k] = MZ ? fma_rn(X[jj][k], sc, T(0)) : add_rn(mul_rn(X[jj][k], sc), mean);
     }
-    if constexpr (!SMD && WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
+    if constexpr (!SMD && !STAGED && WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) {
       // global(4b) is 8-byte aligned: two float2 stores of the own block,
       // no neighbour values needed
       if (b != G::ROWS - 1) {
@@ -658,7 +677,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       prev[0] = s;
     } else if constexpr (DELTA == 0) {
       if (SMD || b != G::ROWS - 1) {
-        if constexpr (WB_EMIT_IMM && !SMD) {
+        if constexpr (WB_EMIT_IMM && !SMD && !STAGED) {
           static_for<JC>([&](auto jjc) {
             if (decltype(jjc)::value == jj) store_group(jjc, y);
           });
@@ -682,7 +701,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         else c[m] = sh[(DELTA + m - 4) & (DELTA > 0 ? 3 : 0)];
       }
       if (!(l31 && j == jfirst)) {
-        if constexpr (WB_EMIT_IMM && !SMD) {
+        if constexpr (WB_EMIT_IMM && !SMD && !STAGED) {
           static_for<JC>([&](auto jjc) {
             if (decltype(jjc)::value == jj) store_group(jjc, c);
           });
@@ -700,7 +719,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       for (int k = 0; k < 4; ++k) prev[k] = y[k];
     }
   }
-  if constexpr (DELTA > 0 && !(!SMD && WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) &&
+  if constexpr (DELTA > 0 && !(!SMD && !STAGED && WB_D2_STG64 && sizeof(T) == 4 && DELTA == 2) &&
                 !(WB_D3_DOWN && VEC == 4 && DELTA == 3)) {
     if (l31 && c0 + JC == J) {  // last group of the warp: own tail only, the head is the next warp's
       const uint32_t b = (warp * J + J - 1) * 32 + 31;
@@ -740,6 +759,53 @@ __device__ __forceinline__ void shift_chunk_any(uint32_t delta, const T (&X)[Geo
   } else {
     if (delta == 0) emit_chunk<T, LOG2N, 0, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf);
     else emit_chunk<T, LOG2N, 1, true, true>(X, c0, prev, sbase, T(1), T(0), lane, warp, 0, zf);
+  }
+}
+
+// The staged write of an emission (kModeFillStaged): scaled values into the
+// shifted shared layout at sbase, warp-end scalars to global at g1.
+template <typename T, int LOG2N>
+__device__ __forceinline__ void stage_chunk_any(uint32_t delta, bool mz, const T (&X)[Geo<T, LOG2N>::JC][4],
+                                                int c0, T (&prev)[4], T* sbase, T* g1, T sc, T mean,
+                                                int lane, int warp) {
+  using G = Geo<T, LOG2N>;
+#define WB_STAGE(D)                                                                                     \
+  (mz ? emit_chunk<T, LOG2N, (D) % G::VEC, true, false, true>(X, c0, prev, sbase, sc, mean, lane, warp, 0, \
+                                                               nullptr, g1)                              \
+      : emit_chunk<T, LOG2N, (D) % G::VEC, false, false, true>(X, c0, prev, sbase, sc, mean, lane, warp, 0, \
+                                                                nullptr, g1))
+  if constexpr (G::VEC == 4) {
+    switch (delta) {
+      case 0: WB_STAGE(0); break;
+      case 1: WB_STAGE(1); break;
+      case 2: WB_STAGE(2); break;
+      default: WB_STAGE(3); break;
+    }
+  } else {
+    if (delta == 0) WB_STAGE(0);
+    else WB_STAGE(1);
+  }
+#undef WB_STAGE
+}
+
+// The slots [lo, hi) of the shifted staging layout (slot = element + sigma)
+// that warp w filled with 16-byte vectors in stage_chunk_any: its segment
+// [w*WE, (w+1)*WE) minus the partial vectors at its ends, which went out as
+// scalars (emit_chunk: lane 0's head, lane 31's last block; the pool's last
+// block when sigma = 0, element N-1 not emitted).
+template <typename T, int LOG2N>
+__device__ __forceinline__ void staged_range(uint32_t sigma, int warp, uint32_t& lo, uint32_t& hi) {
+  using G = Geo<T, LOG2N>;
+  constexpr uint32_t WE = 128u * G::J;  // elements per warp segment
+  lo = warp * WE;
+  hi = lo + WE;
+  if (sigma == 0) {
+    if (warp == G::NW - 1) hi -= 4;
+  } else if constexpr (G::VEC == 4) {
+    lo += 4;
+  } else {
+    lo += 2;
+    hi -= 2;
   }
 }
 
@@ -855,7 +921,8 @@ __device__ __forceinline__ void affine_gather4(const char* base, uint32_t buf, u
 template <typename T, int LOG2N, int J, int PT = 0>
 __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
                                          uint32_t plan, uint32_t b0, T (&X)[J][4],
-                                         const float* hs_lut, bool store = true) {
+                                         const float* hs_lut, bool store = true,
+                                         bool wait_stage = false) {
   static_assert(PT == 0 || PT == 1, "wallace4 pass types");
   using G = Geo<T, LOG2N>;
   constexpr int ROWS = G::ROWS;
@@ -985,6 +1052,12 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
   }
   if constexpr (G::INPLACE) __syncthreads();  // every gather of this pass is done
   if (!store) return;  // the caller writes the shifted layout (bulk emission)
+  if (wait_stage) {
+    // staged emission: this warp's bulk copy must have read its segment of
+    // the buffer these stores overwrite (the segment is the warp's own blocks)
+    if ((threadIdx.x & 31u) == 0) bulk_wait_read();
+    __syncwarp();
+  }
   T* nb = reinterpret_cast<T*>(const_cast<char*>(base) + nxt_off);
   if constexpr (sizeof(T) == 8) {
     // a 4-double block is 32 bytes: two 128-bit stores at a 32-byte lane
@@ -1322,6 +1395,12 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     constexpr bool BULK_OK = MODE == kModeFillBulk;
     static_assert(!BULK_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE), "bulk geometry");
     bool bulk_pending = false;
+    // staged emission (see "Staged emission")
+    constexpr bool STAGED_OK = MODE == kModeFillStaged;
+    static_assert(!STAGED_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE && G::JC == G::J),
+                  "staged geometry");
+    bool stage_pending = false;  // this warp's last bulk copy may still read the next pass's buffer
+    constexpr bool DEFER = STAGED_OK && (sizeof(T) == 4 ? WB_DEFER_F32 : WB_DEFER_F64);
     T* gbase = out_pool + a.lead;  // element 0 of the current emission
     for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
       const int slot = e & 1;
@@ -1372,14 +1451,15 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         // consumer remove its spills but cost a second permutation dispatch
         // per pass: measured slower)
         constexpr int JCL = G::JC;
+        const bool staged = STAGED_OK && do_emit;
+        T X[JCL][4];  // (staged: still live after the barrier)
         for (int c0 = 0; c0 < J && compute; c0 += JCL) {
-          T X[JCL][4];
           if constexpr (ROT)
             run_pass_rot<T, LOG2N, JCL, PT & 1>(cbase, cur_off, cur_off ^ FLIP, plan_p, plan_q, b0 + 32 * c0, X,
                                                 a.rot_c, a.rot_s);
           else
             run_pass<T, LOG2N, JCL, PT>(cbase, cur_off + sh, cur_off ^ FLIP, plan_p, b0 + 32 * c0, X, s_hs,
-                                        !bulk);
+                                        !bulk, STAGED_OK && stage_pending);
           if (do_emit) {
             if constexpr (MODE == kModeDefect) {
               defect_chunk<T, LOG2N, JCL>(X, dsum, dmark, sc, mean_t, mean_zero, b0 + 32 * c0, a.def_threshold);
@@ -1387,6 +1467,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
               if constexpr (BULK_OK) {
                 T* sb = reinterpret_cast<T*>(pbase + (cur_off ^ FLIP)) + sigma;
                 shift_chunk_any<T, LOG2N>(delta, X, c0, prev, sb, lane, warp, &zf);
+              } else if constexpr (STAGED_OK) {
+                // written after the barrier (below)
               } else {
 #if WB_ABLATE == 5
                 emit_chunk_any<T, LOG2N>(delta, mean_zero, X, c0, prev,
@@ -1402,6 +1484,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           }
           x_last = X[JCL - 1][3];
         }
+        if constexpr (STAGED_OK) stage_pending = false;  // waited for in run_pass
         if constexpr (ROT && G::CHAINW)
           if (!compute) __syncthreads();  // the chain warp joins the rotation pass's inner barrier
         if constexpr (MODE == kModeConsume)
@@ -1420,7 +1503,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           fence_proxy_async_smem();  // this thread's shared stores -> visible to the bulk copy
           if (zf) s.zero_seen = 1;
         }
-        if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3) {
+        if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3 && !DEFER) {
           if constexpr (BULK_OK) {
             // bulk kernels run with disable_chi2: S = sum_sq, r and scale are
             // functions of the current sum_sq alone, nothing in the launch
@@ -1443,6 +1526,37 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         cur_off ^= PFLIP;
         sh = bulk ? sigma * uint32_t(sizeof(T)) : 0u;
         T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
+        if constexpr (STAGED_OK) {
+          if (staged) {
+            // the pass's source buffer is dead: the scaled values go there in
+            // the shifted layout, and each warp sends its segment (one bulk
+            // copy, issued by lane 0) while the next pass runs; that pass
+            // waits for the copy's read before its stores (run_pass)
+            // (the scale is read here: for d = 1 the owner publishes it
+            // behind the barrier that ends this pass, see below)
+            const T scs = DEFER ? from_double<T>(s.scale[slot]) : sc;
+            T* const sb = reinterpret_cast<T*>(pbase + (cur_off ^ FLIP)) + sigma;
+            if (WB_ABLATE != 8)
+              stage_chunk_any<T, LOG2N>(delta, mean_zero, X, 0, prev, sb, gbase, scs, mean_t, lane, warp);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              uint32_t lo, hi;
+              staged_range<T, LOG2N>(sigma, warp, lo, hi);
+              bulk_s2g(gbase + (lo - sigma), static_cast<uint32_t>(__cvta_generic_to_shared(sb - sigma + lo)),
+                       (hi - lo) * uint32_t(sizeof(T)));
+              bulk_commit();
+            }
+            stage_pending = WB_ABLATE != 7;
+            // generator.cpp:373-375 for this emission and S/r/scale of the
+            // next one, off the barrier's critical path: the next reader is
+            // the next emission, behind at least one more barrier
+            if (DEFER && tid == G::OWNER && WB_ABLATE != 3) {
+              chain_close(s, slot, static_cast<double>(x_last));
+              if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+            }
+          }
+        }
         if (G::CHAINW && fast && tid == G::CT) {
           // generator.cpp:373-375 for emission e, then S/r/scale of e+1; the
           // compute warps pick them up at emission e+1 (acquire on s.ready)
@@ -1566,6 +1680,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       }
     }
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
+    if (STAGED_OK && lane == 0) bulk_wait_all();
+    if (DEFER) __syncthreads();  // the owner's last chain precedes the epilogue
     if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
   }
   T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
@@ -1654,8 +1770,13 @@ cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream
     case kModeFill: return launch_pool_mode<T, LOG2N, kModeFill, PT>(a, n_pools, stream);
     case kModeFillBulk:
       // the host selects it for the throughput geometry and wallace4 only
-      if constexpr (LOG2N < 16 && LOG2N >= 7 && PT < 2)
+      if constexpr (LOG2N < 16 && LOG2N >= 7 && PT < 2 && !Geo<T, LOG2N>::INPLACE)
         return launch_pool_mode<T, LOG2N, kModeFillBulk, PT>(a, n_pools, stream);
+      else
+        return cudaErrorInvalidValue;
+    case kModeFillStaged:
+      if constexpr (LOG2N < 16 && LOG2N >= 7 && PT < 2 && !Geo<T, LOG2N>::INPLACE)
+        return launch_pool_mode<T, LOG2N, kModeFillStaged, PT>(a, n_pools, stream);
       else
         return cudaErrorInvalidValue;
     case kModePasses: return launch_pool_mode<T, LOG2N, kModePasses, PT>(a, n_pools, stream);
