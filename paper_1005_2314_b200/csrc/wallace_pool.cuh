@@ -1452,8 +1452,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         // per pass: measured slower)
         constexpr int JCL = G::JC;
         const bool staged = STAGED_OK && do_emit;
-        T X[JCL][4];  // (staged: still live after the barrier)
+        T Xo[STAGED_OK ? JCL : 1][4];  // staged: the pass's values stay live after the barrier
         for (int c0 = 0; c0 < J && compute; c0 += JCL) {
+          T Xi[STAGED_OK ? 1 : JCL][4];
+          T (&X)[JCL][4] = *reinterpret_cast<T(*)[JCL][4]>(STAGED_OK ? &Xo[0][0] : &Xi[0][0]);
           if constexpr (ROT)
             run_pass_rot<T, LOG2N, JCL, PT & 1>(cbase, cur_off, cur_off ^ FLIP, plan_p, plan_q, b0 + 32 * c0, X,
                                                 a.rot_c, a.rot_s);
@@ -1536,6 +1538,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             // behind the barrier that ends this pass, see below)
             const T scs = DEFER ? from_double<T>(s.scale[slot]) : sc;
             T* const sb = reinterpret_cast<T*>(pbase + (cur_off ^ FLIP)) + sigma;
+            T (&X)[JCL][4] = *reinterpret_cast<T(*)[JCL][4]>(&Xo[0][0]);
             if (WB_ABLATE != 8)
               stage_chunk_any<T, LOG2N>(delta, mean_zero, X, 0, prev, sb, gbase, scs, mean_t, lane, warp);
             fence_proxy_async_smem();
