@@ -66,6 +66,10 @@ enum Mode : int32_t {
                      // emission pass's barrier the scaled values are staged
                      // in the dead source buffer and each warp sends its
                      // segment with one bulk copy
+  kModeFillLat = 6,  // emit into the caller's buffer, latency geometry: the
+                     // passes emit raw pool values (bulk copies), a chain
+                     // warp runs the per-emission chi2/scale recurrence off
+                     // the passes' critical path, rescale_kernel applies it
 };
 
 struct FillArgs {
@@ -120,6 +124,9 @@ struct FillArgs {
   double* lg_aux;         // per pool: consumer totals, defect mark, probe x, block partials
   uint64_t lg_aux_stride; // doubles per pool
   uint64_t lg_npools;     // pools of the launch (pool index = blockIdx.y + 65535 * blockIdx.z)
+  // kModeFillLat: per-emission scale of each pool, [n_pools][scale_stride]
+  double* scales;
+  uint64_t scale_stride;
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]

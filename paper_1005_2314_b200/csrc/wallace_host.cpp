@@ -41,6 +41,7 @@ cudaError_t launch_single_pass(int dtype, const FillArgs& a, void* buf_a, void* 
 cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
                         PoolState* st, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
+cudaError_t launch_rescale(int dtype, const FillArgs& a, uint32_t N, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void* leftover,
                                uint64_t n_pools, uint32_t N, double mean, cudaStream_t s);
 cudaError_t launch_reduce_consumer(const double* part_sums, const uint32_t* part_hist,
@@ -223,6 +224,8 @@ struct wallace_handle {
   int kmode = 0;      // 0 auto, 1 throughput, 2 latency
   bool bulk_ok = false;  // fills may use the bulk-emission kernel
   bool staged_ok = false;  // other fills may use the staged-emission kernel
+  bool lat_fill_ok = false;  // latency-geometry fills may decouple the chi2 chain (kModeFillLat)
+  double* d_scales = nullptr;  // kModeFillLat: [n_pools][plan_cap] per-emission scales
   // pools above the on-chip limit: HBM-resident executor (wallace_large.cu)
   bool large = false;
   void* d_lg_pool2 = nullptr;
@@ -461,6 +464,10 @@ wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
     WB_CUDA(timed(h, h->ev_pool, h->stream,
                   [&] { return wb::launch_pool_kernel(h->dtype, h->key, a, h->n_pools, h->stream); }));
     ++g_launches;
+    if (a.mode == wb::kModeFillLat && a.n_emit > 0) {  // the chain's scales onto the raw emissions
+      WB_CUDA(wb::launch_rescale(h->dtype, a, static_cast<uint32_t>(h->N), h->n_pools, h->stream));
+      ++g_launches;
+    }
     WB_CUDA(cudaEventRecord(h->ev_pooled[k & 1], h->stream));
   }
   return WALLACE_OK;
@@ -523,6 +530,12 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     if (mode == wb::kModeFill && h->bulk_ok && h->key < 16 && h->log2n >= 7) a.mode = wb::kModeFillBulk;
     else if (mode == wb::kModeFill && h->staged_ok && h->key < 16 && h->log2n >= 7)
       a.mode = wb::kModeFillStaged;
+    else if (mode == wb::kModeFill && h->lat_fill_ok && h->key >= 16 && h->key < 64) {
+      if (!h->d_scales) WB_CUDA(cudaMalloc(&h->d_scales, h->n_pools * size_t(h->plan_cap) * sizeof(double)));
+      a.mode = wb::kModeFillLat;
+      a.scales = h->d_scales;
+      a.scale_stride = h->plan_cap;
+    }
     if (mode == wb::kModeDefect) a.def_e0 = produced / (h->N - 1);  // defect runs start at an emission
     a.out = out;
     a.out_stride = count;
@@ -785,6 +798,10 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
     // sent by bulk copies (WALLACE_B200_NO_STAGED=1: register emission)
     const char* ns = std::getenv("WALLACE_B200_NO_STAGED");
     h->staged_ok = h->pass_type < 2 && !(ns && ns[0] == '1');
+    // latency geometry (few pools), wallace4, up to 512 compute threads plus
+    // the chain warp (WALLACE_B200_NO_LATFILL=1: the coupled chain)
+    const char* nl = std::getenv("WALLACE_B200_NO_LATFILL");
+    h->lat_fill_ok = h->pass_type < 2 && h->log2n >= 7 && h->log2n <= 11 && !(nl && nl[0] == '1');
   }
   if (!device_seed) {
     WB_CUDA_C(cudaMemcpyAsync(h->d_pools, pools.data(), pools.size(), cudaMemcpyHostToDevice,
@@ -827,6 +844,7 @@ wallace_status wallace_destroy(wallace_handle* h) {
     if (h->ev_pooled[i]) cudaEventDestroy(h->ev_pooled[i]);
   }
   cudaFree(h->d_leftover);
+  cudaFree(h->d_scales);
   cudaFree(h->d_snap_pools);
   cudaFree(h->d_snap_state);
   cudaFree(h->d_snap_leftover);

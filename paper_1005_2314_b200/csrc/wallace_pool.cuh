@@ -377,6 +377,9 @@ struct SState {
   uint32_t x_last_bulk_set;  // bulk kernels: the last emission was a fast one
   double x_last_bulk;        // ... and its pool element N-1
   uint32_t ready;      // chain-warp kernels: S/r/scale of every emission <= ready published
+  uint32_t produced;   // kModeFillLat: emissions whose (x_last, sum_sq) are in the ring
+  uint32_t end_off;    // kModeFillLat: the compute threads' final buffer offset and shift
+  uint32_t end_sh;
 };
 
 // S, r, scale of the emission in `slot` from the current reserved value.
@@ -415,6 +418,14 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
                    static_cast<uint32_t>(__cvta_generic_to_shared(p))),
                "r"(v)
                : "memory");
+}
+
+// Barrier of the pass loop: the whole CTA, or (NB) named barrier 1 over the
+// NT compute threads when a decoupled chain warp runs beside the passes.
+template <bool NB, int NT>
+__device__ __forceinline__ void loop_bar() {
+  if constexpr (NB) asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  else __syncthreads();
 }
 
 // generator.cpp:20-34 recompute_sum_sq — sequential Neumaier, one thread.
@@ -471,22 +482,22 @@ __device__ double neumaier_sq(const T* v, int n) {
 // all threads.
 // LAT: the latency kernel (one pool per SM, the renormalisation is on the
 // critical path: vector loads, out of line); otherwise inline scalar loads
-template <typename T, int N, int THREADS, bool LAT>
+template <typename T, int N, int THREADS, bool LAT, bool NB = false>
 __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
   if (tid == 0) {
     const double ss = neumaier_sq<T, LAT>(cur, N);
     s.renorm_ok = ss > 0.0;
     s.renorm_k = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
   }
-  __syncthreads();
+  loop_bar<NB, THREADS>();
   if (s.renorm_ok) {
     const double k = s.renorm_k;
     for (int i = tid; i < N; i += THREADS)
       cur[i] = from_double<T>(__dmul_rn(static_cast<double>(cur[i]), k));
-    __syncthreads();
+    loop_bar<NB, THREADS>();
     if (tid == 0) s.sum_sq = neumaier_sq<T, LAT>(cur, N);
   }
-  __syncthreads();
+  loop_bar<NB, THREADS>();
 }
 
 // ---------------------------------------------------------------------------
@@ -1255,12 +1266,24 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
+// Threads of a pool_kernel instantiation: kModeFillLat adds the chain warp.
+template <typename T, int LOG2N, int MODE>
+constexpr int kernel_threads() {
+  return Geo<T, LOG2N>::THREADS + (MODE == kModeFillLat ? 32 : 0);
+}
+// kModeFillLat ring: (x_last, sum_sq) of every emission of a launch
+constexpr uint32_t kLatRingMax = 2048;
+
 template <typename T, int LOG2N, int MODE, int PT>
-__global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
+__global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), Geo<T, LOG2N>::MINB)
     pool_kernel(const __grid_constant__ FillArgs a) {
   using G = Geo<T, LOG2N>;
   using SM = Smem<T, LOG2N>;
-  constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = G::THREADS;
+  // DEC (kModeFillLat): decoupled chain warp (tid >= CT), see "Latency fills"
+  constexpr bool DEC = MODE == kModeFillLat;
+  static_assert(!DEC || (G::LAT && !G::CHAINW && PT < 2 && G::CT <= 512), "latency-fill geometry");
+  constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = kernel_threads<T, LOG2N, MODE>();
+  constexpr int LT = DEC ? G::CT : THREADS;  // threads of the pass loop
   constexpr uint32_t BUF = SM::BUF;
   constexpr bool FAST = ROWS >= 32;
   // buffer 0 at offset 0, buffer 1 at BSTRIDE; plans in dynamic smem
@@ -1277,6 +1300,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
   unsigned char* const pbase = SM::STATIC ? s_pool : dsmem;
   T* const pools = reinterpret_cast<T*>(pbase);
   uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsmem + (SM::STATIC ? 0 : SM::TOTAL));
+  // kModeFillLat: (x_last, sum_sq) per emission, after the plans
+  double* const ring = reinterpret_cast<double*>(dsmem + (SM::STATIC ? 0 : SM::TOTAL) +
+                                                 ((a.n_passes * 4u * (PT >= 2 ? 2u : 1u) + 15u) & ~15u));
+  (void)ring;
   __shared__ SState s;
   __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
   // defect suite: per-warp partial sums / marks of the last two emissions
@@ -1286,7 +1313,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t b0 = warp * J * 32 + lane;  // first 4-block of this thread
-  const bool compute = !G::CHAINW || tid < G::CT;  // owns 4-blocks (else: chain warp)
+  const bool compute = !(G::CHAINW || DEC) || tid < G::CT;  // owns 4-blocks (else: chain warp)
   const uint64_t pool = blockIdx.x;
   const bool mean_zero = a.mean_is_zero != 0;
   const T mean_t = from_double<T>(a.mean);
@@ -1304,8 +1331,9 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     s.zero_seen = 0;
     s.x_last_bulk_set = 0;
     s.ready = 0;
+    s.produced = 0;
     s.flags = st.flags;
-    if (MODE != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
+    if (MODE != kModePasses && !DEC && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
   }
   if constexpr (MODE == kModeConsume)
     for (int i = tid; i < 258; i += THREADS) s_hist[i] = 0;
@@ -1394,6 +1422,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     // compiled out there, which keeps the general kernel's registers)
     constexpr bool BULK_OK = MODE == kModeFillBulk;
     static_assert(!BULK_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE), "bulk geometry");
+    // raw pool values sent by one bulk copy per emission: the bulk kernel, and
+    // the latency fill (whose values rescale_kernel scales afterwards)
+    constexpr bool RAWB = BULK_OK || DEC;
+    static_assert(!DEC || FAST, "latency-fill geometry");
     bool bulk_pending = false;
     // staged emission (see "Staged emission")
     constexpr bool STAGED_OK = MODE == kModeFillStaged;
@@ -1402,7 +1434,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
     bool stage_pending = false;  // this warp's last bulk copy may still read the next pass's buffer
     constexpr bool DEFER = STAGED_OK && (sizeof(T) == 4 ? WB_DEFER_F32 : WB_DEFER_F64);
     T* gbase = out_pool + a.lead;  // element 0 of the current emission
-    for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
+    // (DEC: the chain warp skips the passes and runs the chain below)
+    for (uint32_t e = 0; e < ((!DEC || compute) ? a.n_emit : 0u); ++e, gbase += N - 1) {
       const int slot = e & 1;
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
       for (uint32_t q = 1; q <= a.d; ++q, ++p) {
@@ -1428,7 +1461,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
 #endif
         }
         // the emission is the pool itself: shifted shared write + bulk copy
-        const bool bulk = BULK_OK && do_emit;
+        const bool bulk = RAWB && do_emit;
         // element shift of the layout this pass writes (bulk) so that slot
         // and global address of every emitted element agree mod 16 bytes
         const uint32_t sigma = (G::VEC - delta) & (G::VEC - 1);
@@ -1466,7 +1499,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             if constexpr (MODE == kModeDefect) {
               defect_chunk<T, LOG2N, JCL>(X, dsum, dmark, sc, mean_t, mean_zero, b0 + 32 * c0, a.def_threshold);
             } else if constexpr (MODE != kModeConsume) {
-              if constexpr (BULK_OK) {
+              if constexpr (RAWB) {
                 T* sb = reinterpret_cast<T*>(pbase + (cur_off ^ FLIP)) + sigma;
                 shift_chunk_any<T, LOG2N>(delta, X, c0, prev, sb, lane, warp, &zf);
               } else if constexpr (STAGED_OK) {
@@ -1503,9 +1536,18 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         }
         if (bulk) {
           fence_proxy_async_smem();  // this thread's shared stores -> visible to the bulk copy
-          if (zf) s.zero_seen = 1;
+          if (BULK_OK && zf) s.zero_seen = 1;
         }
-        if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3 && !DEFER) {
+        if constexpr (DEC) {
+          // hand this emission's pool element N-1 and sum of squares to the
+          // chain warp (generator.cpp:358-364, 373-375 run there)
+          if (do_emit && tid == G::OWNER) {
+            ring[2 * e] = static_cast<double>(x_last);
+            ring[2 * e + 1] = s.sum_sq;
+            st_release_cta(&s.produced, e + 1);
+          }
+        }
+        if (!G::CHAINW && !DEC && do_emit && tid == G::OWNER && WB_ABLATE != 3 && !DEFER) {
           if constexpr (BULK_OK) {
             // bulk kernels run with disable_chi2: S = sum_sq, r and scale are
             // functions of the current sum_sq alone, nothing in the launch
@@ -1524,7 +1566,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         // before this barrier releases that buffer for overwriting
         if (bulk_pending && tid == 0) bulk_wait_read();
         bulk_pending = false;
-        __syncthreads();
+        loop_bar<DEC, LT>();
         cur_off ^= PFLIP;
         sh = bulk ? sigma * uint32_t(sizeof(T)) : 0u;
         T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
@@ -1581,10 +1623,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             a.def_marks[pool * a.def_stride + a.def_e0 + e] = m ? 1 : 0;
           }
         }
-        if (BULK_OK && bulk) {
+        if (RAWB && bulk) {
           // the aligned middle [delta, delta + L) in one copy; the <= VEC-1
           // head values [0, delta) and tail values [delta + L, N-1) as
-          // scalar stores of x*1 + 0
+          // scalar stores of x*1 + 0 (DEC: x, scaled by rescale_kernel)
           constexpr uint32_t NE = N - 1;
           const uint32_t L = ((NE - delta) / G::VEC) * G::VEC;
           if (tid == 0) {
@@ -1594,10 +1636,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           } else if (uint32_t(tid) <= NE - L) {
             const uint32_t t = tid - 1;
             const uint32_t i = t < delta ? t : L + t;
-            stg1(gbase + i, fma_rn(cur[i], T(1), T(0)));
+            stg1(gbase + i, DEC ? cur[i] : fma_rn(cur[i], T(1), T(0)));
           }
           bulk_pending = true;
-          if (s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk copy landed
+          if (BULK_OK && s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk copy landed
             if (tid == 0) {
               bulk_wait_all();
               fence_proxy_async_global();
@@ -1612,10 +1654,10 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
         }
         if (renorm_now) {
           if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
-          renormalize<T, N, THREADS, G::LAT>(cur, s, tid);
+          renormalize<T, N, LT, G::LAT, DEC>(cur, s, tid);
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
-          if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
-          __syncthreads();
+          if (!DEC && tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
+          loop_bar<DEC, LT>();
         }
         if (emit_pass && !fast) {
           // slow emission from shared memory: the partial last emission, an
@@ -1631,8 +1673,8 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
           const T sc = from_double<T>(s.scale[slot]);
           double ds = 0.0;
           bool dm = false;
-          for (uint32_t i = tid; i < limit; i += THREADS) {
-            const T v = emit_value(cur[i], sc, mean_t, mean_zero);
+          for (uint32_t i = tid; i < limit; i += LT) {
+            const T v = DEC ? cur[i] : emit_value(cur[i], sc, mean_t, mean_zero);
             if constexpr (MODE == kModeConsume) {
               cons.add(v);
             } else if constexpr (MODE == kModeDefect) {
@@ -1653,7 +1695,11 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
             }
             __syncthreads();
           }
-          if (tid == 0) {
+          if (DEC && tid == 0) {
+            ring[2 * e] = static_cast<double>(cur[N - 1]);
+            ring[2 * e + 1] = s.sum_sq;
+            st_release_cta(&s.produced, e + 1);
+          } else if (tid == 0) {
             chain_close(s, slot, static_cast<double>(cur[N - 1]));
             if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
             s.ready = e + 1;
@@ -1668,7 +1714,7 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
               a.def_marks[pool * a.def_stride + a.def_e0 + e] = m ? 1 : 0;
             }
           }
-          __syncthreads();
+          loop_bar<DEC, LT>();
         }
         pc = (pc + 1) & 255u;
       }
@@ -1683,6 +1729,47 @@ __global__ void __launch_bounds__(Geo<T, LOG2N>::THREADS, Geo<T, LOG2N>::MINB)
       }
     }
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
+    if constexpr (DEC) {
+      // the chain warp never ran the passes: the epilogue uses the compute
+      // threads' final buffer
+      if (tid == 0) {
+        s.end_off = cur_off;
+        s.end_sh = sh;
+      }
+      // the chain warp (lane 0): the per-emission recurrence of refill_
+      // (generator.cpp:358-364, 373-375; chi2.cpp:27-59), one emission
+      // behind the passes at most; its scales go to rescale_kernel
+      if (!compute && lane == 0) {
+        double reserved = s.reserved_prev, lS = s.last_chi2, lr = s.last_r, lsc = s.last_scale;
+        uint32_t clamp = 0, flags = 0;
+        double* const scl = a.scales + pool * a.scale_stride;
+        for (uint32_t e = 0; e < a.n_emit; ++e) {
+          // S_e depends on the previous emission only: drawn while waiting
+          const double S0 = a.chi2.disable ? 0.0 : chi2_draw(reserved, a.chi2, clamp, flags);
+          while (ld_acquire_cta(&s.produced) <= e) __nanosleep(20);
+          const double xl = ring[2 * e], ss = ring[2 * e + 1];
+          // disable_chi2: S is the sum of squares refill_ sees (after a
+          // renormalisation, the new one: chain_rescale)
+          const double S = a.chi2.disable ? ss : S0;
+          const double r = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(S, ss)) : 0.0;
+          const double sc = __dmul_rn(a.sigma, r);
+          scl[e] = sc;
+          reserved = __dmul_rn(xl, r);
+          lS = S;
+          lr = r;
+          lsc = sc;
+        }
+        s.reserved_prev = reserved;
+        s.last_chi2 = lS;
+        s.last_r = lr;
+        s.last_scale = lsc;
+        s.clamp = clamp;
+        s.flags |= flags;
+      }
+      __syncthreads();  // the chain's state precedes the epilogue
+      cur_off = s.end_off;
+      sh = s.end_sh;
+    }
     if (STAGED_OK && lane == 0) bulk_wait_all();
     if (DEFER) __syncthreads();  // the owner's last chain precedes the epilogue
     if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
@@ -1751,7 +1838,9 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
   using SM = Smem<T, LOG2N>;
   constexpr size_t PW = PT >= 2 ? 2 : 1;
   const size_t plans = (a.n_passes * 4 * PW + 15) & ~size_t(15);
-  const size_t smem = (SM::STATIC ? 0 : size_t(SM::TOTAL)) + plans;
+  const size_t ring = MODE == kModeFillLat ? 16 * size_t(a.n_emit) : 0;
+  if (MODE == kModeFillLat && a.n_emit > kLatRingMax) return cudaErrorInvalidValue;
+  const size_t smem = (SM::STATIC ? 0 : size_t(SM::TOTAL)) + plans + ring;
   auto fn = pool_kernel<T, LOG2N, MODE, PT>;
   static bool configured = false;  // per instantiation
   if (!configured) {
@@ -1759,11 +1848,12 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
                                          cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(SM::STATIC ? 16 * 1024 : SM::TOTAL + 16 * 1024));
+                               int((SM::STATIC ? 16 * 1024 : SM::TOTAL + 16 * 1024) +
+                                   (MODE == kModeFillLat ? 16 * kLatRingMax : 0)));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  fn<<<dim3(unsigned(n_pools)), dim3(Geo<T, LOG2N>::THREADS), smem, stream>>>(a);
+  fn<<<dim3(unsigned(n_pools)), dim3(kernel_threads<T, LOG2N, MODE>()), smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -1775,6 +1865,11 @@ cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream
       // the host selects it for the throughput geometry and wallace4 only
       if constexpr (LOG2N < 16 && LOG2N >= 7 && PT < 2 && !Geo<T, LOG2N>::INPLACE)
         return launch_pool_mode<T, LOG2N, kModeFillBulk, PT>(a, n_pools, stream);
+      else
+        return cudaErrorInvalidValue;
+    case kModeFillLat:
+      if constexpr (LOG2N >= 16 + 7 && PT < 2 && Geo<T, LOG2N>::CT <= 512 && !Geo<T, LOG2N>::CHAINW)
+        return launch_pool_mode<T, LOG2N, kModeFillLat, PT>(a, n_pools, stream);
       else
         return cudaErrorInvalidValue;
     case kModeFillStaged:
