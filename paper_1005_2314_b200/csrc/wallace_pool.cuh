@@ -612,6 +612,22 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
       stg_vec(p, v);
     }
   };
+  // a 4-value block as VEC-wide stores; fp64 into shared memory: the two
+  // 16-byte halves at a 32-byte lane stride would hit each bank twice per
+  // 8-lane phase, so lanes with bit 2 set store the upper half first
+  // (lanes l and l+4 then cover complementary banks, as in run_pass)
+  auto put_block = [&](T* p, const T* w) {
+    if constexpr (VEC == 2 && (SMD || STAGED)) {
+      const bool sw = (lane & 4) != 0;
+      const T fa[2] = {sw ? w[2] : w[0], sw ? w[3] : w[1]};
+      const T fb[2] = {sw ? w[0] : w[2], sw ? w[1] : w[3]};
+      put_vec(p + (sw ? 2 : 0), fa);
+      put_vec(p + (sw ? 0 : 2), fb);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; v += VEC) put_vec(p + v, w + v);
+    }
+  };
   auto put1 = [&](T* p, T v) {
     if constexpr (SMD) *p = v;
     else if constexpr (STAGED) stg1(g1 + (p - gbase), v);
@@ -694,7 +710,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
           });
         } else {
 #pragma unroll
-          for (int v = 0; v < 4; v += VEC) put_vec(gbase + 4 * b + v, y + v);
+          put_block(gbase + 4 * b, y);
         }
       } else {
         put1(gbase + 4 * b + 0, y[0]);
@@ -719,7 +735,7 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
         } else {
           const uint32_t cb = l31 ? b - 32 : b;
 #pragma unroll
-          for (int v = 0; v < 4; v += VEC) put_vec(gbase + 4 * cb + DELTA + v, c + v);
+          put_block(gbase + 4 * cb + DELTA, c);
         }
       }
       if (j == jfirst && lane == 0) {  // head of this warp's first block
