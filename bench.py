@@ -302,6 +302,13 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": alg_bytes,
                     "store_only_peak": store_gbs, "frac_of_store_only_peak": achieved / store_gbs}
 
+    if consume:
+        # the consumer kernel's own device time (the step also waits for the
+        # 2 KB result on the host, which adds host jitter to ms_per_step)
+        roofline = {"bound": "smem+issue (no output written)", "kernel": "pool_kernel (consume)",
+                    "kernel_ms": per_launch_ms, "launches_per_step": launches_per_step,
+                    "variates_per_s_kernel": variates_rank / launches_per_step / (per_launch_ms / 1e3)}
+
     # end to end through the C-ABI into pinned host memory
     e2e = None
     if rank == 0 and consume and not args.no_e2e:

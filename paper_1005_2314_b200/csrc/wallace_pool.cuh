@@ -1238,27 +1238,36 @@ __device__ __forceinline__ void run_pass_rot(const char* base, uint32_t cur_off,
 
 // Emission of the values already in registers (fast path) into the fused
 // consumer instead of memory.
-template <typename T, int LOG2N, int JCL>
-__device__ __forceinline__ void consume_chunk(const T (&X)[JCL][4], Consumer<T>& cons, T sc, T mean,
-                                              bool mz, uint32_t b0c) {
+// (MZ is a template parameter: with a runtime flag the compiler evaluates
+// both forms of emit_value for every value)
+template <typename T, int LOG2N, int JCL, bool MZ>
+__device__ __forceinline__ void consume_chunk_mz(const T (&X)[JCL][4], Consumer<T>& cons, T sc, T mean,
+                                                 uint32_t b0c) {
   using G = Geo<T, LOG2N>;
 #pragma unroll
   for (int j = 0; j < JCL; ++j) {
     const uint32_t b = b0c + 32 * j;
     T y[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean, mz);
+    for (int k = 0; k < 4; ++k) y[k] = emit_value(X[j][k], sc, mean, MZ);
     cons.add_group(y, b == G::ROWS - 1 ? 3 : 4);
   }
+}
+template <typename T, int LOG2N, int JCL>
+__device__ __forceinline__ void consume_chunk(const T (&X)[JCL][4], Consumer<T>& cons, T sc, T mean,
+                                              bool mz, uint32_t b0c) {
+  if (mz) consume_chunk_mz<T, LOG2N, JCL, true>(X, cons, sc, mean, b0c);
+  else consume_chunk_mz<T, LOG2N, JCL, false>(X, cons, sc, mean, b0c);
 }
 
 // Defect-suite consumer of one chunk (stats.cpp:340-369 pool_sum_squares_test,
 // :424-447 rare_event_adjacency): the fp64 sum of squares of this thread's
 // emitted (standardized) values and whether any |v| exceeds the threshold.
 // Element N-1 is the reserved value, not emitted.
-template <typename T, int LOG2N, int JCL>
-__device__ __forceinline__ void defect_chunk(const T (&X)[JCL][4], double& dsum, bool& mark, T sc, T mean,
-                                             bool mz, uint32_t b0c, double thr) {
+template <typename T, int LOG2N, int JCL, bool MZ>
+__device__ __forceinline__ void defect_chunk_mz(const T (&X)[JCL][4], double& dsum, bool& mark, T sc, T mean,
+                                                uint32_t b0c, double thr) {
+  constexpr bool mz = MZ;
   using G = Geo<T, LOG2N>;
   // four independent accumulators (one per block slot) keep the fp64 add
   // chain short; the order is a tree anyway (reference: sequential)
@@ -1275,6 +1284,12 @@ __device__ __forceinline__ void defect_chunk(const T (&X)[JCL][4], double& dsum,
     }
   }
   dsum = __dadd_rn(dsum, __dadd_rn(__dadd_rn(d4[0], d4[1]), __dadd_rn(d4[2], d4[3])));
+}
+template <typename T, int LOG2N, int JCL>
+__device__ __forceinline__ void defect_chunk(const T (&X)[JCL][4], double& dsum, bool& mark, T sc, T mean,
+                                             bool mz, uint32_t b0c, double thr) {
+  if (mz) defect_chunk_mz<T, LOG2N, JCL, true>(X, dsum, mark, sc, mean, b0c, thr);
+  else defect_chunk_mz<T, LOG2N, JCL, false>(X, dsum, mark, sc, mean, b0c, thr);
 }
 __device__ __forceinline__ double warp_sum_f64(double v) {
 #pragma unroll

@@ -23,7 +23,9 @@ for lib in libs:
         try:
             d = json.loads(r.stdout.strip().splitlines()[-1])
             frac = (d.get("roofline") or {}).get("frac")
+            kms = (d.get("roofline") or {}).get("kernel_ms")
             print(f"{name:24s} cfg{c} parity={'ok' if ok else 'FAIL'} ms={d['ms_per_step']:.3f} "
+                  f"kernel_ms={kms if kms is None else round(kms, 3)} "
                   f"frac={frac if frac is None else round(frac, 3)} sm_mhz={d['clocks']['sm_mhz']}",
                   flush=True)
         except Exception:  # noqa: BLE001
