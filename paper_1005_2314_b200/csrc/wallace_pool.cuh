@@ -155,6 +155,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_DEFER_F64
 #define WB_DEFER_F64 1
 #endif
+// 1: the consumer kernel's register budget follows its shared-memory limit
+#ifndef WB_CONS_REGS
+#define WB_CONS_REGS 1
+#endif
 #ifndef WB_HS_LUT
 #define WB_HS_LUT 1
 #endif
@@ -1302,11 +1306,27 @@ template <typename T, int LOG2N, int MODE>
 constexpr int kernel_threads() {
   return Geo<T, LOG2N>::THREADS + (MODE == kModeFillLat ? 32 : 0);
 }
+// Resident CTAs per SM the kernel is compiled for (its register budget).
+// The consumer kernel keeps 258 histogram bins and no output path: its CTAs
+// are limited by shared memory only, so it may use the registers that leaves.
+template <typename T, int LOG2N, int MODE>
+constexpr int kernel_minb() {
+  using G = Geo<T, LOG2N>;
+  if constexpr (MODE == kModeConsume && !G::LAT && WB_CONS_REGS) {
+    constexpr int per_cta = G::BUFS * G::N * int(sizeof(T)) + 4096;
+    constexpr int by_smem = (220 * 1024) / per_cta;
+    constexpr int by_threads = 2048 / G::THREADS;
+    constexpr int m = by_smem < by_threads ? by_smem : by_threads;
+    return m < 1 ? 1 : m;
+  } else {
+    return G::MINB;
+  }
+}
 // kModeFillLat ring: (x_last, sum_sq) of every emission of a launch
 constexpr uint32_t kLatRingMax = 2048;
 
 template <typename T, int LOG2N, int MODE, int PT>
-__global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), Geo<T, LOG2N>::MINB)
+__global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<T, LOG2N, MODE>())
     pool_kernel(const __grid_constant__ FillArgs a) {
   using G = Geo<T, LOG2N>;
   using SM = Smem<T, LOG2N>;
