@@ -66,10 +66,11 @@ enum Mode : int32_t {
                      // emission pass's barrier the scaled values are staged
                      // in the dead source buffer and each warp sends its
                      // segment with one bulk copy
-  kModeFillLat = 6,  // emit into the caller's buffer, latency geometry: the
-                     // passes emit raw pool values (bulk copies), a chain
-                     // warp runs the per-emission chi2/scale recurrence off
-                     // the passes' critical path, rescale_kernel applies it
+  kModeFillLat = 6,  // emit into the caller's buffer, latency geometry: each
+                     // emission's raw pool goes to a pitched row by one bulk
+                     // copy, a chain warp runs the per-emission chi2/scale
+                     // recurrence off the passes' critical path, and
+                     // rescale_kernel writes x*scale+mean to the output
 };
 
 struct FillArgs {
@@ -124,9 +125,13 @@ struct FillArgs {
   double* lg_aux;         // per pool: consumer totals, defect mark, probe x, block partials
   uint64_t lg_aux_stride; // doubles per pool
   uint64_t lg_npools;     // pools of the launch (pool index = blockIdx.y + 65535 * blockIdx.z)
-  // kModeFillLat: per-emission scale of each pool, [n_pools][scale_stride]
+  // kModeFillLat: per-emission scale of each pool, [n_pools][scale_stride],
+  // and the raw emissions, one pitched row of N values per emission:
+  // [n_pools][lat_rows][N]
   double* scales;
   uint64_t scale_stride;
+  void* lat_raw;
+  uint64_t lat_rows;
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]

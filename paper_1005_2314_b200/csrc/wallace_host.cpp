@@ -226,6 +226,8 @@ struct wallace_handle {
   bool staged_ok = false;  // other fills may use the staged-emission kernel
   bool lat_fill_ok = false;  // latency-geometry fills may decouple the chi2 chain (kModeFillLat)
   double* d_scales = nullptr;  // kModeFillLat: [n_pools][plan_cap] per-emission scales
+  void* d_lat_raw = nullptr;   // kModeFillLat: [n_pools][lat_rows][N] raw emissions
+  uint64_t lat_rows = 0;       // kModeFillLat: emissions per launch
   // pools above the on-chip limit: HBM-resident executor (wallace_large.cu)
   bool large = false;
   void* d_lg_pool2 = nullptr;
@@ -531,10 +533,20 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     else if (mode == wb::kModeFill && h->staged_ok && h->key < 16 && h->log2n >= 7)
       a.mode = wb::kModeFillStaged;
     else if (mode == wb::kModeFill && h->lat_fill_ok && h->key >= 16 && h->key < 64) {
-      if (!h->d_scales) WB_CUDA(cudaMalloc(&h->d_scales, h->n_pools * size_t(h->plan_cap) * sizeof(double)));
+      if (!h->d_scales) {
+        // one pitched row of N raw values per emission of a launch, at most
+        // 256 MiB for the handle
+        const uint64_t row_bytes = h->n_pools * h->N * h->esize;
+        h->lat_rows = std::max<uint64_t>(1, std::min<uint64_t>(h->plan_cap / std::max<uint64_t>(1, d),
+                                                                (256ull << 20) / row_bytes));
+        WB_CUDA(cudaMalloc(&h->d_scales, h->n_pools * size_t(h->plan_cap) * sizeof(double)));
+        WB_CUDA(cudaMalloc(&h->d_lat_raw, h->lat_rows * row_bytes));
+      }
       a.mode = wb::kModeFillLat;
       a.scales = h->d_scales;
       a.scale_stride = h->plan_cap;
+      a.lat_raw = h->d_lat_raw;
+      a.lat_rows = h->lat_rows;
     }
     if (mode == wb::kModeDefect) a.def_e0 = produced / (h->N - 1);  // defect runs start at an emission
     a.out = out;
@@ -554,6 +566,7 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     if (e_total > 0) {
       if (d <= h->plan_cap) {
         e = std::min<uint64_t>(e_total, h->plan_cap / d);
+        if (a.mode == wb::kModeFillLat) e = std::min<uint64_t>(e, h->lat_rows);
         passes = e * d;
       } else {
         // an emission longer than one launch: run d-1 passes first, then a
@@ -845,6 +858,7 @@ wallace_status wallace_destroy(wallace_handle* h) {
   }
   cudaFree(h->d_leftover);
   cudaFree(h->d_scales);
+  cudaFree(h->d_lat_raw);
   cudaFree(h->d_snap_pools);
   cudaFree(h->d_snap_state);
   cudaFree(h->d_snap_leftover);

@@ -221,24 +221,25 @@ __global__ void materialize_kernel(const T* pools, PoolState* st, T* leftover, u
   if (threadIdx.x == 0) st[pool].flags |= kFlagLeftover;
 }
 
-// kModeFillLat epilogue: the passes emitted raw pool values; apply each
-// emission's scale and the mean (generator.cpp:366-368, the same rounding as
-// emit_value in pool_kernel).  Emission e of pool p covers elements
-// [lead + e*(N-1), lead + (e+1)*(N-1)) of the launch's slice (the last one
-// last_limit values).  blockIdx.y = pool.
-template <typename T>
+// kModeFillLat epilogue: the passes sent each emission's raw pool to a
+// pitched row; write x*scale + mean of its first N-1 values to the output
+// (generator.cpp:366-368, the same rounding as emit_value in pool_kernel).
+// Emission e of pool p covers elements [lead + e*(N-1), lead + (e+1)*(N-1))
+// of the launch's slice (the last one last_limit values).  blockIdx.y = pool.
+template <typename T, bool MZ>
 __global__ void __launch_bounds__(256) rescale_kernel(const FillArgs a, uint32_t N) {
   const uint64_t pool = blockIdx.y;
   const uint64_t n1 = N - 1;
   const uint64_t count = a.n_emit ? (a.n_emit - 1) * n1 + a.last_limit : 0;
   T* const out = static_cast<T*>(a.out) + pool * a.out_stride + a.out_offset + a.lead;
+  const T* const raw = static_cast<const T*>(a.lat_raw) + pool * a.lat_rows * N;
   const double* const scl = a.scales + pool * a.scale_stride;
   const T mean = from_double<T>(a.mean);
-  const bool mz = a.mean_is_zero != 0;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t e = static_cast<uint32_t>(i / n1);
-    out[i] = emit_value(out[i], from_double<T>(scl[e]), mean, mz);
+    const uint64_t k = i - e * n1;
+    out[i] = emit_value(__ldcs(raw + e * uint64_t(N) + k), from_double<T>(scl[e]), mean, MZ);
   }
 }
 
@@ -247,8 +248,13 @@ cudaError_t launch_rescale(int dtype, const FillArgs& a, uint32_t N, uint64_t n_
   if (count == 0) return cudaSuccess;
   const unsigned bx = unsigned(std::min<uint64_t>(1024, (count + 1023) / 1024));
   const dim3 grid(bx, unsigned(n_pools));
-  if (dtype == 0) rescale_kernel<float><<<grid, 256, 0, s>>>(a, N);
-  else rescale_kernel<double><<<grid, 256, 0, s>>>(a, N);
+  if (dtype == 0) {
+    if (a.mean_is_zero) rescale_kernel<float, true><<<grid, 256, 0, s>>>(a, N);
+    else rescale_kernel<float, false><<<grid, 256, 0, s>>>(a, N);
+  } else {
+    if (a.mean_is_zero) rescale_kernel<double, true><<<grid, 256, 0, s>>>(a, N);
+    else rescale_kernel<double, false><<<grid, 256, 0, s>>>(a, N);
+  }
   return cudaGetLastError();
 }
 

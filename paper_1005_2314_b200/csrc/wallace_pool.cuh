@@ -84,7 +84,7 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 // ABLATION builds only (timing experiments, wrong output): 1 = skip the
 // fast emission, 2 = skip its global stores, 3 = skip the scalar chain,
 // 7 = staged emission without the wait for the bulk copy's read, 8 = staged
-// emission without its shared stores
+// emission without its shared stores, 13 = latency fill without the chain
 #ifndef WB_ABLATE
 #define WB_ABLATE 0
 #endif
@@ -382,8 +382,7 @@ struct SState {
   double x_last_bulk;        // ... and its pool element N-1
   uint32_t ready;      // chain-warp kernels: S/r/scale of every emission <= ready published
   uint32_t produced;   // kModeFillLat: emissions whose (x_last, sum_sq) are in the ring
-  uint32_t end_off;    // kModeFillLat: the compute threads' final buffer offset and shift
-  uint32_t end_sh;
+  uint32_t end_off;    // kModeFillLat: the compute threads' final buffer offset
 };
 
 // S, r, scale of the emission in `slot` from the current reserved value.
@@ -1334,7 +1333,6 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
   constexpr bool DEC = MODE == kModeFillLat;
   static_assert(!DEC || (G::LAT && !G::CHAINW && PT < 2 && G::CT <= 512), "latency-fill geometry");
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = kernel_threads<T, LOG2N, MODE>();
-  constexpr int LT = DEC ? G::CT : THREADS;  // threads of the pass loop
   constexpr uint32_t BUF = SM::BUF;
   constexpr bool FAST = ROWS >= 32;
   // buffer 0 at offset 0, buffer 1 at BSTRIDE; plans in dynamic smem
@@ -1466,6 +1464,98 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     }
     if (probe)
       for (int k = 0; k < 6; ++k) a.probe_acc[(pool * a.n_probes + tid) * 6 + k] = pa[k];
+  } else if constexpr (DEC) {
+    // ---- latency fill (kModeFillLat): a lean pass loop for the compute
+    // warps, the chi2/scale chain in the last warp ----------------------------
+    if (compute) {
+      bool pending = false;  // thread 0's last row copy may still read its buffer
+      uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
+      for (uint32_t e = 0; e < a.n_emit; ++e) {
+        for (uint32_t q = 1; q <= a.d; ++q, ++p) {
+          const bool emit_pass = q == a.d;
+          const bool renorm_now = pc == 0;
+          const uint32_t plan_p = plan;
+          plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
+          T X[G::J][4];
+          run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
+          if (emit_pass) {
+            // the pool this pass wrote is the raw emission: one bulk copy
+            // after the barrier sends it to its pitched row
+            fence_proxy_async_smem();
+            // pool element N-1 and the sum of squares of this emission for
+            // the chain warp (generator.cpp:358-364, 373-375 run there)
+            if (!renorm_now && tid == G::OWNER) {
+              ring[2 * e] = static_cast<double>(X[G::J - 1][3]);
+              ring[2 * e + 1] = s.sum_sq;
+              st_release_cta(&s.produced, e + 1);
+            }
+          }
+          // the copy issued after the previous pass read the buffer the
+          // next pass overwrites
+          if (pending && tid == 0) bulk_wait_read();
+          pending = false;
+          loop_bar<true, G::CT>();
+          cur_off ^= FLIP;
+          T* const cur = reinterpret_cast<T*>(pbase + cur_off);
+          if (renorm_now) {
+            renormalize<T, N, G::CT, true, true>(cur, s, tid);
+            if (emit_pass) {
+              fence_proxy_async_smem();
+              loop_bar<true, G::CT>();
+            }
+          }
+          if (emit_pass && tid == 0) {
+            if (renorm_now) {  // refill_ after step_pass renormalised (generator.cpp:342, 363)
+              ring[2 * e] = static_cast<double>(cur[N - 1]);
+              ring[2 * e + 1] = s.sum_sq;
+              st_release_cta(&s.produced, e + 1);
+            }
+            T* const row = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows + e) * N;
+            bulk_s2g(row, static_cast<uint32_t>(__cvta_generic_to_shared(cur)), N * uint32_t(sizeof(T)));
+            bulk_commit();
+            pending = true;
+          }
+          pc = (pc + 1) & 255u;
+        }
+      }
+      if (tid == 0) {
+        bulk_wait_all();  // the rows are complete before rescale_kernel reads them
+        s.end_off = cur_off;
+      }
+    } else {
+      // the chain warp (lane 0): the per-emission recurrence of refill_
+      // (generator.cpp:358-364, 373-375; chi2.cpp:27-59), one emission
+      // behind the passes at most; its scales go to rescale_kernel
+      if (!compute && lane == 0) {
+        double reserved = s.reserved_prev, lS = s.last_chi2, lr = s.last_r, lsc = s.last_scale;
+        uint32_t clamp = 0, flags = 0;
+        double* const scl = a.scales + pool * a.scale_stride;
+        for (uint32_t e = 0; e < (WB_ABLATE == 13 ? 0u : a.n_emit); ++e) {
+          // S_e depends on the previous emission only: drawn while waiting
+          const double S0 = a.chi2.disable ? 0.0 : chi2_draw(reserved, a.chi2, clamp, flags);
+          while (ld_acquire_cta(&s.produced) <= e) __nanosleep(20);
+          const double xl = ring[2 * e], ss = ring[2 * e + 1];
+          // disable_chi2: S is the sum of squares refill_ sees (after a
+          // renormalisation, the new one: chain_rescale)
+          const double S = a.chi2.disable ? ss : S0;
+          const double r = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(S, ss)) : 0.0;
+          const double sc = __dmul_rn(a.sigma, r);
+          scl[e] = sc;
+          reserved = __dmul_rn(xl, r);
+          lS = S;
+          lr = r;
+          lsc = sc;
+        }
+        s.reserved_prev = reserved;
+        s.last_chi2 = lS;
+        s.last_r = lr;
+        s.last_scale = lsc;
+        s.clamp = clamp;
+        s.flags |= flags;
+      }
+    }
+    __syncthreads();  // the chain's state and the final buffer precede the epilogue
+    cur_off = s.end_off;
   } else {
     uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
     // bulk emission (see "Bulk emission") for the throughput geometry
@@ -1473,10 +1563,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     // compiled out there, which keeps the general kernel's registers)
     constexpr bool BULK_OK = MODE == kModeFillBulk;
     static_assert(!BULK_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE), "bulk geometry");
-    // raw pool values sent by one bulk copy per emission: the bulk kernel, and
-    // the latency fill (whose values rescale_kernel scales afterwards)
-    constexpr bool RAWB = BULK_OK || DEC;
-    static_assert(!DEC || FAST, "latency-fill geometry");
+    constexpr bool RAWB = BULK_OK;  // raw pool values sent by one bulk copy per emission
     bool bulk_pending = false;
     // staged emission (see "Staged emission")
     constexpr bool STAGED_OK = MODE == kModeFillStaged;
@@ -1485,8 +1572,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     bool stage_pending = false;  // this warp's last bulk copy may still read the next pass's buffer
     constexpr bool DEFER = STAGED_OK && (sizeof(T) == 4 ? WB_DEFER_F32 : WB_DEFER_F64);
     T* gbase = out_pool + a.lead;  // element 0 of the current emission
-    // (DEC: the chain warp skips the passes and runs the chain below)
-    for (uint32_t e = 0; e < ((!DEC || compute) ? a.n_emit : 0u); ++e, gbase += N - 1) {
+    for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
       const int slot = e & 1;
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
       for (uint32_t q = 1; q <= a.d; ++q, ++p) {
@@ -1589,16 +1675,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           fence_proxy_async_smem();  // this thread's shared stores -> visible to the bulk copy
           if (BULK_OK && zf) s.zero_seen = 1;
         }
-        if constexpr (DEC) {
-          // hand this emission's pool element N-1 and sum of squares to the
-          // chain warp (generator.cpp:358-364, 373-375 run there)
-          if (do_emit && tid == G::OWNER) {
-            ring[2 * e] = static_cast<double>(x_last);
-            ring[2 * e + 1] = s.sum_sq;
-            st_release_cta(&s.produced, e + 1);
-          }
-        }
-        if (!G::CHAINW && !DEC && do_emit && tid == G::OWNER && WB_ABLATE != 3 && !DEFER) {
+        if (!G::CHAINW && do_emit && tid == G::OWNER && WB_ABLATE != 3 && !DEFER) {
           if constexpr (BULK_OK) {
             // bulk kernels run with disable_chi2: S = sum_sq, r and scale are
             // functions of the current sum_sq alone, nothing in the launch
@@ -1617,7 +1694,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         // before this barrier releases that buffer for overwriting
         if (bulk_pending && tid == 0) bulk_wait_read();
         bulk_pending = false;
-        loop_bar<DEC, LT>();
+        __syncthreads();
         cur_off ^= PFLIP;
         sh = bulk ? sigma * uint32_t(sizeof(T)) : 0u;
         T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
@@ -1677,7 +1754,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         if (RAWB && bulk) {
           // the aligned middle [delta, delta + L) in one copy; the <= VEC-1
           // head values [0, delta) and tail values [delta + L, N-1) as
-          // scalar stores of x*1 + 0 (DEC: x, scaled by rescale_kernel)
+          // scalar stores of x*1 + 0
           constexpr uint32_t NE = N - 1;
           const uint32_t L = ((NE - delta) / G::VEC) * G::VEC;
           if (tid == 0) {
@@ -1687,7 +1764,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           } else if (uint32_t(tid) <= NE - L) {
             const uint32_t t = tid - 1;
             const uint32_t i = t < delta ? t : L + t;
-            stg1(gbase + i, DEC ? cur[i] : fma_rn(cur[i], T(1), T(0)));
+            stg1(gbase + i, fma_rn(cur[i], T(1), T(0)));
           }
           bulk_pending = true;
           if (BULK_OK && s.zero_seen) {  // rare: rewrite -0 as +0 once the bulk copy landed
@@ -1705,10 +1782,10 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         }
         if (renorm_now) {
           if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
-          renormalize<T, N, LT, G::LAT, DEC>(cur, s, tid);
+          renormalize<T, N, THREADS, G::LAT>(cur, s, tid);
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
-          if (!DEC && tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
-          loop_bar<DEC, LT>();
+          if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
+          __syncthreads();
         }
         if (emit_pass && !fast) {
           // slow emission from shared memory: the partial last emission, an
@@ -1724,8 +1801,8 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           const T sc = from_double<T>(s.scale[slot]);
           double ds = 0.0;
           bool dm = false;
-          for (uint32_t i = tid; i < limit; i += LT) {
-            const T v = DEC ? cur[i] : emit_value(cur[i], sc, mean_t, mean_zero);
+          for (uint32_t i = tid; i < limit; i += THREADS) {
+            const T v = emit_value(cur[i], sc, mean_t, mean_zero);
             if constexpr (MODE == kModeConsume) {
               cons.add(v);
             } else if constexpr (MODE == kModeDefect) {
@@ -1746,11 +1823,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
             }
             __syncthreads();
           }
-          if (DEC && tid == 0) {
-            ring[2 * e] = static_cast<double>(cur[N - 1]);
-            ring[2 * e + 1] = s.sum_sq;
-            st_release_cta(&s.produced, e + 1);
-          } else if (tid == 0) {
+          if (tid == 0) {
             chain_close(s, slot, static_cast<double>(cur[N - 1]));
             if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
             s.ready = e + 1;
@@ -1765,7 +1838,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
               a.def_marks[pool * a.def_stride + a.def_e0 + e] = m ? 1 : 0;
             }
           }
-          loop_bar<DEC, LT>();
+          __syncthreads();
         }
         pc = (pc + 1) & 255u;
       }
@@ -1780,47 +1853,6 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
       }
     }
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
-    if constexpr (DEC) {
-      // the chain warp never ran the passes: the epilogue uses the compute
-      // threads' final buffer
-      if (tid == 0) {
-        s.end_off = cur_off;
-        s.end_sh = sh;
-      }
-      // the chain warp (lane 0): the per-emission recurrence of refill_
-      // (generator.cpp:358-364, 373-375; chi2.cpp:27-59), one emission
-      // behind the passes at most; its scales go to rescale_kernel
-      if (!compute && lane == 0) {
-        double reserved = s.reserved_prev, lS = s.last_chi2, lr = s.last_r, lsc = s.last_scale;
-        uint32_t clamp = 0, flags = 0;
-        double* const scl = a.scales + pool * a.scale_stride;
-        for (uint32_t e = 0; e < a.n_emit; ++e) {
-          // S_e depends on the previous emission only: drawn while waiting
-          const double S0 = a.chi2.disable ? 0.0 : chi2_draw(reserved, a.chi2, clamp, flags);
-          while (ld_acquire_cta(&s.produced) <= e) __nanosleep(20);
-          const double xl = ring[2 * e], ss = ring[2 * e + 1];
-          // disable_chi2: S is the sum of squares refill_ sees (after a
-          // renormalisation, the new one: chain_rescale)
-          const double S = a.chi2.disable ? ss : S0;
-          const double r = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(S, ss)) : 0.0;
-          const double sc = __dmul_rn(a.sigma, r);
-          scl[e] = sc;
-          reserved = __dmul_rn(xl, r);
-          lS = S;
-          lr = r;
-          lsc = sc;
-        }
-        s.reserved_prev = reserved;
-        s.last_chi2 = lS;
-        s.last_r = lr;
-        s.last_scale = lsc;
-        s.clamp = clamp;
-        s.flags |= flags;
-      }
-      __syncthreads();  // the chain's state precedes the epilogue
-      cur_off = s.end_off;
-      sh = s.end_sh;
-    }
     if (STAGED_OK && lane == 0) bulk_wait_all();
     if (DEFER) __syncthreads();  // the owner's last chain precedes the epilogue
     if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
