@@ -117,6 +117,9 @@ struct FillArgs {
   void* lg_pool2;
   void* lg_state;
   uint64_t lg_stride;     // default_stride(rows) % rows
+  uint64_t lg_stride_inv; // its inverse mod rows (rows a power of two, stride odd)
+  int32_t lg_row_major;   // wallace4 stride passes: a thread per gathered row (coalesced)
+  int32_t pad_rm;
   uint64_t lg_alpha;      // default_multipliers(N)
   uint64_t lg_beta;
   uint64_t lg_pass0;

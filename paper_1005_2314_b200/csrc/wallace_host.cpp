@@ -387,6 +387,16 @@ wb::FillArgs base_args(wallace_handle* h) {
     a.lg_aux = h->d_lg_aux;
     a.lg_aux_stride = wb::large_aux_stride(h->N);
     a.lg_stride = default_stride(rows) % rows;
+    {
+      // inverse of the (odd) stride mod 2^64 by Newton's iteration, then mod rows
+      uint64_t inv = a.lg_stride;
+      for (int k = 0; k < 6; ++k) inv *= 2 - a.lg_stride * inv;
+      a.lg_stride_inv = inv & (rows - 1);
+    }
+    {
+      const char* bm = std::getenv("WALLACE_B200_LG_BLOCKMAJOR");
+      a.lg_row_major = (bm && bm[0] == '1') ? 0 : 1;
+    }
     a.lg_alpha = al;
     a.lg_beta = be;
     a.lg_log2n = h->log2n;

@@ -117,6 +117,48 @@ __global__ void lg_pass_wallace(const FillArgs a, const T* in, T* out, uint32_t 
   if (emit_slot >= 0) lg_emit4(a, pool, 4 * b, x, emit_slot, gofs, limit);
 }
 
+// The same pass with a thread per gathered *row*: row r holds elements
+// r, r+rows, r+2rows, r+3rows, the inputs of the 4-block b whose row is
+// r = (off + b*stride) mod rows, i.e. b = (r - off) * stride^-1 mod rows.
+// Consecutive threads then load consecutive addresses (every sector fully
+// used, against one 4-byte value per 32-byte sector for a thread per block),
+// and each thread stores its block as one 16-byte vector.  Same arithmetic,
+// same results.
+template <typename T>
+__global__ void lg_pass_wallace_rows(const FillArgs a, const T* in, T* out, uint32_t p, uint64_t N,
+                                     int emit_slot, uint64_t gofs, uint32_t limit) {
+  const uint64_t pool = lg_pool_index();
+  if (pool >= a.lg_npools) return;
+  const uint64_t rows = N / 4;
+  const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const uint32_t* w = plan_at(a, pool, p, 2);
+  const uint64_t off = w[0];
+  const uint32_t variant = w[1];
+  const T* src = in + pool * N;
+  T v[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = src[c * rows + r];
+  const uint64_t b = ((r - off) * a.lg_stride_inv) & (rows - 1);
+  const T aa = add_rn(v[0], v[1]), bb = sub_rn(v[0], v[1]), cc = add_rn(v[2], v[3]), dd = sub_rn(v[2], v[3]);
+  const T z[4] = {sub_rn(aa, dd), add_rn(bb, cc), sub_rn(bb, cc), sub_rn(-aa, dd)};
+  const int perm = int(variant >> 4);
+  T x[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const T h = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+    x[k] = mul_rn(h, z[perm_at(perm, k)]);
+  }
+  T* dst = out + pool * N + 4 * b;
+  if constexpr (sizeof(T) == 4) {
+    *reinterpret_cast<float4*>(dst) = make_float4(x[0], x[1], x[2], x[3]);
+  } else {
+    reinterpret_cast<double2*>(dst)[0] = make_double2(x[0], x[1]);
+    reinterpret_cast<double2*>(dst)[1] = make_double2(x[2], x[3]);
+  }
+  if (emit_slot >= 0) lg_emit4(a, pool, 4 * b, x, emit_slot, gofs, limit);
+}
+
 // One rotation half-sweep (generator.cpp:113-172), a thread per 4-block of
 // the output; sweep 1 gathers the block's neighbours g[4b-1], g[4b+4] too.
 template <typename T, int MIX, int SWEEP>
@@ -439,7 +481,10 @@ cudaError_t run_large(const FillArgs& args, uint64_t n_pools, cudaStream_t st) {
   // one pass; emit_slot >= 0 fuses the emission (values i < limit at gofs)
   auto pass = [&](uint32_t p, int es = -1, uint64_t go = 0, uint32_t lim = 0) {
     if (!rot) {
-      if (pt == 0) lg_pass_wallace<T, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, es, go, lim);
+      if (pt == 0 && a.lg_row_major)
+        lg_pass_wallace_rows<T><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, es, go, lim);
+      else if (pt == 0)
+        lg_pass_wallace<T, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, es, go, lim);
       else lg_pass_wallace<T, 1><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, es, go, lim);
     } else if (pt == 2) {
       lg_pass_rotation<T, 0, 0><<<grid_rows, kLgThreads, 0, st>>>(a, w[cur], w[cur ^ 1], p, N, -1, 0, 0);
