@@ -134,6 +134,9 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_REGS_PP
 #define WB_REGS_PP 80
 #endif
+#ifndef WB_REGS_PP_F64
+#define WB_REGS_PP_F64 WB_REGS_PP
+#endif
 #ifndef WB_J_F32
 #define WB_J_F32 8
 #endif
@@ -201,7 +204,7 @@ struct Geo {
   static constexpr int SMEM_PER_CTA = BUFS * N * sizeof(T) + 2048;
   static constexpr int MINB_RAW = (220 * 1024) / SMEM_PER_CTA;
   static constexpr int MINB_SMEM = MINB_RAW < 1 ? 1 : (MINB_RAW * THREADS > 2048 ? 2048 / THREADS : MINB_RAW);
-  static constexpr int REG_BUDGET = INPLACE ? WB_REGS_INPLACE : WB_REGS_PP;
+  static constexpr int REG_BUDGET = INPLACE ? WB_REGS_INPLACE : (sizeof(T) == 8 ? WB_REGS_PP_F64 : WB_REGS_PP);
   static constexpr int MINB_REGS = 65536 / (THREADS * REG_BUDGET) < 1 ? 1 : 65536 / (THREADS * REG_BUDGET);
   static constexpr int MINB = LAT ? 1 : (MINB_SMEM < MINB_REGS ? MINB_SMEM : MINB_REGS);
   // affine mixing multipliers (generator.cpp:286-294 default_multipliers);
@@ -1329,7 +1332,8 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     pool_kernel(const __grid_constant__ FillArgs a) {
   using G = Geo<T, LOG2N>;
   using SM = Smem<T, LOG2N>;
-  // DEC (kModeFillLat): decoupled chain warp (tid >= CT), see "Latency fills"
+  // DEC (kModeFillLat): lean pass loop + decoupled chain warp (tid >= CT),
+  // DESIGN.md §5 "Latency fills"
   constexpr bool DEC = MODE == kModeFillLat;
   static_assert(!DEC || (G::LAT && !G::CHAINW && PT < 2 && G::CT <= 512), "latency-fill geometry");
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = kernel_threads<T, LOG2N, MODE>();
@@ -1558,14 +1562,14 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     cur_off = s.end_off;
   } else {
     uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
-    // bulk emission (see "Bulk emission") for the throughput geometry
-    // bulk emission (its own instantiation: the register emission path is
-    // compiled out there, which keeps the general kernel's registers)
+    // bulk emission (see "Bulk emission" above; its own instantiation: the
+    // register emission path is compiled out there, which keeps the general
+    // kernel's registers)
     constexpr bool BULK_OK = MODE == kModeFillBulk;
     static_assert(!BULK_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE), "bulk geometry");
     constexpr bool RAWB = BULK_OK;  // raw pool values sent by one bulk copy per emission
     bool bulk_pending = false;
-    // staged emission (see "Staged emission")
+    // staged emission (stage_chunk_any / staged_range above)
     constexpr bool STAGED_OK = MODE == kModeFillStaged;
     static_assert(!STAGED_OK || (FAST && !G::LAT && !ROT && !G::CHAINW && !G::INPLACE && G::JC == G::J),
                   "staged geometry");
