@@ -162,6 +162,10 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_CONS_REGS
 #define WB_CONS_REGS 1
 #endif
+// at least this many 4-blocks per thread in the latency kernels
+#ifndef WB_LAT_J
+#define WB_LAT_J 1
+#endif
 #ifndef WB_HS_LUT
 #define WB_HS_LUT 1
 #endif
@@ -177,8 +181,8 @@ struct Geo {
   static constexpr int ROWS = N / 4;
   // groups (4-blocks) per thread: enough independent gathers per thread to
   // hide LDS latency, few enough warps per pool for cheap barriers.
-  static constexpr int JWANT = LAT ? (ROWS > (WB_CHAINW ? 512 : 1024) ? ROWS / (WB_CHAINW ? 512 : 1024) : 1)
-                                   : (sizeof(T) == 4 ? WB_J_F32 : WB_J_F64);
+  static constexpr int JLAT = ROWS > (WB_CHAINW ? 512 : 1024) ? ROWS / (WB_CHAINW ? 512 : 1024) : 1;
+  static constexpr int JWANT = LAT ? (JLAT > WB_LAT_J ? JLAT : WB_LAT_J) : (sizeof(T) == 4 ? WB_J_F32 : WB_J_F64);
   static constexpr int J = (ROWS >= 32 * JWANT) ? JWANT : (ROWS >= 32 ? ROWS / 32 : 1);
   static constexpr int JCWANT = LAT ? J : (sizeof(T) == 4 ? WB_JC_F32 : WB_JC_F64);
   static constexpr int JC = J < JCWANT ? J : JCWANT;
