@@ -162,6 +162,12 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_CONS_REGS
 #define WB_CONS_REGS 1
 #endif
+// latency fills: 1 = each thread stores its 4-blocks of the emission pass to
+// the pitched row from registers (no bulk copy, no read wait on the next
+// pass); 0 = one cp.async.bulk of the pool per emission
+#ifndef WB_LAT_STG
+#define WB_LAT_STG 1
+#endif
 // at least this many 4-blocks per thread in the latency kernels
 #ifndef WB_LAT_J
 #define WB_LAT_J 1
@@ -1486,10 +1492,21 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
           T X[G::J][4];
           run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
+          T* const row = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows + e) * N;
+          if (WB_LAT_STG && emit_pass && !renorm_now) {
+            // the pool this pass wrote is the raw emission: each thread's
+            // 4-blocks go to the pitched row straight from registers
+#pragma unroll
+            for (int j = 0; j < G::J; ++j) {
+              T* const d = row + 4 * (b0 + 32 * j);
+              stg_vec(d, X[j]);
+              if constexpr (sizeof(T) == 8) stg_vec(d + 2, X[j] + 2);
+            }
+          }
           if (emit_pass) {
-            // the pool this pass wrote is the raw emission: one bulk copy
-            // after the barrier sends it to its pitched row
-            fence_proxy_async_smem();
+            // WB_LAT_STG 0: the pool this pass wrote is the raw emission, one
+            // bulk copy after the barrier sends it to its pitched row
+            if (!WB_LAT_STG) fence_proxy_async_smem();
             // pool element N-1 and the sum of squares of this emission for
             // the chain warp (generator.cpp:358-364, 373-375 run there)
             if (!renorm_now && tid == G::OWNER) {
@@ -1507,18 +1524,28 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           T* const cur = reinterpret_cast<T*>(pbase + cur_off);
           if (renorm_now) {
             renormalize<T, N, G::CT, true, true>(cur, s, tid);
-            if (emit_pass) {
+            if (WB_LAT_STG && emit_pass) {
+              // renormalised emission: each thread's own 4-blocks, from the
+              // pool (renormalize ends on a barrier)
+#pragma unroll
+              for (int j = 0; j < G::J; ++j) {
+                const T* const v = cur + 4 * (b0 + 32 * j);
+                T* const d = row + 4 * (b0 + 32 * j);
+                stg_vec(d, v);
+                if constexpr (sizeof(T) == 8) stg_vec(d + 2, v + 2);
+              }
+            } else if (emit_pass) {
               fence_proxy_async_smem();
               loop_bar<true, G::CT>();
             }
           }
-          if (emit_pass && tid == 0) {
-            if (renorm_now) {  // refill_ after step_pass renormalised (generator.cpp:342, 363)
-              ring[2 * e] = static_cast<double>(cur[N - 1]);
-              ring[2 * e + 1] = s.sum_sq;
-              st_release_cta(&s.produced, e + 1);
-            }
-            T* const row = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows + e) * N;
+          if (emit_pass && tid == 0 && renorm_now) {
+            // refill_ after step_pass renormalised (generator.cpp:342, 363)
+            ring[2 * e] = static_cast<double>(cur[N - 1]);
+            ring[2 * e + 1] = s.sum_sq;
+            st_release_cta(&s.produced, e + 1);
+          }
+          if (!WB_LAT_STG && emit_pass && tid == 0) {
             bulk_s2g(row, static_cast<uint32_t>(__cvta_generic_to_shared(cur)), N * uint32_t(sizeof(T)));
             bulk_commit();
             pending = true;
@@ -1527,7 +1554,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         }
       }
       if (tid == 0) {
-        bulk_wait_all();  // the rows are complete before rescale_kernel reads them
+        if (!WB_LAT_STG) bulk_wait_all();  // the rows are complete before rescale_kernel reads them
         s.end_off = cur_off;
       }
     } else {
