@@ -725,7 +725,6 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
             if (decltype(jjc)::value == jj) store_group(jjc, y);
           });
         } else {
-#pragma unroll
           put_block(gbase + 4 * b, y);
         }
       } else {
@@ -750,7 +749,6 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
           });
         } else {
           const uint32_t cb = l31 ? b - 32 : b;
-#pragma unroll
           put_block(gbase + 4 * cb + DELTA, c);
         }
       }
@@ -1328,7 +1326,8 @@ constexpr int kernel_minb() {
     constexpr int per_cta = G::BUFS * G::N * int(sizeof(T)) + 4096;
     constexpr int by_smem = (220 * 1024) / per_cta;
     constexpr int by_threads = 2048 / G::THREADS;
-    constexpr int m = by_smem < by_threads ? by_smem : by_threads;
+    constexpr int m0 = by_smem < by_threads ? by_smem : by_threads;
+    constexpr int m = m0 > 32 ? 32 : m0;  // at most 32 resident CTAs per SM
     return m < 1 ? 1 : m;
   } else {
     return G::MINB;
@@ -1347,7 +1346,6 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
   constexpr bool DEC = MODE == kModeFillLat;
   static_assert(!DEC || (G::LAT && !G::CHAINW && PT < 2 && G::CT <= 512), "latency-fill geometry");
   constexpr int N = G::N, ROWS = G::ROWS, J = G::J, THREADS = kernel_threads<T, LOG2N, MODE>();
-  constexpr uint32_t BUF = SM::BUF;
   constexpr bool FAST = ROWS >= 32;
   // buffer 0 at offset 0, buffer 1 at BSTRIDE; plans in dynamic smem
   constexpr uint32_t FLIP = G::INPLACE ? 0u : SM::BSTRIDE;  // cur_off ^ FLIP = next buffer
