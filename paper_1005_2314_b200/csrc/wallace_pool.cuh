@@ -16,6 +16,7 @@
 // (/root/reference/proj/CMakeLists.txt:10-14).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 
@@ -1958,8 +1959,13 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
   if (MODE == kModeFillLat && a.n_emit > kLatRingMax) return cudaErrorInvalidValue;
   const size_t smem = (SM::STATIC ? 0 : size_t(SM::TOTAL)) + plans + ring;
   auto fn = pool_kernel<T, LOG2N, MODE, PT>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
+  // attributes are set once per instantiation and device; concurrent first
+  // launches from several host threads set them twice, which is harmless
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+  const uint64_t dev_bit = uint64_t(1) << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & dev_bit)) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess)
@@ -1967,7 +1973,7 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
                                int((SM::STATIC ? 16 * 1024 : SM::TOTAL + 16 * 1024) +
                                    (MODE == kModeFillLat ? 16 * kLatRingMax : 0)));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(dev_bit, std::memory_order_release);
   }
   fn<<<dim3(unsigned(n_pools)), dim3(kernel_threads<T, LOG2N, MODE>()), smem, stream>>>(a);
   return cudaGetLastError();
