@@ -200,6 +200,20 @@ constexpr uint64_t kMagic = 0x5741'4c4c'4143'4531ull;  // "WALLACE1"
 
 }  // namespace
 
+// Device block sums/counts of the consumer reduction and their pinned host
+// copy, kept between calls (grown on demand).
+struct ReduceScratch {
+  void* d_buf = nullptr;
+  void* h_buf = nullptr;
+  uint64_t cap = 0;  // blocks
+  void release() {
+    cudaFree(d_buf);
+    cudaFreeHost(h_buf);
+    d_buf = h_buf = nullptr;
+    cap = 0;
+  }
+};
+
 struct wallace_handle {
   wallace_config cfg{};
   int dtype = 0;
@@ -253,6 +267,7 @@ struct wallace_handle {
   double* d_part_sums = nullptr;
   uint32_t* d_part_hist = nullptr;
   uint64_t part_cap = 0;
+  ReduceScratch red;  // the partials' block reduction and its pinned host copy
 
   // staging for fill_host
   void* d_stage = nullptr;
@@ -874,6 +889,7 @@ wallace_status wallace_destroy(wallace_handle* h) {
   cudaFree(h->d_snap_leftover);
   cudaFree(h->d_part_sums);
   cudaFree(h->d_part_hist);
+  h->red.release();
   cudaFree(h->d_stage);
   cudaFree(h->d_lg_pool2);
   cudaFree(h->d_lg_state);
@@ -1674,23 +1690,27 @@ wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint6
 
 static wallace_status finish_consumer(cudaStream_t stream, const double* part_sums,
                                       const uint32_t* part_hist, uint64_t n_parts, double sums[4],
-                                      uint64_t hist[258]) {
+                                      uint64_t hist[258], ReduceScratch& r) {
   const uint64_t chunk = 256;
   const uint64_t blocks = (n_parts + chunk - 1) / chunk;
-  double* d_bs = nullptr;
-  unsigned long long* d_bh = nullptr;
-  WB_CUDA(cudaMalloc(&d_bs, blocks * 4 * sizeof(double)));
-  WB_CUDA(cudaMalloc(&d_bh, blocks * 258 * sizeof(unsigned long long)));
+  if (r.cap < blocks) {  // grown once; a cudaMalloc/cudaFree per call would synchronise the device
+    r.release();
+    const size_t bytes = blocks * (4 + 258) * 8;
+    WB_CUDA(cudaMalloc(&r.d_buf, bytes));
+    WB_CUDA(cudaMallocHost(&r.h_buf, bytes));
+    r.cap = blocks;
+  }
+  double* d_bs = static_cast<double*>(r.d_buf);
+  unsigned long long* d_bh = reinterpret_cast<unsigned long long*>(d_bs + blocks * 4);
   cudaError_t e = wb::launch_reduce_consumer(part_sums, part_hist, n_parts, chunk, d_bs, d_bh, stream);
   ++g_launches;
-  std::vector<double> bs(blocks * 4);
-  std::vector<unsigned long long> bh(blocks * 258);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(bs.data(), d_bs, bs.size() * 8, cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(bh.data(), d_bh, bh.size() * 8, cudaMemcpyDeviceToHost, stream);
+  // one copy of the block sums and counts into pinned memory
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(r.h_buf, r.d_buf, blocks * (4 + 258) * 8, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  cudaFree(d_bs);
-  cudaFree(d_bh);
   if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "consumer reduction: %s", cudaGetErrorString(e));
+  const double* bs = static_cast<const double*>(r.h_buf);
+  const unsigned long long* bh = reinterpret_cast<const unsigned long long*>(bs + blocks * 4);
   for (int k = 0; k < 4; ++k) sums[k] = 0.0;
   for (int b = 0; b < 258; ++b) hist[b] = 0;
   for (uint64_t i = 0; i < blocks; ++i) {
@@ -1745,7 +1765,7 @@ static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sum
     first = false;
     double s4[4];
     uint64_t h258[258];
-    st = finish_consumer(h->stream, h->d_part_sums, h->d_part_hist, h->n_pools, s4, h258);
+    st = finish_consumer(h->stream, h->d_part_sums, h->d_part_hist, h->n_pools, s4, h258, h->red);
     if (st) return st;
     for (int k = 0; k < 4; ++k) tot[k] += s4[k];
     for (int b = 0; b < 258; ++b) th[b] += h258[b];
@@ -1785,7 +1805,9 @@ wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_ba
   ++g_launches;
   wallace_status st = WALLACE_OK;
   if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "boxmuller: %s", cudaGetErrorString(e));
-  if (!st) st = finish_consumer(s, d_ps, d_ph, blocks, sums, hist);
+  ReduceScratch red;
+  if (!st) st = finish_consumer(s, d_ps, d_ph, blocks, sums, hist, red);
+  red.release();
   cudaFree(d_seeds);
   cudaFree(d_ps);
   cudaFree(d_ph);
