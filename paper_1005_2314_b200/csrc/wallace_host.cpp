@@ -1212,14 +1212,25 @@ wallace_status wallace_fill_from_snapshot(wallace_handle* h, void* dev_out, uint
   return run_emit(h, dev_out, count, wb::kModeFill, h->d_snap_state, h->d_snap_pools);
 }
 
+// The handle's device staging buffer, grown to at least `bytes`.
+static wallace_status ensure_stage(wallace_handle* h, uint64_t bytes) {
+  if (h->stage_bytes >= bytes) return WALLACE_OK;
+  cudaFree(h->d_stage);
+  h->d_stage = nullptr;
+  h->stage_bytes = 0;
+  WB_CUDA(cudaMalloc(&h->d_stage, bytes));
+  h->stage_bytes = bytes;
+  return WALLACE_OK;
+}
+
 wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* reserved,
                                  double* chi2_draw) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   void* out = dev_values;
-  void* tmp = nullptr;
-  if (!out) {
-    WB_CUDA(cudaMalloc(&tmp, h->n_pools * (h->N - 1) * h->esize));
-    out = tmp;
+  if (!out) {  // values discarded: emit into the staging buffer
+    const wallace_status se = ensure_stage(h, h->n_pools * (h->N - 1) * h->esize);
+    if (se) return se;
+    out = h->d_stage;
   }
   // refill_ + cursor_ = out_.size(): discard the partial buffer, so the
   // emission starts with no leftover (the device cursor is only read when a
@@ -1240,7 +1251,6 @@ wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* re
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "next_pool: %s", cudaGetErrorString(e));
   }
-  if (tmp) cudaFree(tmp);
   return st;
 }
 
@@ -1248,14 +1258,9 @@ wallace_status wallace_next_pool_host(wallace_handle* h, void* host_values, doub
                                       double* chi2_draw) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   const uint64_t bytes = h->n_pools * (h->N - 1) * h->esize;
-  if (h->stage_bytes < bytes) {
-    cudaFree(h->d_stage);
-    h->d_stage = nullptr;
-    h->stage_bytes = 0;
-    WB_CUDA(cudaMalloc(&h->d_stage, bytes));
-    h->stage_bytes = bytes;
-  }
-  wallace_status st = wallace_next_pool(h, h->d_stage, reserved, chi2_draw);
+  wallace_status st = ensure_stage(h, bytes);
+  if (st) return st;
+  st = wallace_next_pool(h, h->d_stage, reserved, chi2_draw);
   if (st) return st;
   if (host_values) {
     WB_CUDA(cudaMemcpyAsync(host_values, h->d_stage, bytes, cudaMemcpyDeviceToHost, h->stream));
