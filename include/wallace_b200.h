@@ -139,7 +139,9 @@ wallace_status wallace_get_pool(wallace_handle* h, uint64_t pool, double* raw_ou
 wallace_status wallace_get_pool_info(wallace_handle* h, uint64_t pool, wallace_pool_info* out);
 
 /* Checkpoint / resume (no reference equivalent: Generator state is private,
- * SURVEY §5).  The state image is pools + per-pool state, host memory. */
+ * SURVEY §5).  The state image is pools + per-pool state, host memory; it
+ * carries a hash of the configuration and loads only into a handle of the
+ * same configuration, pool size, dtype and pool count. */
 uint64_t wallace_state_bytes(const wallace_handle* h);
 wallace_status wallace_save_state(wallace_handle* h, void* host_buf, uint64_t bytes);
 wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint64_t bytes);
@@ -152,6 +154,24 @@ wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint6
 wallace_status wallace_snapshot(wallace_handle* h);
 wallace_status wallace_fill_from_snapshot(wallace_handle* h, void* dev_out,
                                           uint64_t count_per_pool);
+/* The live state becomes the snapshot again (the snapshot is kept). */
+wallace_status wallace_restore_snapshot(wallace_handle* h);
+/* Two snapshot slots (slot 0 is the one of wallace_snapshot /
+ * wallace_restore_snapshot / wallace_fill_from_snapshot). */
+wallace_status wallace_snapshot_ex(wallace_handle* h, int32_t slot);
+wallace_status wallace_restore_snapshot_ex(wallace_handle* h, int32_t slot);
+
+/* wallace_fill_host without the wait: the block's generation and its copy to
+ * host_out (pinned memory, see wallace_host_alloc) are queued on the
+ * handle's stream; wallace_synchronize() waits for them (and reports
+ * chi2_sample's error).  host_out must stay valid until then. */
+wallace_status wallace_fill_host_async(wallace_handle* h, void* host_out, uint64_t count_per_pool);
+/* Page-locked host memory for wallace_fill_host_async / fast host fills. */
+wallace_status wallace_host_alloc(uint64_t bytes, void** out);
+void wallace_host_free(void* p);
+/* count_per_pool further values of every pool, generated and dropped (the
+ * stream advances exactly as wallace_fill's would).  Asynchronous. */
+wallace_status wallace_discard(wallace_handle* h, uint64_t count_per_pool);
 
 /* Fused consumer (BASELINE config 5): generates count_per_pool values per
  * pool exactly as wallace_fill would, but consumes them in-kernel into
@@ -165,11 +185,71 @@ wallace_status wallace_consume(wallace_handle* h, uint64_t count_per_pool, doubl
 wallace_status wallace_consume_from_snapshot(wallace_handle* h, uint64_t count_per_pool,
                                              double sums[4], uint64_t hist[258]);
 
-/* Box-Muller comparator (baselines.cpp:68-92): stream p consumes the
- * uniform stream UniformState(seeds[p] or seed_base+p) exactly as
- * boxmuller_next does (u1 == 0 -> 2^-53, cached twin), evaluated on the
- * device in fp32 (log/sincos are not bit-exact with glibc; compare
- * statistically), and feeds the same consumer as wallace_consume. */
+/* ---- the reference's conventional generators (baselines.hpp:27-72) ------- */
+
+/* maxent::UniformState (baselines.hpp:27-33) and BaselineState (:49-55). */
+typedef struct wallace_uniform_state {
+  uint64_t s[4];
+  uint64_t draws;
+} wallace_uniform_state;
+typedef struct wallace_baseline_state {
+  wallace_uniform_state uniform;
+  int32_t has_cached; /* std::optional<double> cached */
+  int32_t reserved_;
+  double cached;
+} wallace_baseline_state;
+enum { WALLACE_BASELINE_POLAR = 0, WALLACE_BASELINE_BOXMULLER = 1 };
+
+/* Host functions, bit-identical to the reference on the same libm:
+ * splitmix64 / UniformState(seed) / uniform_bits / uniform_next
+ * (baselines.cpp:19-49), polar_next (:51-66), boxmuller_pair (:68-78,
+ * InvalidParameterError outside its domain), boxmuller_next (:80-92),
+ * exact_chi2_oracle (:94-104). */
+uint64_t wallace_splitmix64(uint64_t* state);
+void wallace_uniform_seed(uint64_t seed, wallace_uniform_state* out);
+uint64_t wallace_uniform_bits(wallace_uniform_state* u);
+double wallace_uniform_next(wallace_uniform_state* u);
+void wallace_baseline_seed(uint64_t seed, wallace_baseline_state* out);
+double wallace_polar_next(wallace_baseline_state* s);
+wallace_status wallace_boxmuller_pair(double u1, double u2, double* z1, double* z2);
+double wallace_boxmuller_next(wallace_baseline_state* s);
+wallace_status wallace_exact_chi2_oracle(uint64_t nu, wallace_baseline_state* s, double* out);
+
+/* chi2.hpp:21-41: compute_a (nu >= 1), Chi2Params::for_nu (nu >= 8, returns
+ * a_value), chi2_sample (InvalidParameterError for non-finite x; *clamped
+ * set when the draw is clamped to 1e-6 nu). */
+wallace_status wallace_compute_a(uint64_t nu, double* a);
+wallace_status wallace_chi2_params(uint64_t nu, double* a_value);
+wallace_status wallace_chi2_sample(double x, uint64_t nu, double a_value, int32_t method,
+                                   int32_t* clamped, double* out);
+
+/* transforms.hpp:64-137: wallace_variant(id) (entries row-major 4x4,
+ * source_row, row_sign; any pointer may be NULL; id in [0, 384)) and
+ * rotation_from_t (InvalidParameterError for non-finite t). */
+wallace_status wallace_variant(int32_t id, double entries[16], uint8_t source_row[4],
+                               double row_sign[4]);
+wallace_status wallace_rotation_from_t(double t, double* c, double* s);
+
+/* Device streams of polar_next / boxmuller_next (baselines.cpp:51-92), one
+ * thread per BaselineState, fp64: states[n_streams] (host) continue where
+ * they are and are advanced; stream p's next `count` values land in the
+ * DEVICE buffer dev_out[p*count, (p+1)*count).  The uniform words, the
+ * Polar acceptance sequence and the draw counts are exact; the values use
+ * CUDA's fp64 log/sqrt/sincos (a few ulps from glibc's, see
+ * tests/test_gpu_baselines.py).  Synchronous. */
+wallace_status wallace_baseline_fill(int32_t method, wallace_baseline_state* states,
+                                     uint64_t n_streams, uint64_t count, double* dev_out,
+                                     void* stream);
+
+/* Config-5 comparator: stream p = BaselineState(seeds[p] or seed_base+p),
+ * `count_per_stream` values of `method` generated as wallace_baseline_fill
+ * would, consumed in-kernel into the same sums[4] / hist[258] as
+ * wallace_consume (fp64).  *device_ms (optional): the kernel's device time
+ * (CUDA events).  Synchronous. */
+wallace_status wallace_baseline_consume(int32_t method, const uint64_t* seeds, uint64_t seed_base,
+                                        uint64_t n_streams, uint64_t count_per_stream, void* stream,
+                                        double sums[4], uint64_t hist[258], double* device_ms);
+/* = wallace_baseline_consume(WALLACE_BASELINE_BOXMULLER, ...) */
 wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_base,
                                          uint64_t n_streams, uint64_t count_per_stream,
                                          void* stream, double sums[4], uint64_t hist[258]);
@@ -189,8 +269,23 @@ wallace_status wallace_profile_end(wallace_handle* h, double* pool_kernel_ms,
  * exposed for tests and tuning. */
 wallace_status wallace_set_kernel_mode(wallace_handle* h, int32_t mode);
 
-/* Rebind the handle to another stream. */
+/* Rebind the handle to another stream.  Work already queued on the old
+ * stream is ordered before everything issued after the switch. */
 wallace_status wallace_set_stream(wallace_handle* h, void* stream);
+
+/* Waits for the handle's queued work.  chi2_sample's InvalidParameterError
+ * (chi2.cpp:29-31: a non-finite reserved value, e.g. after inject_pool of
+ * a non-finite pool, reached from refill_ inside fill/next_pool,
+ * generator.cpp:358-361) is detected on the device: the synchronous calls
+ * (wallace_fill_host, wallace_next_pool(_host), wallace_consume*,
+ * wallace_write_stream, wallace_pool_defect_stats, this call) return
+ * WALLACE_ERR_INVALID_PARAM "chi2_sample: x must be finite" for every
+ * emission they or an earlier asynchronous wallace_fill drew; wallace_fill
+ * itself reports an earlier call's error once it is known, at the latest
+ * the next synchronous call does.  Each detection is reported once; the
+ * non-finite value stays in the pool state, so later emissions raise again,
+ * as every later refill_ of the reference throws. */
+wallace_status wallace_synchronize(wallace_handle* h);
 
 /* Number of kernels this library has launched (all handles). */
 uint64_t wallace_kernel_launches(void);

@@ -20,10 +20,14 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -65,6 +69,168 @@ inline void check(wallace_status st) {
 enum class TransformFamily { wallace4, rotation };
 enum class MixingScheme { stride_transpose, affine };
 enum class Chi2Method { sqrt_shift, wilson_hilferty, cubic_a };
+
+// ---- baselines.hpp:27-72: the uniform helper and the conventional normal
+// generators (host, bit-identical to the reference through the C-ABI) -------
+struct UniformState {
+  std::array<std::uint64_t, 4> s{1, 2, 3, 4};
+  std::uint64_t draws = 0;
+  UniformState() = default;
+  explicit UniformState(std::uint64_t seed) {
+    wallace_uniform_state c{};
+    wallace_uniform_seed(seed, &c);
+    from_c(c);
+  }
+  wallace_uniform_state to_c() const {
+    wallace_uniform_state c{};
+    for (int k = 0; k < 4; ++k) c.s[k] = s[static_cast<std::size_t>(k)];
+    c.draws = draws;
+    return c;
+  }
+  void from_c(const wallace_uniform_state& c) {
+    for (int k = 0; k < 4; ++k) s[static_cast<std::size_t>(k)] = c.s[k];
+    draws = c.draws;
+  }
+};
+inline std::uint64_t splitmix64(std::uint64_t& state) { return wallace_splitmix64(&state); }
+inline std::uint64_t uniform_bits(UniformState& u) {
+  wallace_uniform_state c = u.to_c();
+  const std::uint64_t w = wallace_uniform_bits(&c);
+  u.from_c(c);
+  return w;
+}
+inline double uniform_next(UniformState& u) {
+  wallace_uniform_state c = u.to_c();
+  const double v = wallace_uniform_next(&c);
+  u.from_c(c);
+  return v;
+}
+
+struct BaselineState {
+  UniformState uniform;
+  std::optional<double> cached;
+  BaselineState() = default;
+  explicit BaselineState(std::uint64_t seed) : uniform(seed) {}
+  wallace_baseline_state to_c() const {
+    wallace_baseline_state c{};
+    c.uniform = uniform.to_c();
+    c.has_cached = cached ? 1 : 0;
+    c.cached = cached ? *cached : 0.0;
+    return c;
+  }
+  void from_c(const wallace_baseline_state& c) {
+    uniform.from_c(c.uniform);
+    if (c.has_cached) cached = c.cached;
+    else cached.reset();
+  }
+};
+inline double polar_next(BaselineState& s) {
+  wallace_baseline_state c = s.to_c();
+  const double v = wallace_polar_next(&c);
+  s.from_c(c);
+  return v;
+}
+inline std::pair<double, double> boxmuller_pair(double u1, double u2) {
+  double z1 = 0.0, z2 = 0.0;
+  check(wallace_boxmuller_pair(u1, u2, &z1, &z2));
+  return {z1, z2};
+}
+inline double boxmuller_next(BaselineState& s) {
+  wallace_baseline_state c = s.to_c();
+  const double v = wallace_boxmuller_next(&c);
+  s.from_c(c);
+  return v;
+}
+inline double exact_chi2_oracle(std::uint64_t nu, BaselineState& s) {
+  wallace_baseline_state c = s.to_c();
+  double v = 0.0;
+  check(wallace_exact_chi2_oracle(nu, &c, &v));
+  s.from_c(c);
+  return v;
+}
+
+// ---- chi2.hpp:21-41 ----------------------------------------------------------
+inline double compute_a(std::uint64_t nu) {
+  double a = 0.0;
+  check(wallace_compute_a(nu, &a));
+  return a;
+}
+struct Chi2Params {
+  std::uint64_t nu = 0;
+  double a_value = 0.0;
+  static Chi2Params for_nu(std::uint64_t nu) {
+    Chi2Params p;
+    p.nu = nu;
+    check(wallace_chi2_params(nu, &p.a_value));
+    return p;
+  }
+};
+inline double chi2_sample(double x, const Chi2Params& params, Chi2Method method, bool* clamped = nullptr) {
+  double s = 0.0;
+  std::int32_t c = 0;
+  check(wallace_chi2_sample(x, params.nu, params.a_value, static_cast<std::int32_t>(method), &c, &s));
+  if (clamped != nullptr) *clamped = c != 0;
+  return s;
+}
+
+// ---- transforms.hpp:21-137 ---------------------------------------------------
+struct RotationCoeffs {
+  double c;
+  double s;
+  double t;
+};
+inline RotationCoeffs rotation_from_t(double t) {
+  RotationCoeffs r{0.0, 0.0, t};
+  check(wallace_rotation_from_t(t, &r.c, &r.s));
+  return r;
+}
+inline std::pair<double, double> apply_rotation(double x1, double x2, const RotationCoeffs& r) {
+  return {r.c * x1 + r.s * x2, -r.s * x1 + r.c * x2};
+}
+inline std::span<const double> rotation_t_table() {
+  static const std::array<double, 16> table = [] {
+    std::array<double, 16> t{};
+    wallace_rotation_table(t.data(), nullptr, nullptr);
+    return t;
+  }();
+  return table;
+}
+
+inline constexpr std::size_t wallace_variant_count = 384;
+struct WallaceMatrix {
+  std::array<std::array<double, 4>, 4> entries;
+  int variant_id = 0;
+  std::array<std::uint8_t, 4> source_row{0, 1, 2, 3};
+  std::array<double, 4> row_sign{1.0, 1.0, 1.0, 1.0};
+};
+inline WallaceMatrix wallace_variant(int variant_id) {
+  WallaceMatrix m{};
+  double e[16];
+  check(::wallace_variant(variant_id, e, m.source_row.data(), m.row_sign.data()));
+  m.variant_id = variant_id;
+  for (int k = 0; k < 4; ++k)
+    for (int j = 0; j < 4; ++j) m.entries[static_cast<std::size_t>(k)][static_cast<std::size_t>(j)] = e[4 * k + j];
+  return m;
+}
+inline WallaceMatrix wallace_a1() { return wallace_variant(0); }
+inline std::vector<WallaceMatrix> wallace_variants(std::size_t count) {
+  if (count < 1 || count > wallace_variant_count)
+    throw InvalidParameterError("wallace_variants: count must be in [1, 384], got " + std::to_string(count));
+  std::vector<WallaceMatrix> out;
+  out.reserve(count);
+  for (std::size_t id = 0; id < count; ++id) out.push_back(wallace_variant(static_cast<int>(id)));
+  return out;
+}
+// transforms.hpp:89-103: the signed butterfly (eight additions, one halving
+// per output), the op order of the pass kernels
+inline std::array<double, 4> apply_wallace4(const std::array<double, 4>& v, const WallaceMatrix& m) {
+  const double a = v[0] + v[1], b = v[0] - v[1], c = v[2] + v[3], d = v[2] - v[3];
+  const std::array<double, 4> z{a - d, b + c, b - c, -a - d};
+  std::array<double, 4> out{};
+  for (std::size_t k = 0; k < 4; ++k) out[k] = (0.5 * m.row_sign[k]) * z[m.source_row[k]];
+  return out;
+}
+inline std::uint64_t default_stride(std::uint64_t rows) { return wallace_default_stride(rows); }
 
 // maxent::GeneratorConfig (generator.hpp:21-45)
 struct GeneratorConfig {
@@ -195,10 +361,13 @@ class PoolBatch {
     return *this;
   }
 
-  // fill(count) for every pool into a DEVICE buffer of n_pools*count values.
+  // fill(count) for every pool into a DEVICE buffer of n_pools*count values
+  // (asynchronous: chi2_sample's error is raised by the next synchronising
+  // call, e.g. synchronize()).
   void fill_device(void* dev_out, std::uint64_t count_per_pool) {
     check(wallace_fill(h_, dev_out, count_per_pool));
   }
+  void synchronize() { check(wallace_synchronize(h_)); }
   // fill(count) for every pool into HOST memory (end to end).
   void fill_host(void* host_out, std::uint64_t count_per_pool) {
     check(wallace_fill_host(h_, host_out, count_per_pool));
@@ -254,14 +423,41 @@ class PoolBatch {
 };
 
 // maxent::Generator (generator.hpp:98-149): one pool, fp64, bit-identical.
+//
+// The device generates the stream ahead of the caller, in blocks of kBlock
+// values double-buffered in page-locked host memory: while the caller
+// consumes block k, block k+1 is generated and copied
+// (wallace_fill_host_async).  next_normal() is then an inline cursor as in
+// the reference (generator.hpp:102-105) and fill() a copy.  Each block
+// starts with a device snapshot (slot = its buffer), so every call that
+// observes or changes the pool (step_pass, inject_pool, next_pool, pool()
+// and the counters) first rolls the device back to the consumed position
+// (restore the current block's snapshot, replay the values consumed from
+// it: sync_device_) and sees the reference's state.  A chi2_sample error
+// inside a look-ahead block is raised only when the values that need it are
+// requested: that part is regenerated exactly, up to the request.
 class Generator {
  public:
+  static constexpr std::size_t kDefaultBlock = std::size_t(1) << 20;
+
   explicit Generator(GeneratorConfig cfg, void* stream = nullptr)
-      : batch_(cfg, 1, &cfg.seed, WALLACE_F64, stream) {}
+      : batch_(cfg, 1, &cfg.seed, WALLACE_F64, stream) {
+    if (const char* e = std::getenv("WALLACE_B200_LOOKAHEAD")) kBlock = std::max<std::size_t>(1, std::strtoull(e, nullptr, 10));
+    void* p = nullptr;
+    check(wallace_host_alloc(2 * kBlock * sizeof(double), &p));
+    blk_[0] = static_cast<double*>(p);
+    blk_[1] = blk_[0] + kBlock;
+  }
+  ~Generator() {
+    if (inflight_) (void)wallace_synchronize(batch_.handle());
+    wallace_host_free(blk_[0]);
+  }
+  Generator(const Generator&) = delete;
+  Generator& operator=(const Generator&) = delete;
 
   double next_normal() {
-    if (cursor_ == buf_.size()) refill_buffer_();
-    return buf_[cursor_++];
+    if (cur_ == end_) advance_(1);
+    return *cur_++;
   }
 
   // Exactly equivalent to `count` next_normal() calls. count >= 1.
@@ -273,10 +469,25 @@ class Generator {
   }
   void fill(std::span<double> out) {
     if (out.empty()) throw InvalidParameterError("fill: count must be >= 1");
-    std::size_t i = 0;
-    // values already handed to the host by next_normal come first
-    while (i < out.size() && cursor_ < buf_.size()) out[i++] = buf_[cursor_++];
-    if (i < out.size()) batch_.fill_host(out.data() + i, out.size() - i);
+    double* dst = out.data();
+    std::size_t rest = out.size();
+    while (rest > 0) {
+      if (cur_ == end_) {
+        if (rest >= kBlock) {
+          // large requests go straight to the caller's memory from the
+          // consumed position
+          sync_device_();
+          batch_.fill_host(dst, rest);
+          return;
+        }
+        advance_(rest);
+      }
+      const std::size_t k = std::min<std::size_t>(rest, static_cast<std::size_t>(end_ - cur_));
+      std::copy_n(cur_, k, dst);
+      cur_ += k;
+      dst += k;
+      rest -= k;
+    }
   }
 
   struct PoolOutput {
@@ -286,16 +497,16 @@ class Generator {
   };
   // generator.cpp:401-405: refill, discard any partially consumed buffer.
   PoolOutput next_pool() {
+    sync_device_();
     last_pool_.resize(batch_.config().pool_size - 1);
     double reserved = 0.0, chi2 = 0.0;
     check(wallace_next_pool_host(batch_.handle(), last_pool_.data(), &reserved, &chi2));
-    buf_.clear();
-    cursor_ = 0;
     return {std::span<const double>{last_pool_}, reserved, chi2};
   }
 
   const GeneratorConfig& config() const { return batch_.config(); }
   const NormalPool& pool() const {
+    sync_device_();
     const wallace_pool_info i = batch_.info(0);
     pool_cache_.raw = batch_.raw(0);
     pool_cache_.reserved_prev = i.reserved_prev;
@@ -303,34 +514,91 @@ class Generator {
     pool_cache_.sum_sq = i.sum_sq;
     return pool_cache_;
   }
-  std::uint64_t pass_count() const { return batch_.info(0).pass_count; }
-  std::uint64_t uniform_draws() const { return batch_.info(0).uniform_draws; }
-  std::uint64_t chi2_clamp_count() const { return batch_.info(0).chi2_clamp_count; }
+  std::uint64_t pass_count() const { return info_().pass_count; }
+  std::uint64_t uniform_draws() const { return info_().uniform_draws; }
+  std::uint64_t chi2_clamp_count() const { return info_().chi2_clamp_count; }
 
   // One regeneration pass, no emission (generator.cpp:333-343).
-  void step_pass() { batch_.step_pass(1); }
+  void step_pass() {
+    sync_device_();
+    batch_.step_pass(1);
+  }
   // Replace the raw pool; sum of squares recomputed (generator.cpp:407-413).
   void inject_pool(std::span<const double> values) {
     if (values.size() != batch_.config().pool_size)
       throw InvalidParameterError("inject_pool: size must equal pool_size");
+    sync_device_();
     batch_.inject_pool(0, values);
   }
 
-  PoolBatch& batch() { return batch_; }
+  PoolBatch& batch() {
+    sync_device_();
+    return batch_;
+  }
 
  private:
-  // Take the rest of the current emission (never more: the reference's out_
-  // buffer never holds values of a later emission).
-  void refill_buffer_() {
-    const wallace_pool_info i = batch_.info(0);
-    const std::size_t k = i.buffered > 0 ? i.buffered : batch_.config().pool_size - 1;
-    buf_.resize(k);
-    batch_.fill_host(buf_.data(), k);
-    cursor_ = 0;
+  // queue block generation into buffer q (snapshot slot q = its start)
+  void queue_(int q) const {
+    wallace_handle* h = batch_.handle();
+    check(wallace_snapshot_ex(h, q));
+    check(wallace_fill_host_async(h, blk_[q], kBlock));
+    inflight_ = true;
+    q_ = q;
+  }
+  // The current block is used up: make the next one current (at least
+  // `want` values) and queue the one after it.
+  void advance_(std::size_t want) {
+    wallace_handle* h = batch_.handle();
+    if (!inflight_) queue_(c_ < 0 ? 0 : c_ ^ 1);
+    const wallace_status st = wallace_synchronize(h);
+    inflight_ = false;
+    if (st == WALLACE_OK) {
+      c_ = q_;
+      cur_ = blk_[c_];
+      end_ = cur_ + kBlock;
+      queue_(c_ ^ 1);
+      return;
+    }
+    cur_ = end_ = nullptr;
+    c_ = -1;
+    if (st != WALLACE_ERR_INVALID_PARAM) check(st);
+    // chi2_sample threw inside the look-ahead block: regenerate only what
+    // was asked for, so that the error surfaces at the reference's call
+    check(wallace_restore_snapshot_ex(h, q_));
+    exact_.resize(want);
+    check(wallace_fill_host(h, exact_.data(), want));
+    cur_ = exact_.data();
+    end_ = cur_ + want;
+  }
+  // Make the device state the consumed position (roll back the look-ahead).
+  void sync_device_() const {
+    wallace_handle* h = batch_.handle();
+    if (inflight_) {
+      (void)wallace_synchronize(h);  // an error there is in values not handed out
+      inflight_ = false;
+      if (c_ < 0 || cur_ == end_) check(wallace_restore_snapshot_ex(h, q_));  // = the current block's end
+    }
+    if (c_ >= 0 && cur_ != end_) {
+      check(wallace_restore_snapshot_ex(h, c_));
+      const std::size_t used = static_cast<std::size_t>(cur_ - blk_[c_]);
+      if (used > 0) check(wallace_discard(h, used));
+    }
+    cur_ = end_ = nullptr;
+    c_ = -1;
+  }
+  wallace_pool_info info_() const {
+    sync_device_();
+    return batch_.info(0);
   }
   PoolBatch batch_;
-  std::vector<double> buf_;
-  std::size_t cursor_ = 0;
+  std::size_t kBlock = kDefaultBlock;    // values per look-ahead block
+  double* blk_[2] = {nullptr, nullptr};  // page-locked look-ahead buffers
+  mutable double* cur_ = nullptr;        // [cur_, end_): values not yet handed out
+  mutable double* end_ = nullptr;
+  mutable int c_ = -1;                   // buffer of the current look-ahead block (-1: none)
+  mutable int q_ = 0;                    // buffer being generated
+  mutable bool inflight_ = false;
+  std::vector<double> exact_;            // exact regeneration after a look-ahead error
   std::vector<double> last_pool_;
   mutable NormalPool pool_cache_;
 };
@@ -344,7 +612,7 @@ struct TestReport {
   double expected = 0.0;
   double std_error = 0.0;
   double z_score = 0.0;
-  bool pass = false;
+  bool pass = true;
   static TestReport make(std::string name, double statistic, double expected, double std_error) {
     TestReport r;
     r.name = std::move(name);
@@ -360,6 +628,22 @@ struct TestReport {
     }
     r.pass = std::abs(r.z_score) <= 5.0;
     return r;
+  }
+  // stats.cpp:77-96: the CLI's report lines (byte-equal to the reference's)
+  std::string text() const {
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "[%s] %-40s statistic=%- 14.6g expected=%- 14.6g se=%- 12.4g z=%- .3f",
+                  pass ? "PASS" : "FAIL", name.c_str(), statistic, expected, std_error, z_score);
+    return buf;
+  }
+  std::string machine() const {
+    auto g17 = [](double v) {
+      char b[40];
+      std::snprintf(b, sizeof(b), "%.17g", v);
+      return std::string(b);
+    };
+    return "name=" + name + ",statistic=" + g17(statistic) + ",expected=" + g17(expected) +
+           ",se=" + g17(std_error) + ",z=" + g17(z_score) + ",verdict=" + (pass ? "PASS" : "FAIL");
   }
 };
 
@@ -398,6 +682,18 @@ inline MomentSummary moments(std::span<const double> samples) {
     out.excess_kurtosis = nn * m4 / (m2 * m2) - 3.0;
   }
   return out;
+}
+
+// maxent::moment_reports (stats.cpp:98-109): mean / variance / skewness /
+// excess kurtosis against N(0, 1), standard errors 1/sqrt(N), sqrt(2/N),
+// sqrt(6/N), sqrt(24/N)
+inline std::vector<TestReport> moment_reports(const MomentSummary& m, std::string_view prefix) {
+  const double n = static_cast<double>(m.count);
+  const std::string p{prefix};
+  return {TestReport::make(p + ".mean", m.mean, 0.0, 1.0 / std::sqrt(n)),
+          TestReport::make(p + ".variance", m.variance, 1.0, std::sqrt(2.0 / n)),
+          TestReport::make(p + ".skewness", m.skewness, 0.0, std::sqrt(6.0 / n)),
+          TestReport::make(p + ".excess_kurtosis", m.excess_kurtosis, 0.0, std::sqrt(24.0 / n))};
 }
 
 // maxent::CrossPoolOptions (stats.hpp:83-95), streaming variant

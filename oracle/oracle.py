@@ -22,6 +22,7 @@ ORACLE_SO = os.path.join(HERE, "libwallace_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libmaxent_ref.so")
 
 u64 = C.c_uint64
+WO_ERR_CHI2_NONFINITE = -20  # wallace_oracle.h: chi2_sample threw (chi2.cpp:29-31)
 i32 = C.c_int32
 f64 = C.c_double
 vp = C.c_void_p
@@ -154,6 +155,8 @@ def ref_lib():
         L.ref_fill.argtypes = [vp, P(f64), u64]
         L.ref_next_normal.argtypes = [vp]
         L.ref_next_normal.restype = f64
+        L.ref_next_normal_ex.argtypes = [vp, P(C.c_int)]
+        L.ref_next_normal_ex.restype = f64
         L.ref_next_pool.argtypes = [vp, P(f64), P(f64), P(f64)]
         L.ref_step_pass.argtypes = [vp]
         L.ref_inject_pool.argtypes = [vp, P(f64), u64]
@@ -207,6 +210,8 @@ class OracleGen:
     def fill(self, count: int) -> np.ndarray:
         out = np.empty(count, dtype=self.np_dtype)
         rc = self.L.wo_fill(self.h, out.ctypes.data_as(vp), count)
+        if rc == WO_ERR_CHI2_NONFINITE:
+            raise ValueError("chi2_sample: x must be finite")
         if rc != 0:
             raise ValueError("fill: count must be >= 1")
         return out
@@ -214,7 +219,8 @@ class OracleGen:
     def next_pool(self):
         vals = np.empty(self.cfg.pool_size - 1, dtype=self.np_dtype)
         res, chi = f64(), f64()
-        self.L.wo_next_pool(self.h, vals.ctypes.data_as(vp), C.byref(res), C.byref(chi))
+        if self.L.wo_next_pool(self.h, vals.ctypes.data_as(vp), C.byref(res), C.byref(chi)) != 0:
+            raise ValueError("chi2_sample: x must be finite")
         return vals, res.value, chi.value
 
     def step_pass(self):
@@ -264,12 +270,17 @@ class RefGen:
         return out
 
     def next_normal(self) -> float:
-        return self.L.ref_next_normal(self.h)
+        err = C.c_int()
+        v = self.L.ref_next_normal_ex(self.h, C.byref(err))
+        if err.value:
+            raise ValueError(self.L.ref_last_error().decode())
+        return v
 
     def next_pool(self):
         vals = np.empty(self.cfg.pool_size - 1, dtype=np.float64)
         res, chi = f64(), f64()
-        self.L.ref_next_pool(self.h, _dp(vals), C.byref(res), C.byref(chi))
+        if self.L.ref_next_pool(self.h, _dp(vals), C.byref(res), C.byref(chi)) < 0:
+            raise ValueError(self.L.ref_last_error().decode())
         return vals, res.value, chi.value
 
     def step_pass(self):

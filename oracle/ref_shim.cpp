@@ -103,16 +103,35 @@ int ref_fill(void* g, double* out, uint64_t count) {
   }
 }
 
+// next_normal / next_pool can throw (chi2_sample on a non-finite reserved
+// value, chi2.cpp:29-31): *err / the return value report it
+double ref_next_normal_ex(void* g, int* err) {
+  try {
+    *err = 0;
+    return static_cast<maxent::Generator*>(g)->next_normal();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    *err = 1;
+    return 0.0;
+  }
+}
+
 double ref_next_normal(void* g) {
-  return static_cast<maxent::Generator*>(g)->next_normal();
+  int err = 0;
+  return ref_next_normal_ex(g, &err);
 }
 
 int ref_next_pool(void* g, double* values, double* reserved, double* chi2) {
-  auto po = static_cast<maxent::Generator*>(g)->next_pool();
-  if (values) std::memcpy(values, po.values.data(), po.values.size() * 8);
-  *reserved = po.reserved;
-  *chi2 = po.chi2_draw;
-  return static_cast<int>(po.values.size());
+  try {
+    auto po = static_cast<maxent::Generator*>(g)->next_pool();
+    if (values) std::memcpy(values, po.values.data(), po.values.size() * 8);
+    *reserved = po.reserved;
+    *chi2 = po.chi2_draw;
+    return static_cast<int>(po.values.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 void ref_step_pass(void* g) { static_cast<maxent::Generator*>(g)->step_pass(); }
@@ -302,6 +321,65 @@ int ref_cross_pool_fixed(uint64_t n, int family, int mixing, uint64_t seed, uint
     g_err = e.what();
     return -1;
   }
+}
+
+// tools/cmd_test.cpp:40-60 run_moments_suite: the report lines (machine()
+// or text()) of the reference, joined by '\n'; returns the length or -1
+int ref_moments_suite(uint64_t seed, uint64_t n, int machine, char* out, uint64_t cap) {
+  try {
+    std::string all;
+    auto print = [&](const std::vector<maxent::TestReport>& rs) {
+      for (const auto& r : rs) all += (machine ? r.machine() : r.text()) + "\n";
+    };
+    {
+      maxent::GeneratorConfig cfg;
+      cfg.seed = seed;
+      maxent::Generator gen(cfg);
+      print(maxent::moment_reports(maxent::moments(gen.fill(n)), "wallace4"));
+    }
+    {
+      maxent::BaselineState s(seed);
+      std::vector<double> buf(n);
+      for (auto& v : buf) v = maxent::polar_next(s);
+      print(maxent::moment_reports(maxent::moments(buf), "polar"));
+    }
+    {
+      maxent::BaselineState s(seed);
+      std::vector<double> buf(n);
+      for (auto& v : buf) v = maxent::boxmuller_next(s);
+      print(maxent::moment_reports(maxent::moments(buf), "boxmuller"));
+    }
+    if (all.size() + 1 > cap) return -1;
+    std::memcpy(out, all.c_str(), all.size() + 1);
+    return static_cast<int>(all.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// one-core rates of the reference's own call patterns on a Generator
+// (bench.cpp:43-59 fill chunks, cmd_gen.cpp:127-134, next_normal loop):
+// values per second, pattern 0 = next_normal, else fill in `chunk` pieces
+double ref_pattern_rate(uint64_t pool_size, uint64_t seed, int pattern, uint64_t chunk, uint64_t total) {
+  maxent::GeneratorConfig cfg;
+  cfg.pool_size = pool_size;
+  cfg.seed = seed;
+  maxent::Generator gen(cfg);
+  std::vector<double> buf(chunk > 0 ? chunk : 1);
+  double sink = 0.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (pattern == 0) {
+    for (uint64_t i = 0; i < total; ++i) sink += gen.next_normal();
+  } else {
+    for (uint64_t i = 0; i < total; i += chunk) {
+      gen.fill(std::span<double>(buf));
+      sink += buf[0];
+    }
+  }
+  const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (sink == 12345.678) std::puts("");
+  return static_cast<double>(total) / dt;
 }
 
 void ref_polar(uint64_t seed, uint64_t n, double* out) {

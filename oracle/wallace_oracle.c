@@ -267,15 +267,13 @@ void wo_destroy(wo_gen* g) {
 
 int wo_fill(wo_gen* g, void* out, uint64_t count) {
   if (count < 1) return -10;
-  if (g->dtype) fill_f64(g, (double*)out, count);
-  else fill_f32(g, (float*)out, count);
-  return 0;
+  return g->dtype ? fill_f64(g, (double*)out, count) : fill_f32(g, (float*)out, count);
 }
 
 /* generator.cpp:401-405 */
 int wo_next_pool(wo_gen* g, void* values, double* reserved, double* chi2_draw) {
-  if (g->dtype) refill_f64(g);
-  else refill_f32(g);
+  const int rc = g->dtype ? refill_f64(g) : refill_f32(g);
+  if (rc) return rc;
   g->cursor = g->out_len;
   const size_t es = g->dtype ? sizeof(double) : sizeof(float);
   if (values) memcpy(values, g->out, g->out_len * es);

@@ -65,7 +65,10 @@ double wo_chi2_sample(double x, uint64_t nu, double a, int method, int* clamped)
 /* Generator lifecycle; dtype 0 = f32 restatement, 1 = f64 reference. */
 int wo_create(const wo_config* cfg, int dtype, wo_gen** out);
 void wo_destroy(wo_gen* g);
-/* fill(count) — out is float* (f32) or double* (f64) */
+/* chi2_sample's InvalidParameterError for a non-finite reserved value
+ * (chi2.cpp:29-31), raised from refill_ inside fill / next_pool */
+#define WO_ERR_CHI2_NONFINITE (-20)
+/* fill(count) — out is float* (f32) or double* (f64); 0 or an error code */
 int wo_fill(wo_gen* g, void* out, uint64_t count);
 /* next_pool(): writes pool_size-1 values to out */
 int wo_next_pool(wo_gen* g, void* values, double* reserved, double* chi2_draw);

@@ -28,7 +28,8 @@ import numpy as np
 from . import _capi
 
 __all__ = ["GeneratorConfig", "PoolBatch", "ConfigError", "InvalidParameterError",
-           "UnsupportedError", "CudaError", "boxmuller_consume", "kernel_launches"]
+           "UnsupportedError", "CudaError", "boxmuller_consume", "baseline_consume", "BaselineStreams",
+           "BaselineState", "chi2_sample", "kernel_launches"]
 
 
 class ConfigError(ValueError):
@@ -152,21 +153,35 @@ class PoolBatch:
         return torch.float32 if self.dtype == "f32" else torch.float64
 
     # -- generation ----------------------------------------------------------
-    def fill_into(self, out) -> None:
-        """Generator::fill(span) into a device tensor of shape (n_pools, count)."""
+    def _check_out(self, out) -> None:
         if out.dim() != 2 or out.shape[0] != self.n_pools or not out.is_contiguous():
             raise InvalidParameterError("out must be a contiguous (n_pools, count) tensor")
         if out.dtype != self.torch_dtype or not out.is_cuda:
             raise InvalidParameterError("out must be a CUDA tensor of the batch dtype")
+        if out.shape[1] < 1:
+            raise InvalidParameterError("fill: count must be >= 1")
+
+    def fill_into(self, out) -> None:
+        """Generator::fill(span) into a device tensor of shape (n_pools, count).
+        Asynchronous: chi2_sample's error (a non-finite reserved value) is
+        raised by the next synchronising call (synchronize(), fill(), ...)."""
+        self._check_out(out)
         _check(self.L.wallace_fill(self.h, C.c_void_p(out.data_ptr()), out.shape[1]))
 
+    def synchronize(self) -> None:
+        """Wait for the batch's queued work; raises InvalidParameterError
+        where the reference's fill/next_pool would have thrown (chi2.cpp:29-31)."""
+        _check(self.L.wallace_synchronize(self.h))
+
     def fill(self, count: int):
-        """Generator::fill(count) for every pool -> (n_pools, count) CUDA tensor."""
+        """Generator::fill(count) for every pool -> (n_pools, count) CUDA tensor
+        (synchronous: raises like the reference's fill)."""
         if count < 1:
             raise InvalidParameterError("fill: count must be >= 1")
         torch = _torch()
         out = torch.empty((self.n_pools, count), dtype=self.torch_dtype, device="cuda")
         self.fill_into(out)
+        self.synchronize()
         return out
 
     def fill_host(self, count: int, out: Optional[np.ndarray] = None) -> np.ndarray:
@@ -185,6 +200,7 @@ class PoolBatch:
         _check(self.L.wallace_snapshot(self.h))
 
     def fill_from_snapshot_into(self, out) -> None:
+        self._check_out(out)
         _check(self.L.wallace_fill_from_snapshot(self.h, C.c_void_p(out.data_ptr()), out.shape[1]))
 
     def next_pool(self):
@@ -359,19 +375,88 @@ def cross_pool_fixed_sums(cfg: GeneratorConfig, pairs: int, probes) -> np.ndarra
     return acc
 
 
-def boxmuller_consume(n_streams: int, count: int, seed_base: int = 1, seeds=None, stream=None):
-    """Box-Muller comparator on UniformState(seed) streams (baselines.cpp:80-92)."""
+BASELINE_METHODS = {"polar": _capi.WALLACE_BASELINE_POLAR, "boxmuller": _capi.WALLACE_BASELINE_BOXMULLER}
+
+
+def baseline_consume(method: str, n_streams: int, count: int, seed_base: int = 1, seeds=None, stream=None):
+    """Config-5 comparator: BaselineState(seed) streams of polar_next /
+    boxmuller_next (baselines.cpp:51-92) generated on the device in fp64 and
+    consumed in-kernel like PoolBatch.consume.  Returns (sums, hist,
+    kernel device ms)."""
     L = _capi.load()
     sums = np.zeros(4, dtype=np.float64)
     hist = np.zeros(258, dtype=np.uint64)
+    ms = C.c_double()
     sp = None
     if seeds is not None:
         seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
         sp = seeds.ctypes.data_as(C.POINTER(C.c_uint64))
-    _check(L.wallace_boxmuller_consume(sp, seed_base, n_streams, count, _stream_handle(stream),
-                                       sums.ctypes.data_as(C.POINTER(C.c_double)),
-                                       hist.ctypes.data_as(C.POINTER(C.c_uint64))))
+    _check(L.wallace_baseline_consume(BASELINE_METHODS[method], sp, seed_base, n_streams, count,
+                                      _stream_handle(stream), sums.ctypes.data_as(C.POINTER(C.c_double)),
+                                      hist.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(ms)))
+    return sums, hist, ms.value
+
+
+def boxmuller_consume(n_streams: int, count: int, seed_base: int = 1, seeds=None, stream=None):
+    """Box-Muller comparator on UniformState(seed) streams (baselines.cpp:80-92)."""
+    sums, hist, _ = baseline_consume("boxmuller", n_streams, count, seed_base, seeds, stream)
     return sums, hist
+
+
+class BaselineStreams:
+    """n independent BaselineState streams (baselines.hpp:49-55) of polar_next
+    or boxmuller_next, generated on the device (fp64): ``fill(count)``
+    continues every stream and returns a (n_streams, count) CUDA tensor.
+    The uniform words and draw counts are exact; the values are within a few
+    ulps of the reference's glibc transcendentals."""
+
+    def __init__(self, method: str, seeds):
+        self.method = BASELINE_METHODS[method]
+        seeds = [int(s) for s in seeds]
+        self.n = len(seeds)
+        self.states = (_capi.wallace_baseline_state * self.n)()
+        L = _capi.load()
+        for k, s in enumerate(seeds):
+            L.wallace_baseline_seed(s, C.byref(self.states[k]))
+
+    def fill(self, count: int, stream=None):
+        torch = _torch()
+        out = torch.empty((self.n, int(count)), dtype=torch.float64, device="cuda")
+        _check(_capi.load().wallace_baseline_fill(self.method, self.states, self.n, int(count),
+                                                  C.c_void_p(out.data_ptr()), _stream_handle(stream)))
+        return out
+
+    def draws(self, k: int = 0) -> int:
+        return int(self.states[k].uniform.draws)
+
+
+# ---- host functions of the reference's L1a layer (bit-identical, same libm) ----
+class BaselineState:
+    """maxent::BaselineState with polar_next / boxmuller_next (baselines.cpp:51-92)."""
+
+    def __init__(self, seed: int):
+        self.c = _capi.wallace_baseline_state()
+        _capi.load().wallace_baseline_seed(int(seed) & (2**64 - 1), C.byref(self.c))
+
+    def polar_next(self) -> float:
+        return _capi.load().wallace_polar_next(C.byref(self.c))
+
+    def boxmuller_next(self) -> float:
+        return _capi.load().wallace_boxmuller_next(C.byref(self.c))
+
+    @property
+    def draws(self) -> int:
+        return int(self.c.uniform.draws)
+
+
+def chi2_sample(x: float, nu: int, method: int = 2):
+    """chi2_sample(x, Chi2Params::for_nu(nu), method) -> (S, clamped) (chi2.cpp:19-59)."""
+    L = _capi.load()
+    a = C.c_double()
+    _check(L.wallace_chi2_params(int(nu), C.byref(a)))
+    out, cl = C.c_double(), C.c_int32()
+    _check(L.wallace_chi2_sample(float(x), int(nu), a.value, int(method), C.byref(cl), C.byref(out)))
+    return out.value, bool(cl.value)
 
 
 def kernel_launches() -> int:

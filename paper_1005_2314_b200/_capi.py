@@ -54,6 +54,21 @@ class wallace_pass_plan(C.Structure):
     ]
 
 
+class wallace_uniform_state(C.Structure):
+    """maxent::UniformState (baselines.hpp:27-33)."""
+    _fields_ = [("s", u64 * 4), ("draws", u64)]
+
+
+class wallace_baseline_state(C.Structure):
+    """maxent::BaselineState (baselines.hpp:49-55)."""
+    _fields_ = [("uniform", wallace_uniform_state), ("has_cached", i32), ("reserved_", i32),
+                ("cached", f64)]
+
+
+WALLACE_BASELINE_POLAR = 0
+WALLACE_BASELINE_BOXMULLER = 1
+
+
 class wallace_pool_info(C.Structure):
     _fields_ = [
         ("pass_count", u64),
@@ -84,6 +99,13 @@ SYMBOLS = [
     ("wallace_load_state", i32, [vp, vp, u64]),
     ("wallace_snapshot", i32, [vp]),
     ("wallace_fill_from_snapshot", i32, [vp, vp, u64]),
+    ("wallace_restore_snapshot", i32, [vp]),
+    ("wallace_snapshot_ex", i32, [vp, i32]),
+    ("wallace_restore_snapshot_ex", i32, [vp, i32]),
+    ("wallace_fill_host_async", i32, [vp, vp, u64]),
+    ("wallace_host_alloc", i32, [u64, P(vp)]),
+    ("wallace_host_free", None, [vp]),
+    ("wallace_discard", i32, [vp, u64]),
     ("wallace_consume", i32, [vp, u64, P(f64), P(u64)]),
     ("wallace_consume_from_snapshot", i32, [vp, u64, P(f64), P(u64)]),
     ("wallace_boxmuller_consume", i32, [P(u64), u64, u64, u64, vp, P(f64), P(u64)]),
@@ -91,6 +113,7 @@ SYMBOLS = [
     ("wallace_profile_end", i32, [vp, P(f64), P(u64), P(f64), P(u64)]),
     ("wallace_set_kernel_mode", i32, [vp, i32]),
     ("wallace_set_stream", i32, [vp, vp]),
+    ("wallace_synchronize", i32, [vp]),
     ("wallace_kernel_launches", u64, []),
     ("wallace_last_error", C.c_char_p, []),
     ("wallace_validate_config", i32, [P(wallace_config)]),
@@ -107,6 +130,22 @@ SYMBOLS = [
     ("wallace_cross_pool_fixed", i32, [P(wallace_config), u64, C.c_uint32, P(u64), P(u64), P(C.c_double)]),
     ("wallace_create_ex", i32, [P(wallace_config), u64, P(u64), i32, vp, C.c_uint32, P(vp)]),
     ("wallace_pool_defect_stats", i32, [vp, u64, C.c_double, P(C.c_double), P(C.c_uint8)]),
+    ("wallace_splitmix64", u64, [P(u64)]),
+    ("wallace_uniform_seed", None, [u64, P(wallace_uniform_state)]),
+    ("wallace_uniform_bits", u64, [P(wallace_uniform_state)]),
+    ("wallace_uniform_next", f64, [P(wallace_uniform_state)]),
+    ("wallace_baseline_seed", None, [u64, P(wallace_baseline_state)]),
+    ("wallace_polar_next", f64, [P(wallace_baseline_state)]),
+    ("wallace_boxmuller_pair", i32, [f64, f64, P(f64), P(f64)]),
+    ("wallace_boxmuller_next", f64, [P(wallace_baseline_state)]),
+    ("wallace_exact_chi2_oracle", i32, [u64, P(wallace_baseline_state), P(f64)]),
+    ("wallace_compute_a", i32, [u64, P(f64)]),
+    ("wallace_chi2_params", i32, [u64, P(f64)]),
+    ("wallace_chi2_sample", i32, [f64, u64, f64, i32, P(i32), P(f64)]),
+    ("wallace_variant", i32, [i32, P(f64), P(C.c_uint8), P(f64)]),
+    ("wallace_rotation_from_t", i32, [f64, P(f64), P(f64)]),
+    ("wallace_baseline_fill", i32, [i32, P(wallace_baseline_state), u64, u64, vp, vp]),
+    ("wallace_baseline_consume", i32, [i32, P(u64), u64, u64, u64, vp, P(f64), P(u64), P(f64)]),
 ]
 
 _lib = None

@@ -37,7 +37,8 @@ struct alignas(16) PoolState {
 static_assert(sizeof(PoolState) == 128, "PoolState layout");
 
 constexpr uint32_t kFlagLeftover = 1u;      // leftover emission materialized
-constexpr uint32_t kFlagChi2NonFinite = 2u; // chi2_sample saw non-finite x
+constexpr uint32_t kFlagChi2NonFinite = 2u; // chi2_sample saw non-finite x (this launch only;
+                                            // reported through FillArgs::err_word)
 
 // Precomputed chi2 constants (chi2.cpp:27-59).  Every entry is computed on
 // the host with the same double expression the reference evaluates per call,
@@ -138,6 +139,9 @@ struct FillArgs {
   // consumer (kModeConsume)
   double* part_sums;      // [n_pools][4]
   uint32_t* part_hist;    // [n_pools][258]
+  // set (atomicOr 1) when some pool's chi2 draw saw a non-finite reserved
+  // value: the reference's chi2_sample throws there (chi2.cpp:29-31)
+  uint32_t* err_word;
 };
 
 struct PlanArgs {

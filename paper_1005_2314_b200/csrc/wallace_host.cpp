@@ -47,9 +47,11 @@ cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void
 cudaError_t launch_reduce_consumer(const double* part_sums, const uint32_t* part_hist,
                                    uint64_t n_pools, uint64_t chunk, double* blk_sums,
                                    unsigned long long* blk_hist, cudaStream_t s);
-cudaError_t launch_boxmuller(const uint64_t* d_seeds, uint64_t seed_base, uint64_t n_streams,
-                             uint64_t count, double* part_sums, uint32_t* part_hist,
-                             uint64_t n_blocks, int threads, cudaStream_t s);
+cudaError_t launch_baseline_fill(int method, void* states, uint64_t n_streams, uint64_t count, double* out,
+                                 cudaStream_t s);
+cudaError_t launch_baseline_consume(int method, const uint64_t* d_seeds, uint64_t seed_base, uint64_t n_streams,
+                                    uint64_t count, double* part_sums, uint32_t* part_hist, uint64_t n_blocks,
+                                    cudaStream_t s);
 }  // namespace wb
 
 using wb::PoolState;
@@ -237,6 +239,7 @@ struct wallace_handle {
   int key = 0;        // kernel key: log2(N) (+16 for the latency kernel)
   int kmode = 0;      // 0 auto, 1 throughput, 2 latency
   bool bulk_ok = false;  // fills may use the bulk-emission kernel
+  bool bulk_cfg_ok = false;  // ... as far as the configuration goes (finite pools)
   bool staged_ok = false;  // other fills may use the staged-emission kernel
   bool lat_fill_ok = false;  // latency-geometry fills may decouple the chi2 chain (kModeFillLat)
   double* d_scales = nullptr;  // kModeFillLat: [n_pools][plan_cap] per-emission scales
@@ -256,12 +259,19 @@ struct wallace_handle {
   uint64_t def_stride = 0;
   double def_threshold = 0.0;
   void* d_leftover = nullptr;
-  void* d_snap_pools = nullptr;
-  PoolState* d_snap_state = nullptr;
-  void* d_snap_leftover = nullptr;
-  uint32_t snap_cursor = 0;
-  uint64_t snap_pass_count = 0;
-  bool has_snapshot = false;
+  // device snapshots (wallace_snapshot_ex slots 0 and 1)
+  struct Snap {
+    void* pools = nullptr;
+    PoolState* state = nullptr;
+    void* leftover = nullptr;
+    bool leftover_valid = false;  // the live leftover was copied (partial emission materialised)
+    uint32_t cursor = 0;
+    uint64_t pass_count = 0;
+    bool has = false;
+  } snap[2];
+  // wallace_fill_host_async: device staging of the queued block
+  void* d_astage = nullptr;
+  uint64_t astage_bytes = 0;
 
   // consumer scratch
   double* d_part_sums = nullptr;
@@ -284,6 +294,15 @@ struct wallace_handle {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_plan;
   std::vector<cudaEvent_t> ev_free;
+
+  // chi2_sample's non-finite error (chi2.cpp:29-31): the kernels set d_err,
+  // every emitting launch sequence is followed by a copy of it into the
+  // pinned h_err and ev_err; calls report it once the copy has landed (the
+  // synchronous calls wait for it)
+  uint32_t* d_err = nullptr;
+  uint32_t* h_err = nullptr;
+  cudaEvent_t ev_err = nullptr;
+  bool err_queued = false;
 
   uint32_t cursor = 0;      // uniform across pools (all pools advance together)
   uint64_t pass_count = 0;  // uniform
@@ -393,6 +412,7 @@ wb::FillArgs base_args(wallace_handle* h) {
   a.def_marks = h->d_def_marks;
   a.def_stride = h->def_stride;
   a.def_threshold = h->def_threshold;
+  a.err_word = h->d_err;
   if (h->large) {
     const uint64_t rows = h->N / 4;
     uint64_t al = 0, be = 0;
@@ -642,7 +662,36 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     produced += lead + (e == 0 ? 0 : (e == e_total ? remaining : e * n1));
     first = false;
   }
-  return issue(h, ls);
+  wallace_status st = issue(h, ls);
+  if (st) return st;
+  // the error word of these launches -> pinned host memory (see d_err)
+  WB_CUDA(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  WB_CUDA(cudaEventRecord(h->ev_err, h->stream));
+  h->err_queued = true;
+  return WALLACE_OK;
+}
+
+// Reports chi2_sample's error from emitting launches already issued: when
+// `wait`, after they finished (the caller synchronises anyway); otherwise only
+// if their error word has already landed.  The error is reported once.
+wallace_status take_err(wallace_handle* h, bool wait) {
+  if (!h->err_queued) return WALLACE_OK;
+  if (wait) {
+    WB_CUDA(cudaEventSynchronize(h->ev_err));
+  } else if (cudaEventQuery(h->ev_err) != cudaSuccess) {
+    (void)cudaGetLastError();  // cudaErrorNotReady is not an error
+    return WALLACE_OK;
+  }
+  h->err_queued = false;
+  if (*h->h_err == 0) return WALLACE_OK;
+  *h->h_err = 0;
+  WB_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(uint32_t), h->stream));
+  // the reference's refill_ threw before the emission existed (its buffer
+  // stays used up, generator.cpp:358-376): the next value starts a new
+  // emission, whose chi2 draw throws again.  For a batch the partially
+  // consumed emission of every pool is dropped.
+  h->cursor = static_cast<uint32_t>(h->N - 1);
+  return fail(WALLACE_ERR_INVALID_PARAM, "chi2_sample: x must be finite");
 }
 
 }  // namespace
@@ -821,6 +870,11 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
   WB_CUDA_C(cudaMalloc(&h->d_plans, 2 * n_pools * h->plan_cap * h->plan_words * sizeof(uint32_t)));
   WB_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+  WB_CUDA_C(cudaMalloc(&h->d_err, sizeof(uint32_t)));
+  WB_CUDA_C(cudaMallocHost(&h->h_err, sizeof(uint32_t)));
+  *h->h_err = 0;
+  WB_CUDA_C(cudaMemsetAsync(h->d_err, 0, sizeof(uint32_t), h->stream));
+  WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_err, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_planned[i], cudaEventDisableTiming));
     WB_CUDA_C(cudaEventCreateWithFlags(&h->ev_pooled[i], cudaEventDisableTiming));
@@ -830,8 +884,9 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
     // disable_chi2 makes S = sum_sq, so r = S/sum_sq = 1 and scale = sigma
     // exactly; with sigma 1 and mean +0 each emitted value is x*1+0
     const char* nb = std::getenv("WALLACE_B200_NO_BULK");
-    h->bulk_ok = cfg->disable_chi2 && cfg->out_sigma == 1.0 && cfg->out_mean == 0.0 &&
-                 !std::signbit(cfg->out_mean) && h->pass_type < 2 && !(nb && nb[0] == '1');
+    h->bulk_cfg_ok = cfg->disable_chi2 && cfg->out_sigma == 1.0 && cfg->out_mean == 0.0 &&
+                     !std::signbit(cfg->out_mean) && h->pass_type < 2 && !(nb && nb[0] == '1');
+    h->bulk_ok = h->bulk_cfg_ok;
     // any other wallace4 fill: scaled values staged in shared memory and
     // sent by bulk copies (WALLACE_B200_NO_STAGED=1: register emission)
     const char* ns = std::getenv("WALLACE_B200_NO_STAGED");
@@ -881,12 +936,18 @@ wallace_status wallace_destroy(wallace_handle* h) {
     if (h->ev_planned[i]) cudaEventDestroy(h->ev_planned[i]);
     if (h->ev_pooled[i]) cudaEventDestroy(h->ev_pooled[i]);
   }
+  cudaFree(h->d_err);
+  cudaFreeHost(h->h_err);
+  if (h->ev_err) cudaEventDestroy(h->ev_err);
   cudaFree(h->d_leftover);
   cudaFree(h->d_scales);
   cudaFree(h->d_lat_raw);
-  cudaFree(h->d_snap_pools);
-  cudaFree(h->d_snap_state);
-  cudaFree(h->d_snap_leftover);
+  for (auto& sn : h->snap) {
+    cudaFree(sn.pools);
+    cudaFree(sn.state);
+    cudaFree(sn.leftover);
+  }
+  cudaFree(h->d_astage);
   cudaFree(h->d_part_sums);
   cudaFree(h->d_part_hist);
   h->red.release();
@@ -947,14 +1008,32 @@ wallace_status wallace_set_kernel_mode(wallace_handle* h, int32_t mode) {
 
 wallace_status wallace_set_stream(wallace_handle* h, void* stream) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
-  h->stream = static_cast<cudaStream_t>(stream);
+  // work queued on the old stream (pool kernels reading plans / pools /
+  // state) and on the plan side stream precedes everything issued after the
+  // switch: the new stream and the side stream wait for both
+  cudaStream_t ns = static_cast<cudaStream_t>(stream);
+  WB_CUDA(cudaEventRecord(h->ev_start, h->stream));
+  WB_CUDA(cudaStreamWaitEvent(ns, h->ev_start, 0));
+  WB_CUDA(cudaStreamWaitEvent(h->side, h->ev_start, 0));
+  WB_CUDA(cudaEventRecord(h->ev_start, h->side));
+  WB_CUDA(cudaStreamWaitEvent(ns, h->ev_start, 0));
+  h->stream = ns;
   return WALLACE_OK;
+}
+
+wallace_status wallace_synchronize(wallace_handle* h) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  WB_CUDA(cudaStreamSynchronize(h->stream));
+  return take_err(h, true);
 }
 
 wallace_status wallace_fill(wallace_handle* h, void* dev_out, uint64_t count) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (!dev_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
+  // an earlier asynchronous fill's chi2 error, if it is already known
+  wallace_status st = take_err(h, false);
+  if (st) return st;
   return run_emit(h, dev_out, count, wb::kModeFill, h->d_state, h->d_pools);
 }
 
@@ -1122,6 +1201,7 @@ wallace_status wallace_write_stream(wallace_handle* h, uint64_t count, int32_t f
     ::lseek(fd, base + static_cast<off_t>(h->n_pools * count * (format == WALLACE_FMT_F32LE ? 4 : 8)), SEEK_SET);
   cudaStreamSynchronize(h->stream);
   cudaStreamSynchronize(cs);
+  if (!st) st = take_err(h, true);
   return st;
 }
 
@@ -1129,15 +1209,25 @@ wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t cou
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (!host_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
+  wallace_status st0 = take_err(h, false);
+  if (st0) return st0;
   // Stage the whole pool-major block on the device when it fits (HBM is
   // large): one fill and one contiguous device->host copy run at the link's
   // bandwidth.  Otherwise chunk along the per-pool count (strided copies).
+  // Free memory is queried only when the staging buffer must grow; the
+  // stage then takes at most half of it (at least 64 MiB, at most 48 GiB).
   const uint64_t row_bytes = h->n_pools * h->esize;
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
-  const uint64_t max_stage =
-      std::max<uint64_t>(2ull << 30, std::min<uint64_t>(48ull << 30, (free_b + h->stage_bytes) / 2));
-  uint64_t chunk = std::max<uint64_t>(1, max_stage / row_bytes);
+  uint64_t chunk = std::max<uint64_t>(1, h->stage_bytes / row_bytes);
+  if (chunk < count) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      (void)cudaGetLastError();
+      free_b = 0;
+    }
+    const uint64_t max_stage =
+        std::max<uint64_t>(64ull << 20, std::min<uint64_t>(48ull << 30, (free_b + h->stage_bytes) / 2));
+    chunk = std::max<uint64_t>(chunk, std::max<uint64_t>(1, max_stage / row_bytes));
+  }
   chunk = std::min(chunk, count);
   const uint64_t need = chunk * row_bytes;
   if (h->stage_bytes < need) {
@@ -1176,40 +1266,114 @@ wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t cou
                                 h->n_pools, cudaMemcpyDeviceToHost, h->stream));
   }
   WB_CUDA(cudaStreamSynchronize(h->stream));
+  return take_err(h, true);
+}
+
+wallace_status wallace_snapshot_ex(wallace_handle* h, int32_t slot) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (slot < 0 || slot > 1) return fail(WALLACE_ERR_INVALID_PARAM, "snapshot: slot must be 0 or 1");
+  auto& sn = h->snap[slot];
+  const size_t pb = h->n_pools * h->N * h->esize;
+  if (!sn.pools) WB_CUDA(cudaMalloc(&sn.pools, pb));
+  if (!sn.state) WB_CUDA(cudaMalloc(&sn.state, h->n_pools * sizeof(PoolState)));
+  WB_CUDA(cudaMemcpyAsync(sn.pools, h->d_pools, pb, cudaMemcpyDeviceToDevice, h->stream));
+  WB_CUDA(cudaMemcpyAsync(sn.state, h->d_state, h->n_pools * sizeof(PoolState), cudaMemcpyDeviceToDevice,
+                          h->stream));
+  sn.leftover_valid = h->d_leftover && h->cursor < h->N - 1;
+  if (sn.leftover_valid) {
+    const size_t lb = h->n_pools * (h->N - 1) * h->esize;
+    if (!sn.leftover) WB_CUDA(cudaMalloc(&sn.leftover, lb));
+    WB_CUDA(cudaMemcpyAsync(sn.leftover, h->d_leftover, lb, cudaMemcpyDeviceToDevice, h->stream));
+  }
+  sn.cursor = h->cursor;
+  sn.pass_count = h->pass_count;
+  sn.has = true;
   return WALLACE_OK;
 }
 
-wallace_status wallace_snapshot(wallace_handle* h) {
+wallace_status wallace_snapshot(wallace_handle* h) { return wallace_snapshot_ex(h, 0); }
+
+wallace_status wallace_fill_host_async(wallace_handle* h, void* host_out, uint64_t count) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
-  const size_t pb = h->n_pools * h->N * h->esize;
-  if (!h->d_snap_pools) WB_CUDA(cudaMalloc(&h->d_snap_pools, pb));
-  if (!h->d_snap_state) WB_CUDA(cudaMalloc(&h->d_snap_state, h->n_pools * sizeof(PoolState)));
-  WB_CUDA(cudaMemcpyAsync(h->d_snap_pools, h->d_pools, pb, cudaMemcpyDeviceToDevice, h->stream));
-  WB_CUDA(cudaMemcpyAsync(h->d_snap_state, h->d_state, h->n_pools * sizeof(PoolState),
-                          cudaMemcpyDeviceToDevice, h->stream));
-  if (h->d_leftover) {
-    const size_t lb = h->n_pools * (h->N - 1) * h->esize;
-    if (!h->d_snap_leftover) WB_CUDA(cudaMalloc(&h->d_snap_leftover, lb));
-    WB_CUDA(cudaMemcpyAsync(h->d_snap_leftover, h->d_leftover, lb, cudaMemcpyDeviceToDevice,
-                            h->stream));
+  if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
+  if (!host_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
+  wallace_status st = take_err(h, false);
+  if (st) return st;
+  const uint64_t bytes = h->n_pools * count * h->esize;
+  if (h->astage_bytes < bytes) {
+    // the stream's queued work may still read the old staging buffer
+    WB_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(h->d_astage);
+    h->d_astage = nullptr;
+    h->astage_bytes = 0;
+    WB_CUDA(cudaMalloc(&h->d_astage, bytes));
+    h->astage_bytes = bytes;
   }
-  h->snap_cursor = h->cursor;
-  h->snap_pass_count = h->pass_count;
-  h->has_snapshot = true;
+  st = run_emit(h, h->d_astage, count, wb::kModeFill, h->d_state, h->d_pools);
+  if (st) return st;
+  WB_CUDA(cudaMemcpyAsync(host_out, h->d_astage, bytes, cudaMemcpyDeviceToHost, h->stream));
+  return WALLACE_OK;
+}
+
+wallace_status wallace_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return fail(WALLACE_ERR_INVALID_PARAM, "out must not be NULL");
+  *out = nullptr;
+  WB_CUDA(cudaMallocHost(out, bytes));
+  return WALLACE_OK;
+}
+
+void wallace_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+// the live leftover / cursor / pass count of snapshot `sn` (its pools and
+// state are read in place by the first launch, or copied by restore)
+static wallace_status snap_prologue(wallace_handle* h, const wallace_handle::Snap& sn) {
+  if (sn.leftover_valid)
+    WB_CUDA(cudaMemcpyAsync(h->d_leftover, sn.leftover, h->n_pools * (h->N - 1) * h->esize,
+                            cudaMemcpyDeviceToDevice, h->stream));
+  h->cursor = sn.cursor;
+  h->pass_count = sn.pass_count;
   return WALLACE_OK;
 }
 
 wallace_status wallace_fill_from_snapshot(wallace_handle* h, void* dev_out, uint64_t count) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
-  if (!h->has_snapshot) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
+  const auto& sn = h->snap[0];
+  if (!sn.has) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
-  if (h->d_snap_leftover && h->snap_cursor < h->N - 1)
-    WB_CUDA(cudaMemcpyAsync(h->d_leftover, h->d_snap_leftover,
-                            h->n_pools * (h->N - 1) * h->esize, cudaMemcpyDeviceToDevice,
-                            h->stream));
-  h->cursor = h->snap_cursor;
-  h->pass_count = h->snap_pass_count;
-  return run_emit(h, dev_out, count, wb::kModeFill, h->d_snap_state, h->d_snap_pools);
+  if (!dev_out) return fail(WALLACE_ERR_INVALID_PARAM, "fill: output must not be NULL");
+  wallace_status st = take_err(h, false);
+  if (!st) st = snap_prologue(h, sn);
+  if (st) return st;
+  return run_emit(h, dev_out, count, wb::kModeFill, sn.state, sn.pools);
+}
+
+wallace_status wallace_restore_snapshot_ex(wallace_handle* h, int32_t slot) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  if (slot < 0 || slot > 1) return fail(WALLACE_ERR_INVALID_PARAM, "snapshot: slot must be 0 or 1");
+  const auto& sn = h->snap[slot];
+  if (!sn.has) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
+  WB_CUDA(cudaMemcpyAsync(h->d_pools, sn.pools, h->n_pools * h->N * h->esize, cudaMemcpyDeviceToDevice,
+                          h->stream));
+  WB_CUDA(cudaMemcpyAsync(h->d_state, sn.state, h->n_pools * sizeof(PoolState), cudaMemcpyDeviceToDevice,
+                          h->stream));
+  return snap_prologue(h, sn);
+}
+
+wallace_status wallace_restore_snapshot(wallace_handle* h) { return wallace_restore_snapshot_ex(h, 0); }
+
+static wallace_status ensure_stage(wallace_handle* h, uint64_t bytes);
+
+wallace_status wallace_discard(wallace_handle* h, uint64_t count) {
+  if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
+  // fill(count) into the handle's staging buffer, in pieces of at most 64 MiB
+  const uint64_t row = h->n_pools * h->esize;
+  const uint64_t piece = std::max<uint64_t>(1, std::min<uint64_t>(count, (64ull << 20) / row));
+  wallace_status st = ensure_stage(h, piece * row);
+  for (uint64_t done = 0; !st && done < count; done += piece)
+    st = run_emit(h, h->d_stage, std::min(piece, count - done), wb::kModeFill, h->d_state, h->d_pools);
+  return st;
 }
 
 // The handle's device staging buffer, grown to at least `bytes`.
@@ -1236,13 +1400,15 @@ wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* re
   // emission starts with no leftover (the device cursor is only read when a
   // leftover is drained)
   h->cursor = static_cast<uint32_t>(h->N - 1);
-  wallace_status st = run_emit(h, out, h->N - 1, wb::kModeFill, h->d_state, h->d_pools);
+  wallace_status st = take_err(h, false);
+  if (!st) st = run_emit(h, out, h->N - 1, wb::kModeFill, h->d_state, h->d_pools);
   if (!st && (reserved || chi2_draw)) {
     std::vector<PoolState> states(h->n_pools);
     cudaError_t e = cudaMemcpyAsync(states.data(), h->d_state, h->n_pools * sizeof(PoolState),
                                     cudaMemcpyDeviceToHost, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "next_pool: %s", cudaGetErrorString(e));
+    if (!st) st = take_err(h, true);
     for (uint64_t p = 0; p < h->n_pools && !st; ++p) {
       if (reserved) reserved[p] = states[p].reserved_prev;
       if (chi2_draw) chi2_draw[p] = states[p].last_chi2;
@@ -1250,6 +1416,7 @@ wallace_status wallace_next_pool(wallace_handle* h, void* dev_values, double* re
   } else if (!st) {
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "next_pool: %s", cudaGetErrorString(e));
+    if (!st) st = take_err(h, true);
   }
   return st;
 }
@@ -1546,6 +1713,7 @@ wallace_status wallace_pool_defect_stats(wallace_handle* h, uint64_t emissions, 
     if (!st) e = cudaMemcpyAsync(totals, h->d_def_totals, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
     if (!st && e == cudaSuccess) e = cudaMemcpyAsync(marks, h->d_def_marks, n, cudaMemcpyDeviceToHost, h->stream);
     if (!st && e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (!st && e == cudaSuccess) st = take_err(h, true);
   }
   cudaFree(h->d_def_totals);
   cudaFree(h->d_def_marks);
@@ -1602,11 +1770,11 @@ wallace_status wallace_get_pool(wallace_handle* h, uint64_t pool, double* raw_ou
 wallace_status wallace_get_pool_info(wallace_handle* h, uint64_t pool, wallace_pool_info* out) {
   if (!h || !out) return fail(WALLACE_ERR_INVALID_PARAM, "handle/out must not be NULL");
   if (pool >= h->n_pools) return fail(WALLACE_ERR_INVALID_PARAM, "get_pool_info: pool out of range");
+  // (an accessor: never reports chi2_sample's error, as Generator's
+  // accessors never throw, generator.hpp:122-126)
   PoolState ps;
   WB_CUDA(cudaMemcpyAsync(&ps, h->d_state + pool, sizeof(ps), cudaMemcpyDeviceToHost, h->stream));
   WB_CUDA(cudaStreamSynchronize(h->stream));
-  if (ps.flags & wb::kFlagChi2NonFinite)
-    return fail(WALLACE_ERR_INVALID_PARAM, "chi2_sample: x must be finite");
   out->pass_count = ps.pass_count;
   out->uniform_draws = ps.draws;
   out->chi2_clamp_count = ps.clamp_count;
@@ -1616,6 +1784,27 @@ wallace_status wallace_get_pool_info(wallace_handle* h, uint64_t pool, wallace_p
   out->buffered = (h->N - 1) - ps.cursor;
   out->seed = ps.seed;
   return WALLACE_OK;
+}
+
+// FNV-1a over the config fields that shape the stream: an image saved by a
+// handle of another configuration must not load (it would produce values
+// matching neither config)
+static uint64_t config_hash(const wallace_config& c) {
+  uint64_t x = 0xcbf29ce484222325ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) x = (x ^ b[i]) * 0x100000001b3ull;
+  };
+  mix(&c.pool_size, sizeof c.pool_size);
+  mix(&c.transform_family, sizeof c.transform_family);
+  mix(&c.mixing, sizeof c.mixing);
+  mix(&c.chi2_method, sizeof c.chi2_method);
+  mix(&c.fixed_transform, sizeof c.fixed_transform);
+  mix(&c.disable_chi2, sizeof c.disable_chi2);
+  mix(&c.discard_every, sizeof c.discard_every);
+  mix(&c.out_mean, sizeof c.out_mean);
+  mix(&c.out_sigma, sizeof c.out_sigma);
+  return x;
 }
 
 uint64_t wallace_state_bytes(const wallace_handle* h) {
@@ -1631,7 +1820,7 @@ wallace_status wallace_save_state(wallace_handle* h, void* host_buf, uint64_t by
   if (st) return st;
   unsigned char* p = static_cast<unsigned char*>(host_buf);
   uint64_t hdr[8] = {kMagic, h->N, static_cast<uint64_t>(h->dtype), h->n_pools, h->cursor,
-                     h->pass_count, h->d_leftover ? 1ull : 0ull, 0};
+                     h->pass_count, h->d_leftover ? 1ull : 0ull, config_hash(h->cfg)};
   std::memcpy(p, hdr, sizeof(hdr));
   p += 64;
   const size_t pb = h->n_pools * h->N * h->esize;
@@ -1656,8 +1845,12 @@ wallace_status wallace_load_state(wallace_handle* h, const void* host_buf, uint6
   if (hdr[0] != kMagic || hdr[1] != h->N || hdr[2] != static_cast<uint64_t>(h->dtype) ||
       hdr[3] != h->n_pools)
     return fail(WALLACE_ERR_INVALID_PARAM, "load_state: image does not match this handle");
+  if (hdr[7] != config_hash(h->cfg))
+    return fail(WALLACE_ERR_INVALID_PARAM, "load_state: image was saved with another configuration");
+  if (hdr[4] > h->N - 1) return fail(WALLACE_ERR_INVALID_PARAM, "load_state: corrupt image (cursor)");
   p += 64;
   const size_t pb = h->n_pools * h->N * h->esize;
+  h->bulk_ok = h->bulk_cfg_ok;  // re-derived from the image's pools
   if (h->bulk_ok) {  // see wallace_inject_pool: bulk emissions need finite pools
     const uint64_t cnt = h->n_pools * h->N;
     bool finite = true;
@@ -1728,7 +1921,7 @@ static wallace_status finish_consumer(cudaStream_t stream, const double* part_su
 static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sums[4],
                                    uint64_t hist[258], bool from_snapshot) {
   if (!h || !sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "handle/sums/hist must not be NULL");
-  if (from_snapshot && !h->has_snapshot) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
+  if (from_snapshot && !h->snap[0].has) return fail(WALLACE_ERR_INVALID_PARAM, "no snapshot taken");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
   if (h->part_cap < h->n_pools) {
     cudaFree(h->d_part_sums);
@@ -1749,11 +1942,8 @@ static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sum
   const uint64_t per_launch_emit = std::max<uint64_t>(1, h->plan_cap / std::max<uint64_t>(1, d));
   uint64_t done = 0;
   if (from_snapshot) {
-    if (h->d_snap_leftover && h->snap_cursor < h->N - 1)
-      WB_CUDA(cudaMemcpyAsync(h->d_leftover, h->d_snap_leftover, h->n_pools * (h->N - 1) * h->esize,
-                              cudaMemcpyDeviceToDevice, h->stream));
-    h->cursor = h->snap_cursor;
-    h->pass_count = h->snap_pass_count;
+    const wallace_status sp = snap_prologue(h, h->snap[0]);
+    if (sp) return sp;
   }
   bool first = true;
   while (done < count) {
@@ -1764,13 +1954,14 @@ static wallace_status consume_impl(wallace_handle* h, uint64_t count, double sum
     const uint64_t cap = (d > h->plan_cap && lead > 0) ? lead : lead + per_launch_emit * n1;
     const uint64_t c = std::min(cap, count - done);
     const bool snap = from_snapshot && first;
-    wallace_status st = run_emit(h, nullptr, c, wb::kModeConsume, snap ? h->d_snap_state : h->d_state,
-                                 snap ? h->d_snap_pools : h->d_pools);
+    wallace_status st = run_emit(h, nullptr, c, wb::kModeConsume, snap ? h->snap[0].state : h->d_state,
+                                 snap ? h->snap[0].pools : h->d_pools);
     if (st) return st;
     first = false;
     double s4[4];
     uint64_t h258[258];
     st = finish_consumer(h->stream, h->d_part_sums, h->d_part_hist, h->n_pools, s4, h258, h->red);
+    if (!st) st = take_err(h, true);
     if (st) return st;
     for (int k = 0; k < 4; ++k) tot[k] += s4[k];
     for (int b = 0; b < 258; ++b) th[b] += h258[b];
@@ -1790,33 +1981,233 @@ wallace_status wallace_consume_from_snapshot(wallace_handle* h, uint64_t count, 
   return consume_impl(h, count, sums, hist, true);
 }
 
-wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_base, uint64_t n_streams,
-                                         uint64_t count, void* stream, double sums[4], uint64_t hist[258]) {
+wallace_status wallace_baseline_consume(int32_t method, const uint64_t* seeds, uint64_t seed_base,
+                                        uint64_t n_streams, uint64_t count, void* stream, double sums[4],
+                                        uint64_t hist[258], double* device_ms) {
   if (!sums || !hist) return fail(WALLACE_ERR_INVALID_PARAM, "sums/hist must not be NULL");
+  if (method != WALLACE_BASELINE_POLAR && method != WALLACE_BASELINE_BOXMULLER)
+    return fail(WALLACE_ERR_INVALID_PARAM, "baseline: method must be polar (0) or boxmuller (1)");
   if (n_streams < 1 || count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "need >= 1 stream and value");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int threads = 128;
-  const uint64_t blocks = (n_streams + threads - 1) / threads;
+  const uint64_t blocks = (n_streams + 127) / 128;
   uint64_t* d_seeds = nullptr;
   double* d_ps = nullptr;
   uint32_t* d_ph = nullptr;
-  if (seeds) {
-    WB_CUDA(cudaMalloc(&d_seeds, n_streams * 8));
-    WB_CUDA(cudaMemcpyAsync(d_seeds, seeds, n_streams * 8, cudaMemcpyHostToDevice, s));
-  }
-  WB_CUDA(cudaMalloc(&d_ps, blocks * 4 * sizeof(double)));
-  WB_CUDA(cudaMalloc(&d_ph, blocks * 258 * sizeof(uint32_t)));
-  cudaError_t e = wb::launch_boxmuller(d_seeds, seed_base, n_streams, count, d_ps, d_ph, blocks, threads, s);
-  ++g_launches;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
   wallace_status st = WALLACE_OK;
-  if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "boxmuller: %s", cudaGetErrorString(e));
+  cudaError_t e = cudaSuccess;
+  if (seeds) {
+    e = cudaMalloc(&d_seeds, n_streams * 8);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_seeds, seeds, n_streams * 8, cudaMemcpyHostToDevice, s);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&d_ps, blocks * 4 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_ph, blocks * 258 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  if (e == cudaSuccess) e = cudaEventRecord(e0, s);
+  if (e == cudaSuccess) e = wb::launch_baseline_consume(method, d_seeds, seed_base, n_streams, count, d_ps, d_ph,
+                                                        blocks, s);
+  if (e == cudaSuccess) {
+    ++g_launches;
+    e = cudaEventRecord(e1, s);
+  }
+  if (e != cudaSuccess) st = fail(WALLACE_ERR_CUDA, "baseline_consume: %s", cudaGetErrorString(e));
   ReduceScratch red;
   if (!st) st = finish_consumer(s, d_ps, d_ph, blocks, sums, hist, red);
+  if (!st && device_ms) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *device_ms = ms;
+  }
   red.release();
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
   cudaFree(d_seeds);
   cudaFree(d_ps);
   cudaFree(d_ph);
   return st;
+}
+
+wallace_status wallace_boxmuller_consume(const uint64_t* seeds, uint64_t seed_base, uint64_t n_streams,
+                                         uint64_t count, void* stream, double sums[4], uint64_t hist[258]) {
+  return wallace_baseline_consume(WALLACE_BASELINE_BOXMULLER, seeds, seed_base, n_streams, count, stream, sums,
+                                  hist, nullptr);
+}
+
+wallace_status wallace_baseline_fill(int32_t method, wallace_baseline_state* states, uint64_t n_streams,
+                                     uint64_t count, double* dev_out, void* stream) {
+  if (!states || !dev_out) return fail(WALLACE_ERR_INVALID_PARAM, "states/out must not be NULL");
+  if (method != WALLACE_BASELINE_POLAR && method != WALLACE_BASELINE_BOXMULLER)
+    return fail(WALLACE_ERR_INVALID_PARAM, "baseline: method must be polar (0) or boxmuller (1)");
+  if (n_streams < 1 || count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "need >= 1 stream and value");
+  static_assert(sizeof(wallace_baseline_state) == 56, "wallace_baseline_state layout");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  void* d_st = nullptr;
+  const size_t bytes = n_streams * sizeof(wallace_baseline_state);
+  cudaError_t e = cudaMalloc(&d_st, bytes);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_st, states, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = wb::launch_baseline_fill(method, d_st, n_streams, count, dev_out, s);
+  if (e == cudaSuccess) {
+    ++g_launches;
+    e = cudaMemcpyAsync(states, d_st, bytes, cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_st);
+  if (e != cudaSuccess) return fail(WALLACE_ERR_CUDA, "baseline_fill: %s", cudaGetErrorString(e));
+  return WALLACE_OK;
+}
+
+// ---- host helpers of the reference's L1a layer (baselines / chi2 / transforms)
+namespace {
+Uniform to_uniform(const wallace_uniform_state* u) {
+  Uniform x(0);
+  std::memcpy(x.s, u->s, sizeof(x.s));
+  x.draws = u->draws;
+  return x;
+}
+void from_uniform(const Uniform& x, wallace_uniform_state* u) {
+  std::memcpy(u->s, x.s, sizeof(x.s));
+  u->draws = x.draws;
+}
+constexpr double kPi = 3.141592653589793238462643383279502884;  // std::numbers::pi
+}  // namespace
+
+uint64_t wallace_splitmix64(uint64_t* state) { return splitmix64(*state); }
+
+void wallace_uniform_seed(uint64_t seed, wallace_uniform_state* out) {
+  const Uniform u(seed);
+  from_uniform(u, out);
+}
+
+uint64_t wallace_uniform_bits(wallace_uniform_state* u) {
+  Uniform x = to_uniform(u);
+  const uint64_t w = x.bits();
+  from_uniform(x, u);
+  return w;
+}
+
+double wallace_uniform_next(wallace_uniform_state* u) {
+  Uniform x = to_uniform(u);
+  const double v = x.next();
+  from_uniform(x, u);
+  return v;
+}
+
+void wallace_baseline_seed(uint64_t seed, wallace_baseline_state* out) {
+  std::memset(out, 0, sizeof(*out));
+  wallace_uniform_seed(seed, &out->uniform);
+}
+
+double wallace_polar_next(wallace_baseline_state* st) {  // baselines.cpp:51-66
+  Polar p(0);
+  p.u = to_uniform(&st->uniform);
+  p.has = st->has_cached != 0;
+  p.cached = st->cached;
+  const double v = p.next();
+  from_uniform(p.u, &st->uniform);
+  st->has_cached = p.has ? 1 : 0;
+  st->cached = p.has ? p.cached : 0.0;
+  return v;
+}
+
+wallace_status wallace_boxmuller_pair(double u1, double u2, double* z1, double* z2) {  // baselines.cpp:68-78
+  if (!(u1 > 0.0) || u1 > 1.0) return fail(WALLACE_ERR_INVALID_PARAM, "boxmuller_pair: u1 must be in (0, 1]");
+  if (!(u2 >= 0.0) || u2 >= 1.0) return fail(WALLACE_ERR_INVALID_PARAM, "boxmuller_pair: u2 must be in [0, 1)");
+  const double r = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * kPi * u2;
+  if (z1) *z1 = r * std::cos(angle);
+  if (z2) *z2 = r * std::sin(angle);
+  return WALLACE_OK;
+}
+
+double wallace_boxmuller_next(wallace_baseline_state* st) {  // baselines.cpp:80-92
+  if (st->has_cached) {
+    st->has_cached = 0;
+    const double v = st->cached;
+    st->cached = 0.0;
+    return v;
+  }
+  double u1 = wallace_uniform_next(&st->uniform);
+  if (u1 == 0.0) u1 = 0x1.0p-53;
+  const double u2 = wallace_uniform_next(&st->uniform);
+  double z1 = 0.0, z2 = 0.0;
+  wallace_boxmuller_pair(u1, u2, &z1, &z2);
+  st->cached = z2;
+  st->has_cached = 1;
+  return z1;
+}
+
+wallace_status wallace_exact_chi2_oracle(uint64_t nu, wallace_baseline_state* st, double* out) {  // baselines.cpp:94-104
+  if (nu < 1) return fail(WALLACE_ERR_INVALID_PARAM, "exact_chi2_oracle: nu must be >= 1");
+  double sum = 0.0;
+  for (uint64_t i = 0; i < nu; ++i) {
+    const double z = wallace_polar_next(st);
+    sum += z * z;
+  }
+  if (out) *out = sum;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_compute_a(uint64_t nu, double* a) {  // chi2.cpp:11-17
+  if (nu < 1) return fail(WALLACE_ERR_INVALID_PARAM, "compute_a: nu must be >= 1");
+  if (a) *a = compute_a(nu);
+  return WALLACE_OK;
+}
+
+wallace_status wallace_chi2_params(uint64_t nu, double* a_value) {  // chi2.cpp:19-25 Chi2Params::for_nu
+  if (nu < 8)
+    return fail(WALLACE_ERR_INVALID_PARAM, "Chi2Params: nu must be >= 8, got %llu",
+                static_cast<unsigned long long>(nu));
+  if (a_value) *a_value = compute_a(nu);
+  return WALLACE_OK;
+}
+
+wallace_status wallace_chi2_sample(double x, uint64_t nu, double a_value, int32_t method, int32_t* clamped,
+                                   double* out) {  // chi2.cpp:27-59
+  if (!std::isfinite(x)) return fail(WALLACE_ERR_INVALID_PARAM, "chi2_sample: x must be finite");
+  if (method < 0 || method > 2) return fail(WALLACE_ERR_INVALID_PARAM, "chi2_sample: unknown method");
+  const double n = static_cast<double>(nu);
+  double s;
+  if (method == WALLACE_CHI2_SQRT_SHIFT) {
+    const double y = x + std::sqrt(2.0 * n - 1.0);
+    s = 0.5 * y * y;
+  } else if (method == WALLACE_CHI2_WILSON_HILFERTY) {
+    const double d = 2.0 / (9.0 * n);
+    const double y = std::sqrt(d) * x + (1.0 - d);
+    s = n * y * y * y;
+  } else {
+    s = a_value * (x * x - 1.0) + std::sqrt(2.0 * (n - a_value * a_value)) * x + n;
+  }
+  const double floor_v = 1e-6 * n;
+  const bool c = s < floor_v;
+  if (clamped) *clamped = c ? 1 : 0;
+  if (out) *out = c ? floor_v : s;
+  return WALLACE_OK;
+}
+
+wallace_status wallace_variant(int32_t id, double entries[16], uint8_t source_row[4], double row_sign[4]) {
+  // transforms.cpp:15-35, 76-97: entries[k][j] = row_sign[k] * 0.5 * A1[source_row[k]][j]
+  if (id < 0 || id >= 384)
+    return fail(WALLACE_ERR_INVALID_PARAM, "wallace_variant: id out of range [0, 384)");
+  static const int kA1[4][4] = {{1, 1, -1, 1}, {1, -1, 1, 1}, {1, -1, -1, -1}, {-1, -1, -1, 1}};
+  for (int k = 0; k < 4; ++k) {
+    const int src = perm_elem(id >> 4, k);
+    const double sg = ((id & 15) >> k) & 1 ? -1.0 : 1.0;
+    if (source_row) source_row[k] = static_cast<uint8_t>(src);
+    if (row_sign) row_sign[k] = sg;
+    if (entries)
+      for (int j = 0; j < 4; ++j) entries[4 * k + j] = sg * 0.5 * kA1[src][j];
+  }
+  return WALLACE_OK;
+}
+
+wallace_status wallace_rotation_from_t(double t, double* c, double* s) {  // transforms.cpp:52-70
+  if (!std::isfinite(t)) return fail(WALLACE_ERR_INVALID_PARAM, "rotation_from_t: t must be finite");
+  double cc = 0.0, ss = 0.0;
+  rotation_from_t(t, cc, ss);
+  if (c) *c = cc;
+  if (s) *s = ss;
+  return WALLACE_OK;
 }
 
 }  // extern "C"

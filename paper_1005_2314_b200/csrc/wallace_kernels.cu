@@ -13,7 +13,6 @@ namespace wb {
 // stages 32 pools x 32 passes in shared memory so the pool-major plan rows
 // are written with coalesced 128-byte stores.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
 
 __global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
   __shared__ uint32_t tile[4][32][33];
@@ -123,12 +122,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const uint64_t* seeds, uint64
   const uint32_t pairs = N / 2 + 1;  // N values + the reserved one (N even)
   if (threadIdx.x == 0) {
     uint64_t sm = seed, s[4];
-    for (int k = 0; k < 4; ++k) {  // baselines.cpp:19-31 splitmix64 seeding
-      uint64_t z = (sm += 0x9e3779b97f4a7c15ULL);
-      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-      s[k] = z ^ (z >> 31);
-    }
+    for (int k = 0; k < 4; ++k) s[k] = splitmix64_dev(sm);  // baselines.cpp:19-31 seeding
     uint64_t draws = 0;
     auto next_u = [&]() -> double {  // uniform_next (baselines.cpp:33-49)
       const uint64_t w = rotl64(s[1] * 5, 7) * 9;
@@ -279,71 +273,6 @@ __global__ void reduce_consumer_kernel(const double* part_sums, const uint32_t* 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Box-Muller comparator (baselines.cpp:68-92): one thread per stream, the
-// stream's words consumed exactly as boxmuller_next does (two per pair,
-// u1 == 0 -> 2^-53, second value cached), transcendental part in fp32.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128)
-    boxmuller_kernel(const uint64_t* seeds, uint64_t seed_base, uint64_t n_streams,
-                     uint64_t count, double* part_sums, uint32_t* part_hist) {
-  __shared__ uint32_t hist[258];
-  __shared__ double red[4][4];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < 258; i += 128) hist[i] = 0;
-  __syncthreads();
-  Consumer<float> cons;
-  cons.hist = hist;
-  const uint64_t stream = uint64_t(blockIdx.x) * 128 + tid;
-  if (stream < n_streams) {
-    uint64_t sm = seeds ? seeds[stream] : seed_base + stream;
-    uint64_t s[4];
-    for (int k = 0; k < 4; ++k) {  // baselines.cpp:19-31
-      uint64_t z = (sm += 0x9e3779b97f4a7c15ULL);
-      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-      s[k] = z ^ (z >> 31);
-    }
-    for (uint64_t i = 0; i < count; i += 2) {
-      double u[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint64_t w = rotl64(s[1] * 5, 7) * 9;
-        const uint64_t t = s[1] << 17;
-        s[2] ^= s[0];
-        s[3] ^= s[1];
-        s[1] ^= s[2];
-        s[0] ^= s[3];
-        s[2] ^= t;
-        s[3] = rotl64(s[3], 45);
-        u[q] = static_cast<double>(w >> 11) * 0x1.0p-53;
-      }
-      if (u[0] == 0.0) u[0] = 0x1.0p-53;
-      const float r = sqrtf(-2.0f * logf(static_cast<float>(u[0])));
-      float sn, cs;
-      sincospif(2.0f * static_cast<float>(u[1]), &sn, &cs);
-      const float z[2] = {r * cs, r * sn};
-      cons.add_group(z, (i + 1 < count) ? 2 : 1);
-      if ((i & 127) == 126) cons.flush();  // fp32 partials over <= 128 values
-    }
-    cons.flush();
-  }
-  double v[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[k] = __dadd_rn(v[k], __shfl_down_sync(0xffffffffu, v[k], o));
-  if (lane == 0)
-    for (int k = 0; k < 4; ++k) red[k][warp] = v[k];
-  __syncthreads();
-  if (tid < 4) {
-    double acc = 0.0;
-    for (int w = 0; w < 4; ++w) acc = __dadd_rn(acc, red[tid][w]);
-    part_sums[blockIdx.x * 4 + tid] = acc;
-  }
-  for (int i = tid; i < 258; i += 128) part_hist[blockIdx.x * 258 + i] = hist[i];
-}
-
 cudaError_t launch_pool_large(int dtype, const FillArgs& a, uint64_t n_pools, cudaStream_t s);
 
 size_t large_state_bytes() { return sizeof(SState); }
@@ -415,15 +344,6 @@ cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void
   else
     materialize_kernel<double><<<unsigned(n_pools), 256, 0, s>>>(
         static_cast<const double*>(pools), st, static_cast<double*>(leftover), n_pools, N, mean);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_boxmuller(const uint64_t* d_seeds, uint64_t seed_base, uint64_t n_streams,
-                             uint64_t count, double* part_sums, uint32_t* part_hist,
-                             uint64_t n_blocks, int threads, cudaStream_t s) {
-  (void)threads;
-  boxmuller_kernel<<<unsigned(n_blocks), 128, 0, s>>>(d_seeds, seed_base, n_streams, count,
-                                                     part_sums, part_hist);
   return cudaGetLastError();
 }
 

@@ -44,7 +44,7 @@ __global__ void lg_prologue(const FillArgs a, uint64_t n_pools) {
   s.last_chi2 = st.last_chi2;
   s.last_r = st.r;
   s.last_scale = st.scale;
-  s.flags = st.flags;
+  s.flags = st.flags & ~kFlagChi2NonFinite;
   if (a.mode != kModePasses && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
   static_cast<SState*>(a.lg_state)[pool] = s;
 }
@@ -233,8 +233,8 @@ __global__ void lg_renorm_begin(const FillArgs a, const T* pool_buf, uint64_t N)
   const double ss = lg_neumaier(pool_buf + pool * N, N);
   if (threadIdx.x == 0) {
     SState& s = static_cast<SState*>(a.lg_state)[pool];
-    s.renorm_ok = ss > 0.0;
-    s.renorm_k = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
+    s.renorm_ok = !(ss <= 0.0);  // generator.cpp:347: a NaN sum still rescales
+    s.renorm_k = s.renorm_ok ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
   }
 }
 template <typename T>
@@ -296,6 +296,8 @@ __global__ void lg_epilogue(const FillArgs a, uint64_t n_pools) {
   so.pass_count = in.pass_count + a.n_passes;
   so.clamp_count = in.clamp_count + s.clamp;
   uint32_t flags = s.flags;
+  if (flags & kFlagChi2NonFinite) atomicOr(a.err_word, 1u);  // see pool_kernel's epilogue
+  flags &= ~kFlagChi2NonFinite;
   so.scale = s.last_scale;
   so.r = s.last_r;
   so.last_chi2 = s.last_chi2;

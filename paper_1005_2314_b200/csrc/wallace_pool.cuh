@@ -233,6 +233,15 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+// baselines.cpp:19-24 splitmix64 (seeding of UniformState, :26-31)
+__device__ __forceinline__ uint64_t splitmix64_dev(uint64_t& state) {
+  uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
 // ---------------------------------------------------------------------------
 // explicit-rounding arithmetic
 // ---------------------------------------------------------------------------
@@ -503,8 +512,9 @@ template <typename T, int N, int THREADS, bool LAT, bool NB = false>
 __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
   if (tid == 0) {
     const double ss = neumaier_sq<T, LAT>(cur, N);
-    s.renorm_ok = ss > 0.0;
-    s.renorm_k = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
+    // generator.cpp:347 skips only ss <= 0: a NaN sum still rescales (by NaN)
+    s.renorm_ok = !(ss <= 0.0);
+    s.renorm_k = s.renorm_ok ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
   }
   loop_bar<NB, THREADS>();
   if (s.renorm_ok) {
@@ -1394,7 +1404,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     s.x_last_bulk_set = 0;
     s.ready = 0;
     s.produced = 0;
-    s.flags = st.flags;
+    s.flags = st.flags & ~kFlagChi2NonFinite;
     if (MODE != kModePasses && !DEC && a.n_emit > 0) chain_draw(s, 0, a.chi2, a.sigma);
   }
   if constexpr (MODE == kModeConsume)
@@ -1929,6 +1939,10 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     so.pass_count = pass0 + a.n_passes;
     so.clamp_count = a.st_in[pool].clamp_count + s.clamp;
     uint32_t flags = s.flags;
+    // chi2_sample threw in the reference (chi2.cpp:29-31): report it to the
+    // host; the non-finite reserved value re-raises at every later emission
+    if (flags & kFlagChi2NonFinite) atomicOr(a.err_word, 1u);
+    flags &= ~kFlagChi2NonFinite;
     so.scale = s.last_scale;
     so.r = s.last_r;
     so.last_chi2 = s.last_chi2;

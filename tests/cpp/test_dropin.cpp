@@ -4,6 +4,7 @@
 // plus bit-for-bit stream comparison with the UNMODIFIED reference library
 // (oracle/_ref/libmaxent_ref.so, extern "C" shim in oracle/ref_shim.cpp).
 // Needs a GPU.  Exit code 0 = all checks passed.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -39,7 +40,46 @@ double ref_pass_coefficient(uint64_t n, int family, int mixing, const int32_t* i
                             uint64_t i, uint64_t j);
 int ref_cross_pool_fixed(uint64_t n, int family, int mixing, uint64_t seed, uint64_t pairs, uint32_t n_probes,
                          const uint64_t* out_i, const uint64_t* in_j, int expect_q, double* out);
+double ref_next_normal_ex(void* g, int* err);
+int ref_moments_suite(uint64_t seed, uint64_t n, int machine, char* out, uint64_t cap);
+double ref_pattern_rate(uint64_t pool_size, uint64_t seed, int pattern, uint64_t chunk, uint64_t total);
+void ref_uniform_bits(uint64_t seed, uint64_t n, uint64_t* out);
+void ref_polar(uint64_t seed, uint64_t n, double* out);
+void ref_boxmuller(uint64_t seed, uint64_t n, double* out);
+double ref_compute_a(uint64_t nu);
+void ref_wallace_variant(int id, int src[4], double sign[4], double entries[16]);
 }
+
+// ---- tools/cmd_test.cpp:40-60 compiled against the drop-in namespace -------
+// (the reference's statistic caller, unchanged but for the namespace alias)
+namespace maxent = wallace_b200;
+namespace wallace_b200::cli {  // tools/cmd_test.cpp's `namespace maxent::cli`
+static std::string run_moments_suite(uint64_t seed, std::size_t n, bool machine) {
+  std::string all;
+  auto print = [&](const std::vector<maxent::TestReport>& rs) {
+    for (const auto& r : rs) all += (machine ? r.machine() : r.text()) + "\n";
+  };
+  {
+    maxent::GeneratorConfig cfg;
+    cfg.seed = seed;
+    maxent::Generator gen(cfg);
+    print(moment_reports(moments(gen.fill(n)), "wallace4"));
+  }
+  {
+    maxent::BaselineState s(seed);
+    std::vector<double> buf(n);
+    for (auto& v : buf) v = polar_next(s);
+    print(moment_reports(moments(buf), "polar"));
+  }
+  {
+    maxent::BaselineState s(seed);
+    std::vector<double> buf(n);
+    for (auto& v : buf) v = boxmuller_next(s);
+    print(moment_reports(moments(buf), "boxmuller"));
+  }
+  return all;
+}
+}  // namespace wallace_b200::cli
 
 namespace wb = wallace_b200;
 
@@ -448,6 +488,149 @@ int main() {
       same = mine[k].statistic == out4[4 * k] && mine[k].expected == out4[4 * k + 1] &&
              mine[k].std_error == out4[4 * k + 2] && mine[k].z_score == out4[4 * k + 3];
     CHECK(same);
+  }
+  // cmd_test's moments suite through `namespace maxent = wallace_b200`: the
+  // report lines are byte-equal to the reference's (machine and text forms)
+  for (uint64_t seed : {uint64_t(1), uint64_t(42)}) {
+    std::vector<char> buf(1 << 16);
+    for (int machine = 0; machine < 2; ++machine) {
+      const int len = ref_moments_suite(seed, 100000, machine, buf.data(), buf.size());
+      CHECK(len > 0);
+      const std::string mine = maxent::cli::run_moments_suite(seed, 100000, machine != 0);
+      CHECK(mine == std::string(buf.data()));
+      if (seed == 1 && machine) std::printf("%s", mine.c_str());
+    }
+  }
+  // the L1a free functions of the namespace (baselines / chi2 / transforms)
+  {
+    maxent::UniformState u(42);
+    std::vector<uint64_t> w(100);
+    ref_uniform_bits(42, 100, w.data());
+    bool ok = true;
+    for (int i = 0; i < 100; ++i) ok = ok && maxent::uniform_bits(u) == w[static_cast<std::size_t>(i)];
+    CHECK(ok && u.draws == 100);
+    std::vector<double> rp(1001), rb(1001);
+    ref_polar(7, 1001, rp.data());
+    ref_boxmuller(7, 1001, rb.data());
+    maxent::BaselineState sp(7), sb(7);
+    for (int i = 0; i < 1001; ++i) {
+      ok = ok && maxent::polar_next(sp) == rp[static_cast<std::size_t>(i)];
+      ok = ok && maxent::boxmuller_next(sb) == rb[static_cast<std::size_t>(i)];
+    }
+    CHECK(ok);
+    const auto params = maxent::Chi2Params::for_nu(1024);
+    CHECK(params.a_value == ref_compute_a(1024));
+    int rc = 0;
+    bool cl = false;
+    CHECK(maxent::chi2_sample(-0.3, params, maxent::Chi2Method::cubic_a, &cl) ==
+          ref_chi2_sample(-0.3, 1024, 2, &rc));
+    CHECK_THROWS_WITH(maxent::chi2_sample(std::numeric_limits<double>::quiet_NaN(), params,
+                                          maxent::Chi2Method::cubic_a),
+                      maxent::InvalidParameterError, "x must be finite");
+    CHECK_THROWS_AS(maxent::Chi2Params::for_nu(7), maxent::InvalidParameterError);
+    bool vok = true;
+    for (int id = 0; id < 384; ++id) {
+      const auto m = maxent::wallace_variant(id);
+      int src[4];
+      double sg[4], e[16];
+      ref_wallace_variant(id, src, sg, e);
+      for (int k = 0; k < 4; ++k) {
+        vok = vok && m.source_row[static_cast<std::size_t>(k)] == src[k] && m.row_sign[static_cast<std::size_t>(k)] == sg[k];
+        for (int j = 0; j < 4; ++j) vok = vok && m.entries[static_cast<std::size_t>(k)][static_cast<std::size_t>(j)] == e[4 * k + j];
+      }
+    }
+    CHECK(vok);
+    const auto col = maxent::apply_wallace4({1, 0, 0, 0}, maxent::wallace_a1());
+    CHECK(col[0] == 0.5 && col[1] == 0.5 && col[2] == 0.5 && col[3] == -0.5);
+    CHECK(maxent::default_stride(256) == 87 && maxent::default_stride(16) == 7);
+    const auto half = maxent::rotation_from_t(0.5);
+    CHECK(half.c == 0.6 && half.s == 0.8 && maxent::rotation_t_table().size() == 16);
+  }
+  // chi2_sample's throw reaches the drop-in where the reference throws:
+  // inject a non-finite pool, then next_normal / fill until the reference's
+  // next_normal throws; the drop-in throws on the same value
+  for (int how = 0; how < 2; ++how) {
+    wb::GeneratorConfig c = cfg_of(1024, 11);
+    wb::Generator g(c);
+    Ref r(c);
+    CHECK(same_bits(g.fill(3000), r.fill(3000)));
+    std::vector<double> inj(1024);
+    for (int i = 0; i < 1024; ++i) inj[static_cast<std::size_t>(i)] = std::cos(0.1 * i);
+    inj[1023] = std::numeric_limits<double>::infinity();
+    g.inject_pool(inj);
+    ref_inject_pool(r.g, inj.data(), 1024);
+    long ref_at = -1, mine_at = -1;
+    for (long i = 0; i < 200000 && ref_at < 0; ++i) {
+      int err = 0;
+      ref_next_normal_ex(r.g, &err);
+      if (err) ref_at = i;
+    }
+    try {
+      if (how == 0) {
+        for (long i = 0; i < 200000; ++i, mine_at = i) g.next_normal();
+      } else {
+        for (long i = 0; i < 200000; i += 100, mine_at = i) g.fill(100);
+      }
+      mine_at = -1;
+    } catch (const wb::InvalidParameterError& e) {
+      CHECK(std::string(e.what()) == "chi2_sample: x must be finite");
+    }
+    CHECK(ref_at > 0);
+    if (how == 0) CHECK(mine_at == ref_at);
+    else CHECK(mine_at == (ref_at / 100) * 100);
+    CHECK_THROWS_AS(g.next_normal(), wb::InvalidParameterError);  // and again, as the reference
+  }
+  // the look-ahead rolls back exactly: deep inside a block, every
+  // state-observing call sees the reference's state
+  {
+    wb::GeneratorConfig c = cfg_of(512, 123);
+    c.discard_every = 2;
+    wb::Generator g(c);
+    Ref r(c);
+    bool ok = true;
+    for (int round = 0; round < 3; ++round) {
+      for (int i = 0; i < 70001; ++i) ok = ok && g.next_normal() == ref_next_normal(r.g);
+      uint64_t pc, dr, cl;
+      double ss, rpv;
+      ref_get_stats(r.g, &pc, &dr, &cl, &ss, &rpv);
+      ok = ok && g.pass_count() == pc && g.uniform_draws() == dr && g.chi2_clamp_count() == cl;
+      g.step_pass();
+      ref_step_pass(r.g);
+      ok = ok && same_bits(g.fill(33333), r.fill(33333));
+    }
+    CHECK(ok);
+  }
+  // the reference's own call patterns (bench.cpp:43-59 fill(65536),
+  // cmd_gen.cpp:127-134 fill(16384), next_normal) are at least as fast as
+  // the reference on one core
+  {
+    const uint64_t total = 1 << 24;
+    const struct {
+      int pattern;
+      uint64_t chunk;
+      const char* name;
+    } pats[] = {{0, 0, "next_normal"}, {1, 16384, "fill(16384)"}, {1, 65536, "fill(65536)"}};
+    for (const auto& p : pats) {
+      const double ref_rate = ref_pattern_rate(1024, 1, p.pattern, p.chunk, total);
+      wb::Generator g(cfg_of(1024, 1));
+      std::vector<double> buf(p.chunk > 0 ? p.chunk : 1);
+      double sink = 0.0;
+      g.fill(1);  // first block
+      const auto t0 = std::chrono::steady_clock::now();
+      if (p.pattern == 0) {
+        for (uint64_t i = 0; i < total; ++i) sink += g.next_normal();
+      } else {
+        for (uint64_t i = 0; i < total; i += p.chunk) {
+          g.fill(std::span<double>(buf));
+          sink += buf[0];
+        }
+      }
+      const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      const double rate = static_cast<double>(total) / dt;
+      std::printf("drop-in %-12s %.3e values/s  (reference 1 core %.3e, x%.2f)%s\n", p.name, rate, ref_rate,
+                  rate / ref_rate, sink == 1.5 ? " " : "");
+      CHECK(rate >= ref_rate);
+    }
   }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

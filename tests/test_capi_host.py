@@ -147,3 +147,84 @@ def test_pass_coefficient_vs_reference(ref, fam, mix):
             for i in range(n):
                 for j in range(n):
                     assert pb.pass_coefficient(cfg, plan, i, j) == R.ref_pass_coefficient(n, fam, mix, ci, co, i, j)
+
+
+# ---- the reference's L1a layer through the C-ABI (host, bit-identical) -----------
+def test_uniform_polar_boxmuller_host_vs_reference(ref):
+    """UniformState / uniform_bits / polar_next / boxmuller_next
+    (baselines.cpp:19-92) exported by the library equal the reference's."""
+    L = _capi.load()
+    R = ref.ref_lib()
+    for seed in (0, 1, 42, 0xDEADBEEF, 2**64 - 1):
+        u = _capi.wallace_uniform_state()
+        L.wallace_uniform_seed(seed, C.byref(u))
+        want = np.empty(1000, dtype=np.uint64)
+        R.ref_uniform_bits(seed, 1000, want.ctypes.data_as(C.POINTER(C.c_uint64)))
+        got = [L.wallace_uniform_bits(C.byref(u)) for _ in range(1000)]
+        assert got == [int(w) for w in want] and u.draws == 1000
+        for method, ref_fn in (("polar_next", R.ref_polar), ("boxmuller_next", R.ref_boxmuller)):
+            want = np.empty(2001, dtype=np.float64)
+            ref_fn(seed, 2001, want.ctypes.data_as(C.POINTER(C.c_double)))
+            b = pb.BaselineState(seed)
+            got = np.array([getattr(b, method)() for _ in range(2001)])
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (seed, method)
+    # the frozen uniform doubles (test_baselines.cpp:61-74)
+    u = _capi.wallace_uniform_state()
+    L.wallace_uniform_seed(42, C.byref(u))
+    assert L.wallace_uniform_next(C.byref(u)) == 0.083862971059882163
+    assert L.wallace_uniform_next(C.byref(u)) == 0.37898025066266861
+
+
+def test_boxmuller_pair_domain():
+    L = _capi.load()
+    z1, z2 = C.c_double(), C.c_double()
+    assert L.wallace_boxmuller_pair(1.0, 0.0, C.byref(z1), C.byref(z2)) == 0
+    assert z1.value == 0.0 and z2.value == 0.0
+    for u1, u2 in ((0.0, 0.5), (1.5, 0.5), (0.5, 1.0), (0.5, -0.1), (float("nan"), 0.5)):
+        assert L.wallace_boxmuller_pair(u1, u2, C.byref(z1), C.byref(z2)) == _capi.WALLACE_ERR_INVALID_PARAM
+
+
+def test_chi2_helpers_vs_reference(ref):
+    """compute_a / Chi2Params / chi2_sample (chi2.cpp:11-59) and the
+    reference's spot values (test_chi2.cpp:70-127)."""
+    L = _capi.load()
+    R = ref.ref_lib()
+    for nu in (8, 64, 1024, 2048, 4096, 10**6):
+        a = C.c_double()
+        assert L.wallace_chi2_params(nu, C.byref(a)) == 0
+        assert a.value == R.ref_compute_a(nu)
+        rng = np.random.default_rng(nu)
+        for x in np.concatenate([rng.normal(size=200) * 3, [-60.0, -45.0, 0.0, 1e3]]):
+            for m in (0, 1, 2):
+                out, cl = C.c_double(), C.c_int32()
+                rc = C.c_int()
+                assert L.wallace_chi2_sample(float(x), nu, a.value, m, C.byref(cl), C.byref(out)) == 0
+                want = R.ref_chi2_sample(float(x), nu, m, C.byref(rc))
+                assert out.value == want and cl.value == rc.value, (nu, x, m)
+    assert abs(pb.chi2_sample(0.0, 1024, 0)[0] - 1023.5) <= 1e-9  # test_chi2.cpp:70-91
+    assert abs(pb.chi2_sample(0.0, 1024, 1)[0] - 1023.3334) < 1e-3
+    with pytest.raises(pb.InvalidParameterError, match="nu must be >= 8"):
+        pb.chi2_sample(0.0, 7)
+    with pytest.raises(pb.InvalidParameterError, match="x must be finite"):
+        pb.chi2_sample(float("inf"), 1024)
+
+
+def test_variants_and_rotation_vs_reference(ref):
+    """wallace_variant (transforms.cpp:76-97) and rotation_from_t (:52-70)."""
+    L = _capi.load()
+    R = ref.ref_lib()
+    for vid in range(384):
+        e1, s1, g1 = (C.c_double * 16)(), (C.c_uint8 * 4)(), (C.c_double * 4)()
+        assert L.wallace_variant(vid, e1, s1, g1) == 0
+        src, sg, e2 = (C.c_int * 4)(), (C.c_double * 4)(), (C.c_double * 16)()
+        R.ref_wallace_variant(vid, src, sg, e2)
+        assert list(e1) == list(e2) and list(s1) == list(src) and list(g1) == list(sg)
+    assert L.wallace_variant(384, None, None, None) == _capi.WALLACE_ERR_INVALID_PARAM
+    t, c, s = (C.c_double * 16)(), (C.c_double * 16)(), (C.c_double * 16)()
+    L.wallace_rotation_table(t, c, s)
+    cc, ss = C.c_double(), C.c_double()
+    for k in range(16):
+        assert L.wallace_rotation_from_t(t[k], C.byref(cc), C.byref(ss)) == 0
+        assert (cc.value, ss.value) == (c[k], s[k])
+    assert L.wallace_rotation_from_t(0.5, C.byref(cc), C.byref(ss)) == 0 and (cc.value, ss.value) == (0.6, 0.8)
+    assert L.wallace_rotation_from_t(float("inf"), C.byref(cc), C.byref(ss)) == _capi.WALLACE_ERR_INVALID_PARAM

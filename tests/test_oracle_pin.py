@@ -243,3 +243,25 @@ def test_oracle_families_f32_restatement_tracks_reference(ref, fam, mix):
     a = RefGen(c).fill(1 << 19)
     f = OracleGen(c, "f32").fill(1 << 19).astype(np.float64)
     assert np.max(np.abs(f - a)) <= 1e-4
+
+
+# ---- chi2_sample's throw (chi2.cpp:29-31) modelled by the oracle ----------
+from nonfinite_cases import CASES, replay, same_nan_aware  # noqa: E402
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_oracle_throw_matches_reference(ref, case):
+    """The oracle's modelled throw is the reference's: same call, same
+    message, same values before it (f64)."""
+    kw, pos, pre, chunks = CASES[case]
+    v = np.linspace(-1.5, 1.5, kw["pool_size"])
+    v[pos] = np.inf
+    r_outs, r_k, r_msg, rg = replay(lambda: RefGen(Cfg(seed=22, **kw)), pre, v, chunks)
+    o_outs, o_k, o_msg, og = replay(lambda: OracleGen(Cfg(seed=22, **kw), "f64"), pre, v, chunks)
+    assert r_k == o_k and r_msg == o_msg == "chi2_sample: x must be finite"
+    for k in range(r_k):
+        same_nan_aware(o_outs[k], r_outs[k], f"call {k}")
+    rs, os_ = rg.stats(), og.stats()
+    assert rs["pass_count"] == os_["pass_count"] and rs["uniform_draws"] == os_["uniform_draws"]
+
+
