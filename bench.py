@@ -209,21 +209,20 @@ def run_reference(args):
     return 0
 
 
-def run_ours(args):
+def measure(cfg_id, steps, warmup, e2e_steps, pools_override=0, rank=0, world=1, dist=None, sustained=0):
+    """One configured job on this rank's GPU: the device-timed step, the
+    pool_kernel launches inside it (roofline), the end-to-end rate through
+    the C-ABI into pinned host memory, and optionally a sustained run."""
+    import ctypes as C
+
     import numpy as np
     import torch
 
     import paper_1005_2314_b200 as pb
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
-    cfg = dict(CONFIGS[args.config])
-    if args.pools:
-        cfg["pools"] = args.pools
+    cfg = dict(CONFIGS[cfg_id])
+    if pools_override:
+        cfg["pools"] = pools_override
     n_pools, count, dtype = cfg["pools"], cfg["count"], cfg["dtype"]
     esize = 4 if dtype == "f32" else 8
     seeds = np.arange(1 + rank * n_pools, 1 + (rank + 1) * n_pools, dtype=np.uint64)
@@ -235,14 +234,15 @@ def run_ours(args):
     batch.snapshot()
     consume = cfg.get("consume", False)
     out = None if consume else torch.empty((n_pools, count), dtype=batch.torch_dtype, device="cuda")
+    sums_hist = {}
 
     def step():
         if consume:
-            batch.consume_from_snapshot(count)  # synchronous; replays the seeded job
+            sums_hist["r"] = batch.consume_from_snapshot(count)  # synchronous; replays the seeded job
         else:
             batch.fill_from_snapshot_into(out)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     if dist:
@@ -250,21 +250,21 @@ def run_ours(args):
     launches0 = pb.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    import ctypes as C
     L = pb._capi.load()
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         # per-launch CUDA events on the handle's stream bracket every
         # pool_kernel / plan_kernel launch of the timed steps (roofline below)
         L.wallace_profile_begin(batch.h)
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
     pool_ms, plan_ms = C.c_double(), C.c_double()
     pool_n, plan_n = C.c_uint64(), C.c_uint64()
     L.wallace_profile_end(batch.h, C.byref(pool_ms), C.byref(pool_n), C.byref(plan_ms), C.byref(plan_n))
+    batch.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = pb.kernel_launches() - launches0
     if dist:
@@ -272,83 +272,95 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
     variates_rank = n_pools * count
-    value = world * variates_rank * args.steps / (ms / 1e3)
+    value = world * variates_rank * steps / (ms / 1e3)
 
     # dominant kernel timing: pool_kernel launches of the timed steps
     peak, peak_src = measured_peaks()
     per_launch_ms = pool_ms.value / max(1, pool_n.value)
-    launches_per_step = pool_n.value / args.steps
+    launches_per_step = pool_n.value / steps
     alg_bytes = variates_rank * esize / launches_per_step  # written per launch
-    roofline = None
     if not consume:
         achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-        tr = ncu_traffic(args.config)
-        # The path only writes HBM, so also time a store-only pass over the same
-        # output buffer on this box (torch's vectorised fill; tools/probes/
-        # store_peak.cu measured 6816 GB/s for 128-bit streaming stores).
-        fills = []
-        for _ in range(5):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            out.fill_(0.5)
-            b.record(stream)
-            b.synchronize()
-            fills.append(a.elapsed_time(b))
-        store_gbs = out.numel() * out.element_size() / (min(fills) / 1e3) / 1e9
+        tr = ncu_traffic(cfg_id)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
                     "kernel": "pool_kernel", "kernel_ms": per_launch_ms,
                     "kernel_share_of_step": pool_ms.value / max(1e-9, pool_ms.value + plan_ms.value),
-                    "algorithmic_bytes_per_launch": alg_bytes,
-                    "store_only_peak": store_gbs, "frac_of_store_only_peak": achieved / store_gbs}
-
-    if consume:
+                    "algorithmic_bytes_per_launch": alg_bytes}
+    else:
         # the consumer kernel's own device time (the step also waits for the
-        # 2 KB result on the host, which adds host jitter to ms_per_step)
+        # 2 KB result on the host)
         roofline = {"bound": "smem+issue (no output written)", "kernel": "pool_kernel (consume)",
                     "kernel_ms": per_launch_ms, "launches_per_step": launches_per_step,
                     "variates_per_s_kernel": variates_rank / launches_per_step / (per_launch_ms / 1e3)}
+    res = {"cfg": cfg, "value": value, "ms": ms, "steps": steps, "roofline": roofline, "clocks": clk.summary(),
+           "launches": launches, "init_s": init_s, "variates_rank": variates_rank, "esize": esize}
 
-    # end to end through the C-ABI into pinned host memory
+    if sustained and not consume:
+        # the same step back to back for `sustained` steps (power/thermal
+        # steady state; the headline above is a short burst)
+        torch.cuda.synchronize()
+        with ClockSampler(torch.cuda.current_device()) as sclk:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(sustained):
+                step()
+            b.record(stream)
+            torch.cuda.synchronize()
+        sms = a.elapsed_time(b)
+        res["sustained"] = {"steps": sustained, "ms_per_step": sms / sustained,
+                            "value": variates_rank * sustained / (sms / 1e3),
+                            "frac": variates_rank * esize / (sms / sustained / 1e3) / 1e9 / peak,
+                            "clocks": sclk.summary()}
+
+    # end to end through the C-ABI (host memory, every step's transfer timed)
     e2e = None
-    if rank == 0 and consume and not args.no_e2e:
-        # the consumer's result (4 sums + 258 counts) is its only output
-        e2e_steps = max(1, min(args.e2e_steps, args.steps))
-        t1 = time.perf_counter()
-        for _ in range(e2e_steps):
-            batch.consume_from_snapshot(count)
-        dt = (time.perf_counter() - t1) / e2e_steps
-        e2e = {"value": variates_rank / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": 4 * 8 + 258 * 8,
-               "api": "wallace_consume_from_snapshot (C-ABI), wall clock", "s_per_step": dt}
-    if rank == 0 and not consume and not args.no_e2e:
-        try:
-            host = torch.empty((n_pools, count), dtype=batch.torch_dtype, pin_memory=True)
-            e2e_steps = max(1, min(args.e2e_steps, args.steps))
-            batch.fill_host_ptr(host.data_ptr(), count)  # warm-up
+    if rank == 0 and e2e_steps > 0:
+        if consume:
+            # the consumer's result (4 sums + 258 counts) is its only output
             t1 = time.perf_counter()
             for _ in range(e2e_steps):
-                batch.fill_host_ptr(host.data_ptr(), count)
+                batch.consume_from_snapshot(count)
             dt = (time.perf_counter() - t1) / e2e_steps
             e2e = {"value": variates_rank / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": variates_rank * esize,
-                   "api": "wallace_fill_host (C-ABI) into pinned host memory, wall clock",
-                   "s_per_step": dt}
-            del host
-        except Exception as ex:  # noqa: BLE001
-            e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+                   "d2h_bytes_per_step": 4 * 8 + 258 * 8,
+                   "api": "wallace_consume_from_snapshot (C-ABI), wall clock", "s_per_step": dt}
+        else:
+            try:
+                host = torch.empty((n_pools, count), dtype=batch.torch_dtype, pin_memory=True)
+                batch.fill_host_ptr(host.data_ptr(), count)  # warm-up
+                t1 = time.perf_counter()
+                for _ in range(e2e_steps):
+                    batch.fill_host_ptr(host.data_ptr(), count)
+                dt = (time.perf_counter() - t1) / e2e_steps
+                e2e = {"value": variates_rank / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": variates_rank * esize,
+                       "api": "wallace_fill_host (C-ABI) into pinned host memory, wall clock",
+                       "s_per_step": dt,
+                       "note": "a generator has no per-step input: the seeds and pool state are resident "
+                               "from construction, so h2d is 0; every step copies its whole output "
+                               "to the host (the PCIe bound)"}
+                del host
+            except Exception as ex:  # noqa: BLE001
+                e2e = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+    res["e2e"] = e2e
 
-    comparator = None
+    if consume and dist:
+        # the job's result over all ranks: the only exchange of the sharded
+        # job (4 sums + 258 counts), a deterministic rank-order fold
+        from paper_1005_2314_b200.shard import reduce_consumer
+        js, jh = reduce_consumer(*sums_hist["r"])
+        rep = pb.moment_reports(js, world * n_pools * count)
+        res["job_result"] = {"values": int(jh.sum()), "moment_z": {k: round(v[3], 3) for k, v in rep.items()},
+                             "reduction": "shard.reduce_consumer (all_gather + rank-order fold)"}
     if consume and rank == 0:
-        # BASELINE config 5: the same statistics from a Box-Muller kernel fed
-        # by the same per-pool uniform streams (baselines.cpp:80-92)
+        # BASELINE config 5: the same statistics from Box-Muller streams fed
+        # by the same per-pool uniform streams (baselines.cpp:80-92), fp64 on
+        # the device like the reference, timed on the device
         import math
-        sums, hist = batch.consume_from_snapshot(count)
+        sums, hist = sums_hist["r"]
         n = n_pools * count
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        bsums, bhist = pb.boxmuller_consume(n_streams=n_pools, count=count, seeds=seeds)
-        bm_s = time.perf_counter() - t1
+        bsums, bhist, bm_ms = pb.baseline_consume("boxmuller", n_pools, count, seeds=seeds)
 
         def zs(sm):
             return {k: round(v[3], 3) for k, v in pb.moment_reports(sm, n).items()}
@@ -362,11 +374,53 @@ def run_ours(args):
             dof = int(ok.sum()) - 1
             return round((chi2 - dof) / math.sqrt(2 * dof), 3)
 
-        comparator = {"wallace": {"variates_per_s": value, "moment_z": zs(sums), "hist_chi2_z": hist_z(hist)},
-                      "boxmuller": {"variates_per_s": n / bm_s, "moment_z": zs(bsums),
-                                    "hist_chi2_z": hist_z(bhist),
-                                    "note": "fp32 transcendentals, same UniformState(seed) streams, "
-                                            "wall clock incl. launch and 2 KB D2H"}}
+        res["comparator"] = {
+            "wallace": {"variates_per_s_kernel": roofline["variates_per_s_kernel"], "moment_z": zs(sums),
+                        "hist_chi2_z": hist_z(hist)},
+            "boxmuller": {"variates_per_s_kernel": n / (bm_ms / 1e3), "kernel_ms": bm_ms,
+                          "moment_z": zs(bsums), "hist_chi2_z": hist_z(bhist),
+                          "note": "fp64 like boxmuller_next (CUDA log/sincos), the same UniformState(seed) "
+                                  "streams, device time of the fused kernel"},
+            "wallace_over_boxmuller": roofline["variates_per_s_kernel"] / (n / (bm_ms / 1e3))}
+    batch.close()
+    del out
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    r = measure(args.config, args.steps, args.warmup, 0 if args.no_e2e else max(1, min(args.e2e_steps, args.steps)),
+                args.pools, rank, world, dist, sustained=0 if args.no_sustained or world > 1 else args.sustained)
+    cfg = r["cfg"]
+    n_pools, count, dtype = cfg["pools"], cfg["count"], cfg["dtype"]
+
+    if not cfg.get("consume", False):
+        # the path only writes HBM: a store-only pass over an output-sized
+        # buffer on this box beside the copy peak (torch's vectorised fill)
+        out = torch.empty((n_pools, count), dtype=torch.float32 if dtype == "f32" else torch.float64,
+                          device="cuda")
+        stream = torch.cuda.current_stream()
+        fills = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out.fill_(0.5)
+            b.record(stream)
+            b.synchronize()
+            fills.append(a.elapsed_time(b))
+        store_gbs = out.numel() * out.element_size() / (min(fills) / 1e3) / 1e9
+        r["roofline"]["store_only_peak"] = store_gbs
+        r["roofline"]["frac_of_store_only_peak"] = r["roofline"]["achieved"] / store_gbs
+        del out
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -388,20 +442,41 @@ def run_ours(args):
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "error": str(ex)[:200]}
 
+    # every other BASELINE config, measured in this process (rank 0, one GPU)
+    others = {}
+    if rank == 0 and world == 1 and not args.no_configs:
+        for c in (1, 2, 3, 4, 5):
+            if c == args.config:
+                continue
+            o = measure(c, args.config_steps, 3, 0 if args.no_e2e else 1)
+            line = {"workload": o["cfg"]["name"], "dtype": o["cfg"]["dtype"], "value": o["value"],
+                    "unit": UNIT, "ms_per_step": o["ms"] / o["steps"], "steps": o["steps"],
+                    "kernel_ms": o["roofline"]["kernel_ms"], "clocks": o["clocks"], "e2e": o["e2e"]}
+            if "frac" in o["roofline"]:
+                line["roofline_frac"] = o["roofline"]["frac"]
+                line["achieved_gbs"] = o["roofline"]["achieved"]
+            if "comparator" in o:
+                line["comparator"] = o["comparator"]
+            others[f"cfg{c}"] = line
+
     if rank == 0:
+        ms = r["ms"]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": dtype,
             "data": "synthetic (pools seeded by the reference's Polar init)",
             "config": {"workload": cfg["name"], "pools_per_gpu": n_pools, "pool_size": cfg["kw"]["pool_size"],
-                       "variates_per_step_per_gpu": variates_rank,
+                       "variates_per_step_per_gpu": r["variates_rank"],
                        "l2": "output per step (16 GiB for cfg2) >> 126 MB L2; no flush needed",
                        "step": "replay of the seeded job from the device snapshot"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            **({"comparator": comparator} if comparator else {}),
-            "clocks": clk.summary(), "gpu_launches": launches,
-            "init_s": init_s,
+            "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"],
+            **({"comparator": r["comparator"]} if "comparator" in r else {}),
+            **({"job_result": r["job_result"]} if "job_result" in r else {}),
+            **({"sustained": r["sustained"]} if "sustained" in r else {}),
+            "clocks": r["clocks"], "gpu_launches": r["launches"],
+            "init_s": r["init_s"],
+            **({"configs": others} if others else {}),
         }
         print(json.dumps(line))
     if dist:
@@ -421,6 +496,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--pools", type=int, default=0, help="override pools per GPU (profiling only)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--config-steps", type=int, default=10, help="timed steps of each other config")
+    ap.add_argument("--sustained", type=int, default=300, help="back-to-back steps of the sustained block")
+    ap.add_argument("--no-sustained", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

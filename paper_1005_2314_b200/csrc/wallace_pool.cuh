@@ -406,6 +406,7 @@ struct SState {
   uint32_t ready;      // chain-warp kernels: S/r/scale of every emission <= ready published
   uint32_t produced;   // kModeFillLat: emissions whose (x_last, sum_sq) are in the ring
   uint32_t end_off;    // kModeFillLat: the compute threads' final buffer offset
+  int32_t closed;      // owner_chain closed this slot last: last_chi2 / last_scale are its S / scale
 };
 
 // S, r, scale of the emission in `slot` from the current reserved value.
@@ -425,10 +426,37 @@ __device__ __forceinline__ void chain_rescale(SState& s, int slot, const Chi2Con
 }
 // bookkeeping at the end of emission `slot` (generator.cpp:373-375)
 __device__ __forceinline__ void chain_close(SState& s, int slot, double x_last) {
+  s.closed = -1;
   s.reserved_prev = __dmul_rn(x_last, s.r[slot]);
   s.last_chi2 = s.S[slot];
   s.last_r = s.r[slot];
   s.last_scale = s.scale[slot];
+}
+
+// chain_close + chain_draw of the owner thread (the one holding pool element
+// N-1), with one shared-memory round trip: r of this emission and sum_sq
+// are loaded together up front, and the dependent fp64 chain (reserved,
+// chi2, S/sum_sq, sqrt, scale) then runs in registers; the results are
+// stored without being read back.  last_chi2 / last_scale are S / scale of
+// `slot` as drawn (or rescaled) and stay where they are; the epilogue and
+// the next close read them from the slot (SState::closed).
+__device__ __forceinline__ void owner_chain(SState& s, int slot, double x_last, bool next, const Chi2Consts& c,
+                                            double sigma) {
+  const double r_e = s.r[slot];
+  const double ss = s.sum_sq;
+  // generator.cpp:373-375
+  const double reserved = __dmul_rn(x_last, r_e);
+  s.reserved_prev = reserved;
+  s.last_r = r_e;
+  s.closed = slot;
+  if (next) {
+    // generator.cpp:358-364 for the next emission
+    const double S = c.disable ? ss : chi2_draw(reserved, c, s.clamp, s.flags);
+    const double r = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(S, ss)) : 0.0;
+    s.S[slot ^ 1] = S;
+    s.r[slot ^ 1] = r;
+    s.scale[slot ^ 1] = __dmul_rn(sigma, r);
+  }
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
@@ -1399,6 +1427,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     s.last_chi2 = st.last_chi2;
     s.last_r = st.r;
     s.last_scale = st.scale;
+    s.closed = -1;
     s.clamp = 0;
     s.zero_seen = 0;
     s.x_last_bulk_set = 0;
@@ -1730,8 +1759,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
               s.x_last_bulk_set = 1;
             }
           } else {
-            chain_close(s, slot, static_cast<double>(x_last));
-            if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
+            owner_chain(s, slot, static_cast<double>(x_last), e + 1 < a.n_emit, a.chi2, a.sigma);
           }
         }
         // the bulk copy of the previous emission must have read its source
@@ -1768,10 +1796,8 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
             // generator.cpp:373-375 for this emission and S/r/scale of the
             // next one, off the barrier's critical path: the next reader is
             // the next emission, behind at least one more barrier
-            if (DEFER && tid == G::OWNER && WB_ABLATE != 3) {
-              chain_close(s, slot, static_cast<double>(x_last));
-              if (e + 1 < a.n_emit) chain_draw(s, slot ^ 1, a.chi2, a.sigma);
-            }
+            if (DEFER && tid == G::OWNER && WB_ABLATE != 3)
+              owner_chain(s, slot, static_cast<double>(x_last), e + 1 < a.n_emit, a.chi2, a.sigma);
           }
         }
         if (G::CHAINW && fast && tid == G::CT) {
@@ -1898,8 +1924,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     }
     if (bulk_pending && tid == 0) bulk_wait_all();  // smem must outlive the copies
     if (STAGED_OK && lane == 0) bulk_wait_all();
-    if (DEFER) __syncthreads();  // the owner's last chain precedes the epilogue
-    if (G::CHAINW) __syncthreads();  // the chain warp's last close precedes the epilogue
+    __syncthreads();  // the owner's last chain precedes the epilogue
   }
   T* const cur = reinterpret_cast<T*>(pbase + cur_off + sh);
 
@@ -1943,9 +1968,9 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     // host; the non-finite reserved value re-raises at every later emission
     if (flags & kFlagChi2NonFinite) atomicOr(a.err_word, 1u);
     flags &= ~kFlagChi2NonFinite;
-    so.scale = s.last_scale;
+    so.scale = s.closed >= 0 ? s.scale[s.closed] : s.last_scale;
     so.r = s.last_r;
-    so.last_chi2 = s.last_chi2;
+    so.last_chi2 = s.closed >= 0 ? s.S[s.closed] : s.last_chi2;
     if (MODE != kModePasses && a.n_emit > 0) {
       so.cursor = a.last_limit;
       flags &= ~kFlagLeftover;

@@ -61,3 +61,51 @@ def test_two_rank_consumer_reduction():
     ws, wh = consume_pools(Cfg(pool_size=1024), "f32", np.arange(1, 17, dtype=np.uint64), 4096)
     assert np.array_equal(np.array(h0, dtype=np.uint64), wh)
     np.testing.assert_allclose(np.array(s0), ws, rtol=1e-12, atol=1e-9)
+
+
+def _gpu_worker(rank, world, port, n_pools, count, out):
+    """One rank of a sharded config-5 style job on cuda:0: the device
+    consumer over this rank's pools, then the deterministic gloo reduction
+    (the kernels of the two processes never wait on each other)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1005_2314_b200 as pb
+    from paper_1005_2314_b200.shard import reduce_consumer, shard_seeds
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seeds = shard_seeds(n_pools, rank, world)
+    b = pb.PoolBatch(pb.GeneratorConfig(pool_size=1024, discard_every=1), n_pools=len(seeds), seeds=seeds)
+    sums, hist = b.consume(count)
+    b.close()
+    rs, rh = reduce_consumer(sums, hist)
+    out[rank] = (rs.tolist(), [int(x) for x in rh])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_gpu_consume_equals_single_process(cuda):
+    """two processes, each running PoolBatch.consume on its
+    shard_seeds range on the GPU, reduced with shard.reduce_consumer, give
+    the single-process GPU consume of the whole job: histogram exactly, sums
+    to fold-order rounding, identical on both ranks."""
+    import paper_1005_2314_b200 as pb
+    n_pools, count = 600, 3 * 1023 + 17
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    mp.start_processes(_gpu_worker, args=(world, port, n_pools, count, out), nprocs=world, join=True,
+                       start_method="spawn")
+    s0, h0 = out[0]
+    s1, h1 = out[1]
+    assert s0 == s1 and h0 == h1
+    b = pb.PoolBatch(pb.GeneratorConfig(pool_size=1024, discard_every=1), n_pools=n_pools,
+                     seeds=np.arange(1, n_pools + 1, dtype=np.uint64))
+    ws, wh = b.consume(count)
+    assert np.array_equal(np.array(h0, dtype=np.uint64), wh)
+    np.testing.assert_allclose(np.array(s0), ws, rtol=1e-12, atol=1e-9)

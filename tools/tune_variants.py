@@ -19,7 +19,7 @@ for lib in libs:
     ok = smoke.returncode == 0
     for c in configs:
         r = subprocess.run([sys.executable, "bench.py", "--config", str(c), "--steps", "20",
-                            "--no-e2e", "--no-cpu"], cwd=ROOT, env=env, capture_output=True, text=True)
+                            "--no-e2e", "--no-cpu", "--no-configs", "--no-sustained"], cwd=ROOT, env=env, capture_output=True, text=True)
         try:
             d = json.loads(r.stdout.strip().splitlines()[-1])
             frac = (d.get("roofline") or {}).get("frac")
