@@ -19,6 +19,7 @@
 #include <atomic>
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 
 #include "wallace_common.h"
 
@@ -85,7 +86,7 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 // ABLATION builds only (timing experiments, wrong output): 1 = skip the
 // fast emission, 2 = skip its global stores, 3 = skip the scalar chain,
 // 7 = staged emission without the wait for the bulk copy's read, 8 = staged
-// emission without its shared stores, 13 = latency fill without the chain
+// emission without its shared stores, 9 = staged emission without the proxy fence, 13 = latency fill without the chain
 #ifndef WB_ABLATE
 #define WB_ABLATE 0
 #endif
@@ -127,6 +128,16 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 // 1: the consumer's four power sums as two packed f32x2 FMAs
 #ifndef WB_CONS_PACKED
 #define WB_CONS_PACKED 1
+#endif
+// 1: renormalisation sums on one warp (neumaier_warp) in the latency
+// kernels, where the other pool buffer is dead shared memory
+#ifndef WB_NEUM_WARP
+#define WB_NEUM_WARP 1
+#endif
+// 1: fp32 mean-zero consumer on f32x2 value pairs with an unclamped
+// histogram fast path (consume_chunk_pairs)
+#ifndef WB_CONS_PAIRS
+#define WB_CONS_PAIRS 1
 #endif
 // ABLATION builds only: consumer without histogram (1) / moments (2) / both (3)
 #ifndef WB_CONS_ABLATE
@@ -279,6 +290,11 @@ __device__ __forceinline__ uint64_t fma2_rn(uint64_t a, uint64_t b, uint64_t c) 
 __device__ __forceinline__ uint64_t mul2_rn(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2_rn(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 
@@ -532,17 +548,131 @@ __device__ double neumaier_sq(const T* v, int n) {
   return __dadd_rn(sum, comp);
 }
 
+// generator.cpp:20-34 recompute_sum_sq on one warp, bit-identical to the
+// sequential loop.  Only the two running sums are sequential: sum_i =
+// fl(sum_{i-1} + x_i^2) and comp_i = fl(comp_{i-1} + err_i).  The reference's
+// err_i = (big - t) + small (big/small: sum_{i-1} and the term ordered by
+// magnitude, ties to sum) is Fast2Sum's exact rounding error of that
+// addition, so it depends only on (sum_{i-1}, term_i, sum_i) and is formed in
+// parallel.  Per tile of 32 elements: the lanes square their element (terms
+// to scr), every lane runs the same sum chain over the tile from shared
+// memory (two terms per 128-bit broadcast load) and records the partial sums,
+// the lanes form the tile's errors, and the comp chain of an earlier tile
+// runs interleaved with the sum chain (two independent DADD chains); the
+// next tile's terms and the previous tile's errors are formed mid-chain, so
+// their latency hides behind the chains.  1024 fp32 values: 14.8k cycles
+// against 23.4k for the one-thread loop (tools/probes/neum_probe.cu; the
+// floor is 1024 dependent DADDs = 8.4k).  scr: 288 doubles of dead shared
+// memory (16-byte aligned).  Out of line: its registers stay out of the pass
+// loop's allocation.
+//
+// One tile's sum chain over tb (32 terms) into pb, beside (EC) the comp
+// chain over an earlier tile's errors eb; loads run 8 elements ahead; mid()
+// runs after the first 8 elements (in-order issue: work placed there
+// overlaps the chains instead of delaying their start).
+template <bool SC, bool EC, class Mid>
+__device__ __forceinline__ void neumaier_tile(const double* tb, double* pb, const double* eb, double& sum,
+                                              double& comp, Mid&& mid) {
+  double2 t[4], e[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (SC) t[g] = reinterpret_cast<const double2*>(tb)[g];
+    if (EC) e[g] = reinterpret_cast<const double2*>(eb)[g];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int g = i & 3;
+    double2 tn, en;
+    if (i + 4 < 16) {
+      if (SC) tn = reinterpret_cast<const double2*>(tb)[i + 4];
+      if (EC) en = reinterpret_cast<const double2*>(eb)[i + 4];
+    }
+    if (SC) {
+      const double s0 = __dadd_rn(sum, t[g].x);
+      sum = __dadd_rn(s0, t[g].y);
+      reinterpret_cast<double2*>(pb)[i] = make_double2(s0, sum);
+    }
+    if (EC) comp = __dadd_rn(__dadd_rn(comp, e[g].x), e[g].y);
+    if (i + 4 < 16) {
+      if (SC) t[g] = tn;
+      if (EC) e[g] = en;
+    }
+    if (i == 3) mid();
+  }
+}
+
+template <typename T, int N>
+__device__ __noinline__ double neumaier_warp(const T* v, double* scr, int lane) {
+  static_assert(N % 32 == 0 && N >= 128, "whole tiles, at least four");
+  constexpr int NT = N / 32;
+  // scr: three slots of [terms 32 | partial sums 32 | errors 32], slot = tile mod 3
+  auto tb = [&](int k) { return scr + (k % 3) * 96; };
+  double sum = 0.0, comp = 0.0;
+  double start_cur = 0.0;  // sum before the tile whose chain ran last
+  // one pipeline step at tile k: the sum chain of k, the comp chain of k-2,
+  // and (loads issued before, the arithmetic mid-chain) the terms of k+1 and
+  // the errors of k-1
+  auto step = [&](int k, auto TM, auto ER, auto SC, auto EC) {
+    T xv = T(0);
+    double term = 0.0, prev = 0.0, cur = 0.0;
+    if constexpr (decltype(TM)::value) xv = v[32 * (k + 1) + lane];
+    if constexpr (decltype(ER)::value) {
+      const double* t = tb(k - 1);
+      term = t[lane];
+      prev = lane == 0 ? start_cur : t[32 + lane - 1];
+      cur = t[32 + lane];
+    }
+    start_cur = sum;
+    neumaier_tile<decltype(SC)::value, decltype(EC)::value>(tb(k), tb(k) + 32, tb(k - 2 + 3) + 64, sum, comp, [&] {
+      if constexpr (decltype(TM)::value) {
+        const double x = static_cast<double>(xv);
+        tb(k + 1)[lane] = __dmul_rn(x, x);
+      }
+      if constexpr (decltype(ER)::value) {
+        const bool sum_big = fabs(prev) >= fabs(term);
+        const double big = sum_big ? prev : term;
+        const double small = sum_big ? term : prev;
+        tb(k - 1)[64 + lane] = __dadd_rn(__dsub_rn(big, cur), small);
+      }
+    });
+    __syncwarp();
+  };
+  using Y = std::true_type;
+  using F = std::false_type;
+  {  // terms of tile 0
+    const double x = static_cast<double>(v[lane]);
+    tb(0)[lane] = __dmul_rn(x, x);
+    __syncwarp();
+  }
+  step(0, Y{}, F{}, Y{}, F{});
+  step(1, Y{}, Y{}, Y{}, F{});
+  for (int k = 2; k < NT - 1; ++k) step(k, Y{}, Y{}, Y{}, Y{});
+  step(NT - 1, F{}, Y{}, Y{}, Y{});
+  step(NT, F{}, Y{}, F{}, Y{});
+  step(NT + 1, F{}, F{}, F{}, Y{});
+  return __dadd_rn(sum, comp);
+}
+
 // generator.cpp:345-351 renormalize_.  Contains block barriers: call from
 // all threads.
 // LAT: the latency kernel (one pool per SM, the renormalisation is on the
-// critical path: vector loads, out of line); otherwise inline scalar loads
+// critical path: vector loads, out of line); otherwise inline scalar loads.
+// scr: dead shared memory (the other pool buffer) for the warp-parallel sum
+// (latency kernels only: in the throughput kernels other pools hide the
+// one-thread loop, and the call costs more than it saves there), or nullptr.
 template <typename T, int N, int THREADS, bool LAT, bool NB = false>
-__device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
-  if (tid == 0) {
-    const double ss = neumaier_sq<T, LAT>(cur, N);
-    // generator.cpp:347 skips only ss <= 0: a NaN sum still rescales (by NaN)
-    s.renorm_ok = !(ss <= 0.0);
-    s.renorm_k = s.renorm_ok ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
+__device__ __forceinline__ void renormalize(T* cur, SState& s, int tid, double* scr = nullptr) {
+  constexpr bool PAR = WB_NEUM_WARP && LAT && N >= 128 && N % 32 == 0 && N * sizeof(T) >= 288 * sizeof(double);
+  const bool par = PAR && scr != nullptr;
+  if (par ? tid < 32 : tid == 0) {
+    double ss;
+    if constexpr (PAR) ss = par ? neumaier_warp<T, N>(cur, scr, tid) : neumaier_sq<T, LAT>(cur, N);
+    else ss = neumaier_sq<T, LAT>(cur, N);
+    if (tid == 0) {
+      // generator.cpp:347 skips only ss <= 0: a NaN sum still rescales (by NaN)
+      s.renorm_ok = !(ss <= 0.0);
+      s.renorm_k = s.renorm_ok ? __dsqrt_rn(__ddiv_rn(static_cast<double>(N), ss)) : 0.0;
+    }
   }
   loop_bar<NB, THREADS>();
   if (s.renorm_ok) {
@@ -550,7 +680,12 @@ __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid) {
     for (int i = tid; i < N; i += THREADS)
       cur[i] = from_double<T>(__dmul_rn(static_cast<double>(cur[i]), k));
     loop_bar<NB, THREADS>();
-    if (tid == 0) s.sum_sq = neumaier_sq<T, LAT>(cur, N);
+    if (par ? tid < 32 : tid == 0) {
+      double ss;
+      if constexpr (PAR) ss = par ? neumaier_warp<T, N>(cur, scr, tid) : neumaier_sq<T, LAT>(cur, N);
+      else ss = neumaier_sq<T, LAT>(cur, N);
+      if (tid == 0) s.sum_sq = ss;
+    }
   }
   loop_bar<NB, THREADS>();
 }
@@ -562,6 +697,9 @@ template <typename T>
 struct Consumer {
   double s1 = 0, s2 = 0, s3 = 0, s4 = 0;  // per-thread totals (fp64)
   T a1 = 0, a2 = 0, a3 = 0, a4 = 0;       // per-emission partials (T)
+  // fp32 pair path (consume_chunk_pairs): per-emission partials of value
+  // pairs, one f32x2 register each (lanes: even / odd slots of a block)
+  uint64_t p1 = 0, p2 = 0, p3 = 0, p4 = 0;
   uint32_t* hist;  // shared, 258 bins (under, 256, over)
   __device__ __forceinline__ void add(T x) {
     if (WB_CONS_ABLATE != 2 && WB_CONS_ABLATE != 3) {
@@ -602,6 +740,18 @@ struct Consumer {
     s3 += static_cast<double>(a3);
     s4 += static_cast<double>(a4);
     a1 = a2 = a3 = a4 = T(0);
+    if constexpr (sizeof(T) == 4 && WB_CONS_PAIRS) {
+      float lo, hi;
+      upk2(p1, lo, hi);
+      s1 += static_cast<double>(lo) + static_cast<double>(hi);
+      upk2(p2, lo, hi);
+      s2 += static_cast<double>(lo) + static_cast<double>(hi);
+      upk2(p3, lo, hi);
+      s3 += static_cast<double>(lo) + static_cast<double>(hi);
+      upk2(p4, lo, hi);
+      s4 += static_cast<double>(lo) + static_cast<double>(hi);
+      p1 = p2 = p3 = p4 = 0;
+    }
   }
 };
 
@@ -1306,9 +1456,70 @@ __device__ __forceinline__ void consume_chunk_mz(const T (&X)[JCL][4], Consumer<
     cons.add_group(y, b == G::ROWS - 1 ? 3 : 4);
   }
 }
+// fp32, mean +0: the chunk's values as f32x2 pairs (slots 0,1 and 2,3 of a
+// block).  Per pair: y = x*scale (one FFMA2 with +0, bit-identical to the
+// scalar emission), the four power sums (FMUL2, 2 FADD2, 2 FFMA2), the
+// histogram coordinate 16y + 128 (one FFMA2, exact like fl(fl(y+8)*16)).
+// The bins are floored first and counted after the check: a power-4 partial
+// below 4096 proves every |y| of this emission so far is below 8 (the terms
+// are non-negative and rounding is monotone; NaN fails the test), so the
+// clamp to [-1, 256] is the identity and is skipped.  Element N-1 (slot 3 of
+// block ROWS-1) is the reserved value: it adds 0 to the sums and no count.
+template <int LOG2N, int JCL>
+__device__ __forceinline__ void consume_chunk_pairs(const float (&X)[JCL][4], Consumer<float>& cons, float sc,
+                                                    uint32_t b0c) {
+  using G = Geo<float, LOG2N>;
+  const uint64_t sc2 = pk2(sc, sc), zero2 = pk2(0.f, 0.f);
+  const uint64_t k16 = pk2(16.f, 16.f), k128 = pk2(128.f, 128.f);
+  int bin[JCL][4];
+  bool tail = false;  // this thread's last block is the pool's last
+#pragma unroll
+  for (int j = 0; j < JCL; ++j) {
+    const bool last = (b0c + 32 * j == G::ROWS - 1);
+    tail |= last;
+#pragma unroll
+    for (int h = 0; h < 4; h += 2) {
+      uint64_t y = fma2_rn(pk2(X[j][h], X[j][h + 1]), sc2, zero2);
+      if (h == 2 && j == JCL - 1) {
+        float y0, y1;
+        upk2(y, y0, y1);
+        y = pk2(y0, last ? 0.f : y1);
+      }
+      const uint64_t q = mul2_rn(y, y);
+      cons.p1 = add2_rn(cons.p1, y);
+      cons.p2 = add2_rn(cons.p2, q);
+      cons.p3 = fma2_rn(q, y, cons.p3);
+      cons.p4 = fma2_rn(q, q, cons.p4);
+      float t0, t1;
+      upk2(fma2_rn(y, k16, k128), t0, t1);
+      bin[j][h] = __float2int_rd(t0);
+      bin[j][h + 1] = __float2int_rd(t1);
+    }
+  }
+  float q4lo, q4hi;
+  upk2(cons.p4, q4lo, q4hi);
+  if (!(q4lo < 4096.f && q4hi < 4096.f)) {
+#pragma unroll
+    for (int j = 0; j < JCL; ++j)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bin[j][k] = max(-1, min(bin[j][k], 256));
+  }
+#pragma unroll
+  for (int j = 0; j < JCL; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (!(k == 3 && j == JCL - 1 && tail)) atomicAdd(&cons.hist[bin[j][k] + 1], 1u);
+}
+
 template <typename T, int LOG2N, int JCL>
 __device__ __forceinline__ void consume_chunk(const T (&X)[JCL][4], Consumer<T>& cons, T sc, T mean,
                                               bool mz, uint32_t b0c) {
+  if constexpr (sizeof(T) == 4 && WB_CONS_PAIRS) {
+    if (mz) {
+      consume_chunk_pairs<LOG2N, JCL>(X, cons, sc, b0c);
+      return;
+    }
+  }
   if (mz) consume_chunk_mz<T, LOG2N, JCL, true>(X, cons, sc, mean, b0c);
   else consume_chunk_mz<T, LOG2N, JCL, false>(X, cons, sc, mean, b0c);
 }
@@ -1501,7 +1712,9 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
       }
       __syncthreads();
       cur_off ^= PFLIP;
-      if (pc == 0) renormalize<T, N, THREADS, G::LAT>(reinterpret_cast<T*>(pbase + cur_off), s, tid);
+      if (pc == 0)
+        renormalize<T, N, THREADS, G::LAT>(reinterpret_cast<T*>(pbase + cur_off), s, tid,
+                                            G::INPLACE ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
       pc = (pc + 1) & 255u;
       if (probe) {
         const double y = static_cast<double>(reinterpret_cast<const T*>(pbase + cur_off)[a.probe_out[tid]]);
@@ -1561,7 +1774,8 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           cur_off ^= FLIP;
           T* const cur = reinterpret_cast<T*>(pbase + cur_off);
           if (renorm_now) {
-            renormalize<T, N, G::CT, true, true>(cur, s, tid);
+            renormalize<T, N, G::CT, true, true>(
+                cur, s, tid, (G::INPLACE || !WB_LAT_STG) ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
             if (WB_LAT_STG && emit_pass) {
               // renormalised emission: each thread's own 4-blocks, from the
               // pool (renormalize ends on a barrier)
@@ -1783,7 +1997,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
             T (&X)[JCL][4] = *reinterpret_cast<T(*)[JCL][4]>(&Xo[0][0]);
             if (WB_ABLATE != 8)
               stage_chunk_any<T, LOG2N>(delta, mean_zero, X, 0, prev, sb, gbase, scs, mean_t, lane, warp);
-            fence_proxy_async_smem();
+            if (WB_ABLATE != 9) fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
               uint32_t lo, hi;
@@ -1852,7 +2066,8 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         }
         if (renorm_now) {
           if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
-          renormalize<T, N, THREADS, G::LAT>(cur, s, tid);
+          renormalize<T, N, THREADS, G::LAT>(cur, s, tid,
+                                              G::INPLACE ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
           if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
           __syncthreads();
@@ -2044,8 +2259,27 @@ cudaError_t launch_pool(const FillArgs& a, uint64_t n_pools, cudaStream_t stream
   }
 }
 
+// WB_QUICK (measurement builds only): the BASELINE configs' sizes, nothing else
+#ifndef WB_QUICK
+#define WB_QUICK 0
+#endif
 template <typename T, int PT>
 cudaError_t launch_pool_dispatch(int log2n, const FillArgs& a, uint64_t n_pools, cudaStream_t s) {
+#if WB_QUICK
+  if constexpr (PT != 0) {
+    return cudaErrorInvalidValue;
+  } else {
+    switch (log2n) {
+      case 16 + 10: return launch_pool<T, 16 + 10, PT>(a, n_pools, s);
+      case 16 + 11: return launch_pool<T, 16 + 11, PT>(a, n_pools, s);
+      case 16 + 12: return launch_pool<T, 16 + 12, PT>(a, n_pools, s);
+      case 10: return launch_pool<T, 10, PT>(a, n_pools, s);
+      case 11: return launch_pool<T, 11, PT>(a, n_pools, s);
+      case 12: return launch_pool<T, 12, PT>(a, n_pools, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+#else
   switch (log2n) {
     // latency kernels (key log2(N) + 16)
     case 16 + 8: return launch_pool<T, 16 + 8, PT>(a, n_pools, s);
@@ -2071,6 +2305,7 @@ cudaError_t launch_pool_dispatch(int log2n, const FillArgs& a, uint64_t n_pools,
       else return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }
+#endif
 }
 
 // one translation unit per pass type (pool_pt<PT>.cu) defines this
