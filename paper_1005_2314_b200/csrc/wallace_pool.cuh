@@ -86,7 +86,8 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 // ABLATION builds only (timing experiments, wrong output): 1 = skip the
 // fast emission, 2 = skip its global stores, 3 = skip the scalar chain,
 // 7 = staged emission without the wait for the bulk copy's read, 8 = staged
-// emission without its shared stores, 9 = staged emission without the proxy fence, 13 = latency fill without the chain
+// emission without its shared stores, 9 = staged emission without the proxy fence, 13 = latency fill without the chain,
+// 14 = latency fill without the row stores, 16 = latency fill without renormalisation
 #ifndef WB_ABLATE
 #define WB_ABLATE 0
 #endif
@@ -128,6 +129,14 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 // 1: the consumer's four power sums as two packed f32x2 FMAs
 #ifndef WB_CONS_PACKED
 #define WB_CONS_PACKED 1
+#endif
+// latency fills: emissions per release of the chain warp's ring, and the
+// chain warp's sleep between polls (ns)
+#ifndef WB_LAT_BATCH
+#define WB_LAT_BATCH 1
+#endif
+#ifndef WB_LAT_POLL_NS
+#define WB_LAT_POLL_NS 20
 #endif
 // 1: renormalisation sums on one warp (neumaier_warp) in the latency
 // kernels, where the other pool buffer is dead shared memory
@@ -180,9 +189,12 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_LAT_STG
 #define WB_LAT_STG 1
 #endif
-// at least this many 4-blocks per thread in the latency kernels
+// at least this many 4-blocks per thread in the latency kernels (2: four
+// compute warps for N = 1024, so the chain warp shares its SM sub-partition
+// with one compute warp instead of two -- cfg1 0.752 -> 0.727 ms per
+// 2048-pass launch; 1: 0.752, 4: 0.763)
 #ifndef WB_LAT_J
-#define WB_LAT_J 1
+#define WB_LAT_J 2
 #endif
 #ifndef WB_HS_LUT
 #define WB_HS_LUT 1
@@ -190,8 +202,8 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 
 // Kernel geometry.  The template key is log2(N) for the throughput kernel
 // (many pools: few warps per pool, 8 4-blocks per thread) and log2(N) + 16
-// for the latency kernel (few pools: one 4-block per thread, up to 1024
-// threads per pool, so one pass is a short critical path).
+// for the latency kernel (few pools: WB_LAT_J 4-blocks per thread, up to
+// 1024 threads per pool, so one pass is a short critical path).
 template <typename T, int LOG2N>
 struct Geo {
   static constexpr bool LAT = LOG2N >= 16;
@@ -662,7 +674,7 @@ __device__ __noinline__ double neumaier_warp(const T* v, double* scr, int lane) 
 // one-thread loop, and the call costs more than it saves there), or nullptr.
 template <typename T, int N, int THREADS, bool LAT, bool NB = false>
 __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid, double* scr = nullptr) {
-  constexpr bool PAR = WB_NEUM_WARP && LAT && N >= 128 && N % 32 == 0 && N * sizeof(T) >= 288 * sizeof(double);
+  constexpr bool PAR = WB_NEUM_WARP && (LAT || WB_NEUM_WARP == 2) && N >= 128 && N % 32 == 0 && N * sizeof(T) >= 288 * sizeof(double);
   const bool par = PAR && scr != nullptr;
   if (par ? tid < 32 : tid == 0) {
     double ss;
@@ -1744,7 +1756,19 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           T X[G::J][4];
           run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
           T* const row = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows + e) * N;
-          if (WB_LAT_STG && emit_pass && !renorm_now) {
+          // pool element N-1 and the sum of squares of this emission for the
+          // chain warp (generator.cpp:358-364, 373-375 run there), published
+          // before this thread's row stores: the release orders every prior
+          // memory access of the thread, and a pending global store would
+          // hold it (and the pass barrier behind it) for a round trip
+          if (emit_pass && !renorm_now && tid == G::OWNER) {
+            ring[2 * e] = static_cast<double>(X[G::J - 1][3]);
+            ring[2 * e + 1] = s.sum_sq;
+            // released in batches: the release's fence sits on this warp's
+            // path to the pass barrier, and the chain warp polls less often
+            if ((e + 1) % WB_LAT_BATCH == 0 || e + 1 == a.n_emit) st_release_cta(&s.produced, e + 1);
+          }
+          if (WB_LAT_STG && emit_pass && !renorm_now && WB_ABLATE != 14) {
             // the pool this pass wrote is the raw emission: each thread's
             // 4-blocks go to the pitched row straight from registers
 #pragma unroll
@@ -1754,18 +1778,9 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
               if constexpr (sizeof(T) == 8) stg_vec(d + 2, X[j] + 2);
             }
           }
-          if (emit_pass) {
-            // WB_LAT_STG 0: the pool this pass wrote is the raw emission, one
-            // bulk copy after the barrier sends it to its pitched row
-            if (!WB_LAT_STG) fence_proxy_async_smem();
-            // pool element N-1 and the sum of squares of this emission for
-            // the chain warp (generator.cpp:358-364, 373-375 run there)
-            if (!renorm_now && tid == G::OWNER) {
-              ring[2 * e] = static_cast<double>(X[G::J - 1][3]);
-              ring[2 * e + 1] = s.sum_sq;
-              st_release_cta(&s.produced, e + 1);
-            }
-          }
+          // WB_LAT_STG 0: the pool this pass wrote is the raw emission, one
+          // bulk copy after the barrier sends it to its pitched row
+          if (emit_pass && !WB_LAT_STG) fence_proxy_async_smem();
           // the copy issued after the previous pass read the buffer the
           // next pass overwrites
           if (pending && tid == 0) bulk_wait_read();
@@ -1773,7 +1788,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           loop_bar<true, G::CT>();
           cur_off ^= FLIP;
           T* const cur = reinterpret_cast<T*>(pbase + cur_off);
-          if (renorm_now) {
+          if (renorm_now && WB_ABLATE != 16) {
             renormalize<T, N, G::CT, true, true>(
                 cur, s, tid, (G::INPLACE || !WB_LAT_STG) ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
             if (WB_LAT_STG && emit_pass) {
@@ -1820,12 +1835,16 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         for (uint32_t e = 0; e < (WB_ABLATE == 13 ? 0u : a.n_emit); ++e) {
           // S_e depends on the previous emission only: drawn while waiting
           const double S0 = a.chi2.disable ? 0.0 : chi2_draw(reserved, a.chi2, clamp, flags);
-          while (ld_acquire_cta(&s.produced) <= e) __nanosleep(20);
+          while (ld_acquire_cta(&s.produced) <= e) __nanosleep(WB_LAT_POLL_NS);
           const double xl = ring[2 * e], ss = ring[2 * e + 1];
           // disable_chi2: S is the sum of squares refill_ sees (after a
           // renormalisation, the new one: chain_rescale)
           const double S = a.chi2.disable ? ss : S0;
+#if WB_ABLATE == 17
+          const double r = __dmul_rn(S, 9.765625e-4);  // timing only: no division / square root (N = 1024)
+#else
           const double r = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(S, ss)) : 0.0;
+#endif
           const double sc = __dmul_rn(a.sigma, r);
           scl[e] = sc;
           reserved = __dmul_rn(xl, r);
