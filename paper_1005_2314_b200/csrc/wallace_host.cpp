@@ -24,6 +24,7 @@
 #include <string>
 #include <thread>
 #include <utility>
+#include <functional>
 #include <vector>
 
 #include "../../include/wallace_b200.h"
@@ -269,9 +270,16 @@ struct wallace_handle {
     uint64_t pass_count = 0;
     bool has = false;
   } snap[2];
-  // wallace_fill_host_async: device staging of the queued block
+  // wallace_fill_host_async: device staging of the queued block, copied to
+  // the host launch by launch on cp_stream (ev_cp: launch done / copies done)
   void* d_astage = nullptr;
   uint64_t astage_bytes = 0;
+  cudaStream_t cp_stream = nullptr;
+  cudaEvent_t ev_cp = nullptr;
+  // run_emit: at most this many emissions per launch (0: plan_cap / d), and
+  // a callback after each launch's kernels (issue)
+  uint32_t max_emit = 0;
+  std::function<cudaError_t(const wb::FillArgs&)> after_launch;
 
   // consumer scratch
   double* d_part_sums = nullptr;
@@ -515,6 +523,7 @@ wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
       WB_CUDA(wb::launch_rescale(h->dtype, a, static_cast<uint32_t>(h->N), h->n_pools, h->stream));
       ++g_launches;
     }
+    if (h->after_launch) WB_CUDA(h->after_launch(a));
     WB_CUDA(cudaEventRecord(h->ev_pooled[k & 1], h->stream));
   }
   return WALLACE_OK;
@@ -612,6 +621,7 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
       if (d <= h->plan_cap) {
         e = std::min<uint64_t>(e_total, h->plan_cap / d);
         if (a.mode == wb::kModeFillLat) e = std::min<uint64_t>(e, h->lat_rows);
+        if (h->max_emit > 0) e = std::min<uint64_t>(e, h->max_emit);
         passes = e * d;
       } else {
         // an emission longer than one launch: run d-1 passes first, then a
@@ -931,6 +941,8 @@ wallace_status wallace_destroy(wallace_handle* h) {
   cudaFree(h->d_state);
   cudaFree(h->d_plans);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->cp_stream) cudaStreamDestroy(h->cp_stream);
+  if (h->ev_cp) cudaEventDestroy(h->ev_cp);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_planned[i]) cudaEventDestroy(h->ev_planned[i]);
@@ -1293,6 +1305,9 @@ wallace_status wallace_snapshot_ex(wallace_handle* h, int32_t slot) {
 
 wallace_status wallace_snapshot(wallace_handle* h) { return wallace_snapshot_ex(h, 0); }
 
+// emissions per launch of wallace_fill_host_async (copy granularity)
+constexpr uint32_t kPipeEmit = 256;
+
 wallace_status wallace_fill_host_async(wallace_handle* h, void* host_out, uint64_t count) {
   if (!h) return fail(WALLACE_ERR_INVALID_PARAM, "handle must not be NULL");
   if (count < 1) return fail(WALLACE_ERR_INVALID_PARAM, "fill: count must be >= 1");
@@ -1309,9 +1324,34 @@ wallace_status wallace_fill_host_async(wallace_handle* h, void* host_out, uint64
     WB_CUDA(cudaMalloc(&h->d_astage, bytes));
     h->astage_bytes = bytes;
   }
+  // launches of at most kPipeEmit emissions, each one's values copied to the
+  // host on cp_stream while the next launch runs (the look-ahead of the C++
+  // drop-in is one such call per block: generation and PCIe overlap)
+  if (!h->cp_stream) {
+    WB_CUDA(cudaStreamCreateWithFlags(&h->cp_stream, cudaStreamNonBlocking));
+    WB_CUDA(cudaEventCreateWithFlags(&h->ev_cp, cudaEventDisableTiming));
+  }
+  const uint64_t n1 = h->N - 1, esz = h->esize;
+  char* const hb = static_cast<char*>(host_out);
+  char* const db = static_cast<char*>(h->d_astage);
+  h->max_emit = kPipeEmit;
+  h->after_launch = [&](const wb::FillArgs& a) -> cudaError_t {
+    const uint64_t vals = a.lead + (a.n_emit > 0 ? (a.n_emit - 1) * n1 + a.last_limit : 0);
+    if (vals == 0) return cudaSuccess;
+    cudaError_t e = cudaEventRecord(h->ev_cp, h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->cp_stream, h->ev_cp, 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(hb + a.out_offset * esz, count * esz, db + a.out_offset * esz, count * esz, vals * esz,
+                            h->n_pools, cudaMemcpyDeviceToHost, h->cp_stream);
+    return e;
+  };
   st = run_emit(h, h->d_astage, count, wb::kModeFill, h->d_state, h->d_pools);
+  h->after_launch = nullptr;
+  h->max_emit = 0;
   if (st) return st;
-  WB_CUDA(cudaMemcpyAsync(host_out, h->d_astage, bytes, cudaMemcpyDeviceToHost, h->stream));
+  // the handle's stream (what synchronising calls wait on) covers the copies
+  WB_CUDA(cudaEventRecord(h->ev_cp, h->cp_stream));
+  WB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_cp, 0));
   return WALLACE_OK;
 }
 

@@ -14,6 +14,18 @@ namespace wb {
 // are written with coalesced 128-byte stores.
 // ---------------------------------------------------------------------------
 
+// w mod 384 (decode_pass_plan's variant, generator.cpp:249) in 32-bit
+// arithmetic: 2^32 = 256 (mod 384), so w = hi*2^32 + lo = (hi mod 384)*256 +
+// lo (mod 384) -- three constant 32-bit remainders instead of a 64-bit one
+__device__ __forceinline__ uint32_t mod384(uint64_t w) {
+  const uint32_t hi = static_cast<uint32_t>(w >> 32), lo = static_cast<uint32_t>(w);
+  return ((hi % 384u) * 256u + lo % 384u) % 384u;
+}
+
+// LARGE / ROT are compile-time (a.large / a.rotation): a single pool's
+// walk is one thread's dependent chain, exposed once per latency fill, so its
+// loop carries no branches or parameter reloads.
+template <bool LARGE, bool ROT>
 __global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
   __shared__ uint32_t tile[4][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -31,54 +43,61 @@ __global__ void __launch_bounds__(128) plan_kernel(const PlanArgs a) {
   // plan words of this launch: one per pass (wallace4: offset | variant << 16)
   // or two (rotation: per sweep offset | t_index << 16 | negate << 20;
   // decode_pass_plan, generator.cpp:238-257)
-  const uint32_t pw = a.large ? (a.rotation ? 3u : 2u) : (a.rotation ? 2u : 1u);
+  constexpr uint32_t pw = LARGE ? (ROT ? 3u : 2u) : (ROT ? 2u : 1u);
+  const uint32_t off_mask = a.off_mask;
+  const bool fixed = a.fixed_transform != 0;
   const uint32_t n_words = a.n_passes * pw;
-  const uint32_t step = 32u - 32u % pw;  // whole passes per staged tile
+  constexpr uint32_t step = 32u - 32u % pw;  // whole passes per staged tile
+  // one pass's plan words into the tile at word index i
+  auto one_pass = [&](uint32_t i) {
+    uint64_t w2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // baselines.cpp:33-45
+      w2[q] = rotl64(s1 * 5, 7) * 9;
+      const uint64_t t = s1 << 17;
+      s2 ^= s0;
+      s3 ^= s1;
+      s1 ^= s2;
+      s0 ^= s3;
+      s2 ^= t;
+      s3 = rotl64(s3, 45);
+    }
+    if constexpr (LARGE) {
+      // wallace_large.cu plan words: offsets need up to 31 bits
+      uint32_t o0 = static_cast<uint32_t>(w2[1]) & off_mask;
+      uint32_t o1 = static_cast<uint32_t>(w2[1] >> 32) & off_mask;
+      uint32_t x = ROT ? static_cast<uint32_t>((w2[0] & 15u) | ((w2[0] >> 4) & 1u) << 4 |
+                                               ((w2[0] >> 5) & 15u) << 8 | ((w2[0] >> 9) & 1u) << 12)
+                       : mod384(w2[0]);
+      if (fixed) o0 = o1 = x = 0;
+      tile[w][lane][i] = o0;
+      if constexpr (ROT) {
+        tile[w][lane][i + 1] = o1;
+        tile[w][lane][i + 2] = x;
+      } else {
+        tile[w][lane][i + 1] = x;
+      }
+    } else if constexpr (!ROT) {
+      const uint32_t word = (static_cast<uint32_t>(w2[1]) & off_mask) | (mod384(w2[0]) << 16);
+      tile[w][lane][i] = fixed ? 0u : word;  // PassPlan{} (generator.cpp:336-338)
+    } else {
+      uint32_t x0 = (static_cast<uint32_t>(w2[1]) & off_mask) |
+                    static_cast<uint32_t>(w2[0] & 15u) << 16 | static_cast<uint32_t>((w2[0] >> 4) & 1u) << 20;
+      uint32_t x1 = (static_cast<uint32_t>(w2[1] >> 32) & off_mask) |
+                    static_cast<uint32_t>((w2[0] >> 5) & 15u) << 16 |
+                    static_cast<uint32_t>((w2[0] >> 9) & 1u) << 20;
+      if (fixed) x0 = x1 = 0;
+      tile[w][lane][i] = x0;
+      tile[w][lane][i + 1] = x1;
+    }
+  };
   for (uint32_t base = 0; base < n_words; base += step) {
     const uint32_t cnt = min(step, n_words - base);
-    for (uint32_t i = 0; i < cnt; i += pw) {
-      uint64_t w2[2];
+    if (cnt == step) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {  // baselines.cpp:33-45
-        w2[q] = rotl64(s1 * 5, 7) * 9;
-        const uint64_t t = s1 << 17;
-        s2 ^= s0;
-        s3 ^= s1;
-        s1 ^= s2;
-        s0 ^= s3;
-        s2 ^= t;
-        s3 = rotl64(s3, 45);
-      }
-      if (a.large) {
-        // wallace_large.cu plan words: offsets need up to 31 bits
-        uint32_t o0 = static_cast<uint32_t>(w2[1]) & a.off_mask;
-        uint32_t o1 = static_cast<uint32_t>(w2[1] >> 32) & a.off_mask;
-        uint32_t x = a.rotation ? static_cast<uint32_t>((w2[0] & 15u) | ((w2[0] >> 4) & 1u) << 4 |
-                                                        ((w2[0] >> 5) & 15u) << 8 | ((w2[0] >> 9) & 1u) << 12)
-                                : static_cast<uint32_t>(w2[0] % 384u);
-        if (a.fixed_transform) o0 = o1 = x = 0;
-        tile[w][lane][i] = o0;
-        if (a.rotation) {
-          tile[w][lane][i + 1] = o1;
-          tile[w][lane][i + 2] = x;
-        } else {
-          tile[w][lane][i + 1] = x;
-        }
-      } else if (!a.rotation) {
-        uint32_t variant = static_cast<uint32_t>(w2[0] % 384u);
-        uint32_t off = static_cast<uint32_t>(w2[1]) & a.off_mask;
-        if (a.fixed_transform) variant = off = 0;  // PassPlan{} (generator.cpp:336-338)
-        tile[w][lane][i] = off | (variant << 16);
-      } else {
-        uint32_t x0 = (static_cast<uint32_t>(w2[1]) & a.off_mask) |
-                      static_cast<uint32_t>(w2[0] & 15u) << 16 | static_cast<uint32_t>((w2[0] >> 4) & 1u) << 20;
-        uint32_t x1 = (static_cast<uint32_t>(w2[1] >> 32) & a.off_mask) |
-                      static_cast<uint32_t>((w2[0] >> 5) & 15u) << 16 |
-                      static_cast<uint32_t>((w2[0] >> 9) & 1u) << 20;
-        if (a.fixed_transform) x0 = x1 = 0;
-        tile[w][lane][i] = x0;
-        tile[w][lane][i + 1] = x1;
-      }
+      for (uint32_t i = 0; i < step; i += pw) one_pass(i);
+    } else {
+      for (uint32_t i = 0; i < cnt; i += pw) one_pass(i);
     }
     __syncwarp();
     for (int q = 0; q < 32; ++q) {
@@ -317,7 +336,13 @@ int pool_kernel_threads(int dtype, int log2n) {
 
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s) {
   const unsigned blocks = unsigned((a.n_pools + 127) / 128);
-  plan_kernel<<<blocks, 128, 0, s>>>(a);
+  if (a.large) {
+    if (a.rotation) plan_kernel<true, true><<<blocks, 128, 0, s>>>(a);
+    else plan_kernel<true, false><<<blocks, 128, 0, s>>>(a);
+  } else {
+    if (a.rotation) plan_kernel<false, true><<<blocks, 128, 0, s>>>(a);
+    else plan_kernel<false, false><<<blocks, 128, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

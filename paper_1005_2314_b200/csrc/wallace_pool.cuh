@@ -15,7 +15,11 @@
 // reference pins -ffp-contract=off for the same reason
 // (/root/reference/proj/CMakeLists.txt:10-14).
 #include <cuda_runtime.h>
+#ifdef WB_DEBUG_TIMING
+#include <cstdio>
+#endif
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <type_traits>
@@ -129,6 +133,20 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 // 1: the consumer's four power sums as two packed f32x2 FMAs
 #ifndef WB_CONS_PACKED
 #define WB_CONS_PACKED 1
+#endif
+// latency fills: 1 = the per-emission chain runs in a second CTA of a 2-CTA
+// cluster (its own SM), reading the ring over distributed shared memory
+#ifndef WB_LAT_CLUSTER
+#define WB_LAT_CLUSTER 1
+#endif
+// latency fills: 1 = the owner publishes each emission's ring entry during
+// the next pass, after its gathers
+#ifndef WB_LAT_DEFER_PUB
+#define WB_LAT_DEFER_PUB 1
+#endif
+// ... ring entries per mbarrier (batch) of the chain CTA
+#ifndef WB_LAT_CBATCH
+#define WB_LAT_CBATCH 4
 #endif
 // latency fills: emissions per release of the chain warp's ring, and the
 // chain warp's sleep between polls (ns)
@@ -500,6 +518,78 @@ __device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
                    static_cast<uint32_t>(__cvta_generic_to_shared(p))),
                "r"(v)
                : "memory");
+}
+
+// Thread-block-cluster helpers (the latency fill's chain CTA reads the
+// compute CTA's ring over distributed shared memory).
+__device__ __forceinline__ void st_release_cluster(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cluster.shared::cta.u32 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
+}
+// shared::cluster address of `p` (a shared variable) in cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_acquire_cluster(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cluster.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ld_dsmem_f64x2(uint32_t addr, double& x, double& y) {
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void st_dsmem_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_dsmem_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Remote 16-byte store into cluster CTA memory that completes `bytes` on
+// the destination CTA's mbarrier (no fence on the producer's path).
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double x, double y, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(x), "d"(y), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(m))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WB_MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WB_MBAR_WAIT_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m))),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_mbarrier_init_cluster() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// every thread of every CTA of the cluster; orders prior shared (and
+// distributed shared) accesses before those after it
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Barrier of the pass loop: the whole CTA, or (NB) named barrier 1 over the
@@ -1160,11 +1250,17 @@ __device__ __forceinline__ void affine_gather4(const char* base, uint32_t buf, u
 // One pass over the pool in shared memory (generator.cpp:64-85); leaves the
 // signed, permuted outputs of this thread's 4-blocks in X and stores them to
 // the next buffer.  sb = b0*STRIDE + off for this thread's first block.
-template <typename T, int LOG2N, int J, int PT = 0>
+// hook(): work issued right after the pass's gathers (in-order issue: it
+// then overlaps their latency instead of lengthening the pass).
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <typename T, int LOG2N, int J, int PT = 0, class Hook = NoHook>
 __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
                                          uint32_t plan, uint32_t b0, T (&X)[J][4],
                                          const float* hs_lut, bool store = true,
-                                         bool wait_stage = false) {
+                                         bool wait_stage = false, Hook hook = Hook{}) {
+  constexpr bool HOOK = !std::is_same<Hook, NoHook>::value;
   static_assert(PT == 0 || PT == 1, "wallace4 pass types");
   using G = Geo<T, LOG2N>;
   constexpr int ROWS = G::ROWS;
@@ -1240,10 +1336,31 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
 
   // gather + butterfly (apply_wallace4 op order, transforms.hpp:89-103)
   T z[J][4];
+  T vg[HOOK ? J : 1][4];  // HOOK: every gather issued before the hook
+  if constexpr (HOOK) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      vg[j][0] = vg[j][1] = vg[j][2] = vg[j][3] = T(0);
+      if ((ROWS >= 32 || b0 + 32 * j < ROWS) && PT == 0) {
+        constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
+        const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) + cur_off));
+        vg[j][0] = row[0];
+        vg[j][1] = row[ROWS];
+        vg[j][2] = row[2 * ROWS];
+        vg[j][3] = row[3 * ROWS];
+      }
+    }
+    hook();
+  }
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     T v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-    if (ROWS >= 32 || b0 + 32 * j < ROWS) {
+    if constexpr (HOOK && PT == 0) {
+      v0 = vg[j][0];
+      v1 = vg[j][1];
+      v2 = vg[j][2];
+      v3 = vg[j][3];
+    } else if (ROWS >= 32 || b0 + 32 * j < ROWS) {
       if constexpr (PT == 0) {
         constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
         const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) + cur_off));
@@ -1627,6 +1744,10 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
   double* const ring = reinterpret_cast<double*>(dsmem + (SM::STATIC ? 0 : SM::TOTAL) +
                                                  ((a.n_passes * 4u * (PT >= 2 ? 2u : 1u) + 15u) & ~15u));
   (void)ring;
+  // WB_LAT_CLUSTER: one mbarrier per batch of WB_LAT_CBATCH ring entries in
+  // the chain CTA, after its ring (each used for exactly one phase)
+  uint64_t* const rmbar = reinterpret_cast<uint64_t*>(ring + 2 * size_t(a.n_emit));
+  (void)rmbar;
   __shared__ SState s;
   __shared__ uint32_t s_hist[MODE == kModeConsume ? 258 : 1];
   // defect suite: per-warp partial sums / marks of the last two emissions
@@ -1637,7 +1758,15 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t b0 = warp * J * 32 + lane;  // first 4-block of this thread
   const bool compute = !(G::CHAINW || DEC) || tid < G::CT;  // owns 4-blocks (else: chain warp)
-  const uint64_t pool = blockIdx.x;
+  // latency fills with a chain CTA (WB_LAT_CLUSTER): clusters of two CTAs
+  // per pool -- rank 0 runs the passes, rank 1 the per-emission chain on
+  // its own SM, reading rank 0's ring over distributed shared memory
+  constexpr bool CLU = DEC && WB_LAT_CLUSTER;
+  const uint32_t crank = CLU ? (blockIdx.x & 1u) : 0u;
+  const uint64_t pool = CLU ? (blockIdx.x >> 1) : blockIdx.x;
+#ifdef WB_DEBUG_TIMING
+  const long long dbg_t0 = clock64();
+#endif
   const bool mean_zero = a.mean_is_zero != 0;
   const T mean_t = from_double<T>(a.mean);
 
@@ -1672,6 +1801,20 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
   const uint64_t pass0 = a.st_in[pool].pass_count;
   const uint32_t cursor0 = a.st_in[pool].cursor;
   __syncthreads();
+  if constexpr (CLU) {
+    // rank 1: every batch's mbarrier expects its ring entries' bytes; the
+    // cluster barrier publishes the initialisation before rank 0's stores
+    if (crank == 1 && tid == 0) {
+      const uint32_t nb = (a.n_emit + WB_LAT_CBATCH - 1) / WB_LAT_CBATCH;
+      for (uint32_t b = 0; b < nb; ++b) {
+        mbar_init(rmbar + b, 1);
+        const uint32_t cnt = min(uint32_t(WB_LAT_CBATCH), a.n_emit - b * WB_LAT_CBATCH);
+        mbar_arrive_expect_tx(rmbar + b, 16u * cnt);
+      }
+      fence_mbarrier_init_cluster();
+    }
+    cluster_sync_all();
+  }
 
   T* const out_pool = static_cast<T*>(a.out) + pool * a.out_stride + a.out_offset;
   Consumer<T> cons;
@@ -1743,10 +1886,33 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
       for (int k = 0; k < 6; ++k) a.probe_acc[(pool * a.n_probes + tid) * 6 + k] = pa[k];
   } else if constexpr (DEC) {
     // ---- latency fill (kModeFillLat): a lean pass loop for the compute
-    // warps, the chi2/scale chain in the last warp ----------------------------
-    if (compute) {
+    // warps, the chi2/scale chain in the last warp (of the rank-1 CTA with
+    // WB_LAT_CLUSTER) ----------------------------------------------------------
+    if (compute && crank == 0) {
       bool pending = false;  // thread 0's last row copy may still read its buffer
       uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
+      // pool element N-1 and the sum of squares of each emission go to the
+      // chain (generator.cpp:358-364, 373-375 run there).  The owner
+      // publishes emission e during the NEXT pass, right after that pass's
+      // gathers: the release fence then waits on loads the butterfly waits
+      // for anyway, instead of standing between the owner and the pass
+      // barrier (measured: ~115 cycles per pass on the critical path).
+      double ss_reg = s.sum_sq;  // sum_sq changes only at renormalisations
+      bool pub = false;          // the owner holds an unpublished entry
+      double pub_x = 0.0;
+      uint32_t pub_e = 0;
+      auto publish = [&] {
+        if constexpr (CLU) {
+          // into the chain CTA's ring, completing its batch mbarrier
+          if (WB_ABLATE != 18)
+            st_async_f64x2(dsmem_addr(ring + 2 * pub_e, 1), pub_x, ss_reg, dsmem_addr(rmbar + pub_e / WB_LAT_CBATCH, 1));
+        } else {
+          ring[2 * pub_e] = pub_x;
+          ring[2 * pub_e + 1] = ss_reg;
+          if ((pub_e + 1) % WB_LAT_BATCH == 0 || pub_e + 1 == a.n_emit) st_release_cta(&s.produced, pub_e + 1);
+        }
+        pub = false;
+      };
       for (uint32_t e = 0; e < a.n_emit; ++e) {
         for (uint32_t q = 1; q <= a.d; ++q, ++p) {
           const bool emit_pass = q == a.d;
@@ -1754,19 +1920,18 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           const uint32_t plan_p = plan;
           plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
           T X[G::J][4];
-          run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
+          if (WB_LAT_DEFER_PUB)
+            run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs, true, false, [&] {
+              if (pub) publish();
+            });
+          else
+            run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
           T* const row = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows + e) * N;
-          // pool element N-1 and the sum of squares of this emission for the
-          // chain warp (generator.cpp:358-364, 373-375 run there), published
-          // before this thread's row stores: the release orders every prior
-          // memory access of the thread, and a pending global store would
-          // hold it (and the pass barrier behind it) for a round trip
           if (emit_pass && !renorm_now && tid == G::OWNER) {
-            ring[2 * e] = static_cast<double>(X[G::J - 1][3]);
-            ring[2 * e + 1] = s.sum_sq;
-            // released in batches: the release's fence sits on this warp's
-            // path to the pass barrier, and the chain warp polls less often
-            if ((e + 1) % WB_LAT_BATCH == 0 || e + 1 == a.n_emit) st_release_cta(&s.produced, e + 1);
+            pub_x = static_cast<double>(X[G::J - 1][3]);
+            pub_e = e;
+            pub = true;
+            if (!WB_LAT_DEFER_PUB) publish();
           }
           if (WB_LAT_STG && emit_pass && !renorm_now && WB_ABLATE != 14) {
             // the pool this pass wrote is the raw emission: each thread's
@@ -1791,6 +1956,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           if (renorm_now && WB_ABLATE != 16) {
             renormalize<T, N, G::CT, true, true>(
                 cur, s, tid, (G::INPLACE || !WB_LAT_STG) ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
+            ss_reg = s.sum_sq;  // (renormalize ends on a barrier)
             if (WB_LAT_STG && emit_pass) {
               // renormalised emission: each thread's own 4-blocks, from the
               // pool (renormalize ends on a barrier)
@@ -1808,9 +1974,14 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           }
           if (emit_pass && tid == 0 && renorm_now) {
             // refill_ after step_pass renormalised (generator.cpp:342, 363)
-            ring[2 * e] = static_cast<double>(cur[N - 1]);
-            ring[2 * e + 1] = s.sum_sq;
-            st_release_cta(&s.produced, e + 1);
+            if constexpr (CLU) {
+              st_async_f64x2(dsmem_addr(ring + 2 * e, 1), static_cast<double>(cur[N - 1]), s.sum_sq,
+                             dsmem_addr(rmbar + e / WB_LAT_CBATCH, 1));
+            } else {
+              ring[2 * e] = static_cast<double>(cur[N - 1]);
+              ring[2 * e + 1] = s.sum_sq;
+              st_release_cta(&s.produced, e + 1);
+            }
           }
           if (!WB_LAT_STG && emit_pass && tid == 0) {
             bulk_s2g(row, static_cast<uint32_t>(__cvta_generic_to_shared(cur)), N * uint32_t(sizeof(T)));
@@ -1820,23 +1991,43 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           pc = (pc + 1) & 255u;
         }
       }
+      if (pub) publish();  // the owner's last emission
       if (tid == 0) {
         if (!WB_LAT_STG) bulk_wait_all();  // the rows are complete before rescale_kernel reads them
         s.end_off = cur_off;
+#ifdef WB_DEBUG_TIMING
+        printf("compute done at %lld cycles (n_emit %u)\n", clock64() - dbg_t0, a.n_emit);
+#endif
       }
     } else {
       // the chain warp (lane 0): the per-emission recurrence of refill_
       // (generator.cpp:358-364, 373-375; chi2.cpp:27-59), one emission
       // behind the passes at most; its scales go to rescale_kernel
-      if (!compute && lane == 0) {
-        double reserved = s.reserved_prev, lS = s.last_chi2, lr = s.last_r, lsc = s.last_scale;
+      if (!compute && lane == 0 && (!CLU || crank == 1)) {
+        // rank 1 (CLU): the chain state from HBM, rank 0's ring and counter
+        // over distributed shared memory
+        const PoolState& st0 = a.st_in[pool];
+        double reserved = CLU ? st0.reserved_prev : s.reserved_prev;
+        double lS = CLU ? st0.last_chi2 : s.last_chi2;
+        double lr = CLU ? st0.r : s.last_r;
+        double lsc = CLU ? st0.scale : s.last_scale;
+
         uint32_t clamp = 0, flags = 0;
         double* const scl = a.scales + pool * a.scale_stride;
         for (uint32_t e = 0; e < (WB_ABLATE == 13 ? 0u : a.n_emit); ++e) {
           // S_e depends on the previous emission only: drawn while waiting
           const double S0 = a.chi2.disable ? 0.0 : chi2_draw(reserved, a.chi2, clamp, flags);
-          while (ld_acquire_cta(&s.produced) <= e) __nanosleep(WB_LAT_POLL_NS);
-          const double xl = ring[2 * e], ss = ring[2 * e + 1];
+          double xl, ss;
+          if constexpr (CLU) {
+            // this CTA's own ring, filled by rank 0's st.async
+            if (e % WB_LAT_CBATCH == 0 && WB_ABLATE != 18) mbar_wait_parity(rmbar + e / WB_LAT_CBATCH, 0);
+            xl = ring[2 * e];
+            ss = ring[2 * e + 1];
+          } else {
+            while (ld_acquire_cta(&s.produced) <= e) __nanosleep(WB_LAT_POLL_NS);
+            xl = ring[2 * e];
+            ss = ring[2 * e + 1];
+          }
           // disable_chi2: S is the sum of squares refill_ sees (after a
           // renormalisation, the new one: chain_rescale)
           const double S = a.chi2.disable ? ss : S0;
@@ -1852,15 +2043,37 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           lr = r;
           lsc = sc;
         }
-        s.reserved_prev = reserved;
-        s.last_chi2 = lS;
-        s.last_r = lr;
-        s.last_scale = lsc;
-        s.clamp = clamp;
-        s.flags |= flags;
+#ifdef WB_DEBUG_TIMING
+        printf("chain done at %lld cycles (rank %u)\n", clock64() - dbg_t0, crank);
+#endif
+        if constexpr (CLU) {
+          // into rank 0's SState for its epilogue (the cluster barrier below
+          // orders these stores before rank 0 reads them)
+          st_dsmem_f64(dsmem_addr(&s.reserved_prev, 0), reserved);
+          st_dsmem_f64(dsmem_addr(&s.last_chi2, 0), lS);
+          st_dsmem_f64(dsmem_addr(&s.last_r, 0), lr);
+          st_dsmem_f64(dsmem_addr(&s.last_scale, 0), lsc);
+          st_dsmem_u32(dsmem_addr(&s.clamp, 0), clamp);
+          const uint32_t rf = dsmem_addr(&s.flags, 0);
+          st_dsmem_u32(rf, ld_dsmem_u32(rf) | flags);
+        } else {
+          s.reserved_prev = reserved;
+          s.last_chi2 = lS;
+          s.last_r = lr;
+          s.last_scale = lsc;
+          s.clamp = clamp;
+          s.flags |= flags;
+        }
       }
     }
-    __syncthreads();  // the chain's state and the final buffer precede the epilogue
+    if constexpr (CLU) {
+      // the chain CTA's results land in rank 0 before its epilogue, and rank
+      // 0's shared memory (the ring) outlives rank 1's reads
+      cluster_sync_all();
+      if (crank == 1) return;
+    } else {
+      __syncthreads();  // the chain's state and the final buffer precede the epilogue
+    }
     cur_off = s.end_off;
   } else {
     uint32_t plan = a.n_passes > 0 ? s_plans[0] : 0u;
@@ -2228,9 +2441,14 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
   using SM = Smem<T, LOG2N>;
   constexpr size_t PW = PT >= 2 ? 2 : 1;
   const size_t plans = (a.n_passes * 4 * PW + 15) & ~size_t(15);
-  const size_t ring = MODE == kModeFillLat ? 16 * size_t(a.n_emit) : 0;
+  const size_t ring = MODE == kModeFillLat ? 16 * size_t(a.n_emit) + 8 * (size_t(a.n_emit) / WB_LAT_CBATCH + 1) : 0;
   if (MODE == kModeFillLat && a.n_emit > kLatRingMax) return cudaErrorInvalidValue;
-  const size_t smem = (SM::STATIC ? 0 : size_t(SM::TOTAL)) + plans + ring;
+  size_t smem = (SM::STATIC ? 0 : size_t(SM::TOTAL)) + plans + ring;
+  // latency fills with a chain CTA: more than half an SM's shared memory per
+  // CTA, so the two CTAs of a cluster run on different SMs
+  constexpr bool CLU = MODE == kModeFillLat && WB_LAT_CLUSTER;
+  constexpr size_t kCluSmem = 120 * 1024;
+  if (CLU && smem < kCluSmem) smem = kCluSmem;
   auto fn = pool_kernel<T, LOG2N, MODE, PT>;
   // attributes are set once per instantiation and device; concurrent first
   // launches from several host threads set them twice, which is harmless
@@ -2243,13 +2461,30 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
                                          cudaSharedmemCarveoutMaxShared);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int((SM::STATIC ? 16 * 1024 : SM::TOTAL + 16 * 1024) +
-                                   (MODE == kModeFillLat ? 16 * kLatRingMax : 0)));
+                               int(std::max<size_t>(CLU ? kCluSmem : 0,
+                                                    (SM::STATIC ? 16 * 1024 : SM::TOTAL + 16 * 1024) +
+                                                        (MODE == kModeFillLat ? 16 * kLatRingMax : 0))));
     if (e != cudaSuccess) return e;
     configured.fetch_or(dev_bit, std::memory_order_release);
   }
-  fn<<<dim3(unsigned(n_pools)), dim3(kernel_threads<T, LOG2N, MODE>()), smem, stream>>>(a);
-  return cudaGetLastError();
+  if constexpr (CLU) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(unsigned(2 * n_pools));
+    lc.blockDim = dim3(kernel_threads<T, LOG2N, MODE>());
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, fn, a);
+  } else {
+    fn<<<dim3(unsigned(n_pools)), dim3(kernel_threads<T, LOG2N, MODE>()), smem, stream>>>(a);
+    return cudaGetLastError();
+  }
 }
 
 template <typename T, int LOG2N, int PT>

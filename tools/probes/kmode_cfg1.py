@@ -7,10 +7,12 @@ import torch
 import paper_1005_2314_b200 as pb
 
 cfg = pb.GeneratorConfig(pool_size=1024, discard_every=1)
-for mode in ("latency", "throughput", "latency", "throughput"):
-    b = pb.PoolBatch(cfg, n_pools=1, seeds=[1], dtype="f32")
+dt = sys.argv[1] if len(sys.argv) > 1 else "f32"
+modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["latency", "throughput"]
+for mode in modes:
+    b = pb.PoolBatch(cfg, n_pools=1, seeds=[1], dtype=dt)
     b.set_kernel_mode(mode)
-    out = torch.empty((1, 1 << 24), dtype=torch.float32, device="cuda")
+    out = torch.empty((1, 1 << 24), dtype=torch.float32 if dt == "f32" else torch.float64, device="cuda")
     b.snapshot()
     b.fill_from_snapshot_into(out)
     torch.cuda.synchronize()
