@@ -1005,6 +1005,21 @@ wallace_status wallace_profile_end(wallace_handle* h, double* pool_ms, uint64_t*
     if (n) *n = log.size();
     log.clear();
   };
+  // WALLACE_B200_PROFILE_DUMP=1: the launch timeline (ms from the first pool
+  // launch's start) on stderr -- a measurement aid
+  if (const char* d = std::getenv("WALLACE_B200_PROFILE_DUMP"); d && d[0] == '1' && !h->ev_pool.empty()) {
+    const cudaEvent_t t0 = h->ev_pool.front().first;
+    auto dump = [&](const char* what, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& log) {
+      for (auto& [a, b] : log) {
+        float ta = 0.f, tb = 0.f;
+        cudaEventElapsedTime(&ta, t0, a);
+        cudaEventElapsedTime(&tb, t0, b);
+        std::fprintf(stderr, "timeline %s %.4f %.4f\n", what, ta, tb);
+      }
+    };
+    dump("pool", h->ev_pool);
+    dump("plan", h->ev_plan);
+  }
   sum(h->ev_pool, pool_ms, pool_n);
   sum(h->ev_plan, plan_ms, plan_n);
   return WALLACE_OK;

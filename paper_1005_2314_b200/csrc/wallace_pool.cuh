@@ -144,6 +144,12 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_LAT_DEFER_PUB
 #define WB_LAT_DEFER_PUB 1
 #endif
+// ... shared memory (KiB) each CTA of such a cluster requests: more than
+// half an SM, so the two ranks run on different SMs, and enough that no
+// other kernel's block (the concurrent plan kernel) shares their SMs
+#ifndef WB_LAT_CLU_SMEM_KB
+#define WB_LAT_CLU_SMEM_KB 120
+#endif
 // ... ring entries per mbarrier (batch) of the chain CTA
 #ifndef WB_LAT_CBATCH
 #define WB_LAT_CBATCH 4
@@ -2447,7 +2453,7 @@ cudaError_t launch_pool_mode(const FillArgs& a, uint64_t n_pools, cudaStream_t s
   // latency fills with a chain CTA: more than half an SM's shared memory per
   // CTA, so the two CTAs of a cluster run on different SMs
   constexpr bool CLU = MODE == kModeFillLat && WB_LAT_CLUSTER;
-  constexpr size_t kCluSmem = 120 * 1024;
+  constexpr size_t kCluSmem = WB_LAT_CLU_SMEM_KB * 1024;
   if (CLU && smem < kCluSmem) smem = kCluSmem;
   auto fn = pool_kernel<T, LOG2N, MODE, PT>;
   // attributes are set once per instantiation and device; concurrent first
