@@ -139,6 +139,14 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_LAT_CLUSTER
 #define WB_LAT_CLUSTER 1
 #endif
+// fp64 pass stores: 1 = swizzled (conflict-free) 32-byte block stores, for
+// the throughput / the latency kernels
+#ifndef WB_F64_SWZ
+#define WB_F64_SWZ 1
+#endif
+#ifndef WB_LAT_F64_SWZ
+#define WB_LAT_F64_SWZ 0
+#endif
 // latency fills: 1 = the owner publishes each emission's ring entry during
 // the next pass, after its gathers
 #ifndef WB_LAT_DEFER_PUB
@@ -1429,7 +1437,11 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
     // stride would hit each bank twice per 8-lane phase; lanes with bit 2 set
     // store their halves in the opposite order, which makes both stores
     // conflict-free (lanes l and l+4 then cover complementary banks)
-    const bool swz = (b0 >> 2) & 1;
+    // (latency kernels, WB_LAT_F64_SWZ 0: natural order -- there the data
+    // selects and the register moves feeding the stores lengthen the pass
+    // more than the 2-way conflicts do)
+    constexpr bool SWZ = G::LAT ? WB_LAT_F64_SWZ : WB_F64_SWZ;
+    const bool swz = SWZ && ((b0 >> 2) & 1);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t b = b0 + 32 * j;
@@ -1437,8 +1449,13 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
         double2* q = reinterpret_cast<double2*>(nb + 4 * b);
         const double2 lo = make_double2(X[j][0], X[j][1]);
         const double2 hi = make_double2(X[j][2], X[j][3]);
-        q[swz ? 1 : 0] = swz ? hi : lo;
-        q[swz ? 0 : 1] = swz ? lo : hi;
+        if constexpr (SWZ) {
+          q[swz ? 1 : 0] = swz ? hi : lo;
+          q[swz ? 0 : 1] = swz ? lo : hi;
+        } else {
+          q[0] = lo;
+          q[1] = hi;
+        }
       }
     }
   } else {
