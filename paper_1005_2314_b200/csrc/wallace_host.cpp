@@ -1266,31 +1266,52 @@ wallace_status wallace_fill_host(wallace_handle* h, void* host_out, uint64_t cou
   }
   for (uint64_t off = 0; off < count; off += chunk) {
     const uint64_t c = std::min(chunk, count - off);
-    wallace_status st = run_emit(h, h->d_stage, c, wb::kModeFill, h->d_state, h->d_pools);
-    if (st) return st;
     if (c == count) {
-      // one contiguous block: 256 MiB pieces alternating over two streams
-      // (measured 55 GB/s vs 50.5 GB/s for a single 16 GiB copy on this link)
-      const uint64_t total = count * row_bytes;
-      const uint64_t piece = 256ull << 20;
+      // one staged block: each launch's values leave as soon as the launch
+      // is done, in pieces of at most 256 MiB alternating over two copy
+      // streams (two streams: 55 GB/s vs 50.5 GB/s for one 16 GiB copy on
+      // this link), while later launches run
+      const uint64_t piece = 256ull << 20, esz = h->esize;
       if (!h->ws_stream) WB_CUDA(cudaStreamCreateWithFlags(&h->ws_stream, cudaStreamNonBlocking));
+      if (!h->cp_stream) WB_CUDA(cudaStreamCreateWithFlags(&h->cp_stream, cudaStreamNonBlocking));
       if (!h->ws_ef[0]) WB_CUDA(cudaEventCreateWithFlags(&h->ws_ef[0], cudaEventDisableTiming));
       if (!h->ws_ec[0]) WB_CUDA(cudaEventCreateWithFlags(&h->ws_ec[0], cudaEventDisableTiming));
-      WB_CUDA(cudaEventRecord(h->ws_ef[0], h->stream));
-      WB_CUDA(cudaStreamWaitEvent(h->ws_stream, h->ws_ef[0], 0));
+      if (!h->ev_cp) WB_CUDA(cudaEventCreateWithFlags(&h->ev_cp, cudaEventDisableTiming));
+      unsigned char* const hb = static_cast<unsigned char*>(host_out);
+      const unsigned char* const db = static_cast<const unsigned char*>(h->d_stage);
+      const uint64_t n1 = h->N - 1;
       uint64_t k = 0;
-      for (uint64_t o = 0; o < total; o += piece, ++k) {
-        const uint64_t b = std::min(piece, total - o);
-        WB_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(host_out) + o,
-                                static_cast<const unsigned char*>(h->d_stage) + o, b, cudaMemcpyDeviceToHost,
-                                (k & 1) ? h->ws_stream : h->stream));
-      }
+      h->after_launch = [&](const wb::FillArgs& a) -> cudaError_t {
+        const uint64_t vals = a.lead + (a.n_emit > 0 ? (a.n_emit - 1) * n1 + a.last_limit : 0);
+        if (vals == 0) return cudaSuccess;
+        cudaError_t e = cudaEventRecord(h->ws_ef[0], h->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->ws_stream, h->ws_ef[0], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->cp_stream, h->ws_ef[0], 0);
+        if (vals == count) {  // every pool's whole row: one contiguous range
+          const uint64_t total = count * row_bytes;
+          for (uint64_t o = 0; o < total && e == cudaSuccess; o += piece, ++k)
+            e = cudaMemcpyAsync(hb + o, db + o, std::min(piece, total - o), cudaMemcpyDeviceToHost,
+                                (k & 1) ? h->ws_stream : h->cp_stream);
+        } else if (e == cudaSuccess) {
+          e = cudaMemcpy2DAsync(hb + a.out_offset * esz, count * esz, db + a.out_offset * esz, count * esz,
+                                vals * esz, h->n_pools, cudaMemcpyDeviceToHost, (k++ & 1) ? h->ws_stream : h->cp_stream);
+        }
+        return e;
+      };
+      wallace_status st = run_emit(h, h->d_stage, c, wb::kModeFill, h->d_state, h->d_pools);
+      h->after_launch = nullptr;
+      if (st) return st;
       WB_CUDA(cudaEventRecord(h->ws_ec[0], h->ws_stream));
       WB_CUDA(cudaStreamWaitEvent(h->stream, h->ws_ec[0], 0));
-    } else
-      WB_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(host_out) + off * h->esize,
-                                count * h->esize, h->d_stage, c * h->esize, c * h->esize,
-                                h->n_pools, cudaMemcpyDeviceToHost, h->stream));
+      WB_CUDA(cudaEventRecord(h->ev_cp, h->cp_stream));
+      WB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_cp, 0));
+      continue;
+    }
+    wallace_status st = run_emit(h, h->d_stage, c, wb::kModeFill, h->d_state, h->d_pools);
+    if (st) return st;
+    WB_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(host_out) + off * h->esize, count * h->esize,
+                              h->d_stage, c * h->esize, c * h->esize, h->n_pools, cudaMemcpyDeviceToHost,
+                              h->stream));
   }
   WB_CUDA(cudaStreamSynchronize(h->stream));
   return take_err(h, true);
