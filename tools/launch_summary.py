@@ -1,6 +1,6 @@
 """Sum an `ncu --metrics gpu__time_duration.sum --csv --log-file` launch list
-by kernel: count and total us.  Measurement helper:
-python tools/launch_summary.py launches.csv"""
+by kernel: count and total us (or another metric's total).  Measurement
+helper: python tools/launch_summary.py launches.csv [metric]"""
 import collections
 import csv
 import sys
@@ -10,7 +10,10 @@ start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[start]
 ix = {h: i for i, h in enumerate(hdr)}
 tot, cnt = collections.Counter(), collections.Counter()
+metric = sys.argv[2] if len(sys.argv) > 2 else "gpu__time_duration.sum"
 for r in rows[start + 1:]:
+    if "Metric Name" in ix and r[ix["Metric Name"]] != metric:
+        continue
     k = r[ix["Kernel Name"]].split("(")[0][:70]
     tot[k] += float(r[ix["Metric Value"]].replace(",", ""))
     cnt[k] += 1
