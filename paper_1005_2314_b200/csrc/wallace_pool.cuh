@@ -15,6 +15,7 @@
 // reference pins -ffp-contract=off for the same reason
 // (/root/reference/proj/CMakeLists.txt:10-14).
 #include <cuda_runtime.h>
+#include <math_constants.h>
 #ifdef WB_DEBUG_TIMING
 #include <cstdio>
 #endif
@@ -177,6 +178,22 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #endif
 // 1: fp32 mean-zero consumer on f32x2 value pairs with an unclamped
 // histogram fast path (consume_chunk_pairs)
+// owner_chain: chi2_draw inlined as straight-line code per method, the clamp
+// and non-finite bookkeeping behind one rare branch
+#ifndef WB_LEAN_CHAIN
+#define WB_LEAN_CHAIN 1
+#endif
+// consumer: the renormalisation's two sums on the pool's warp (inline
+// neumaier_warp_body) instead of one lane
+#ifndef WB_CONS_NEUM
+#define WB_CONS_NEUM 1
+#endif
+// consumer histogram: floor of the bin coordinate by one round-toward-zero
+// add of 2^23 (FADD, fma pipe) where the bins are known to lie in [0, 256],
+// instead of F2I.FLOOR (a quarter-rate conversion) per value
+#ifndef WB_CONS_RZBIN
+#define WB_CONS_RZBIN 1
+#endif
 #ifndef WB_CONS_PAIRS
 #define WB_CONS_PAIRS 1
 #endif
@@ -339,6 +356,11 @@ __device__ __forceinline__ uint64_t mul2_rn(uint64_t a, uint64_t b) {
 __device__ __forceinline__ uint64_t add2_rn(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2_rz(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 
@@ -511,7 +533,33 @@ __device__ __forceinline__ void owner_chain(SState& s, int slot, double x_last, 
   s.closed = slot;
   if (next) {
     // generator.cpp:358-364 for the next emission
-    const double S = c.disable ? ss : chi2_draw(reserved, c, s.clamp, s.flags);
+    double S;
+    if (WB_LEAN_CHAIN && !c.disable) {
+      // chi2_draw's arithmetic with the method as a uniform branch around
+      // straight-line code; the clamp count and the non-finite flag (rare)
+      // behind one test: v is finite and >= floor in every common case
+      double v;
+      if (c.method == 2) {
+        const double t1 = __dmul_rn(c.a, __dsub_rn(__dmul_rn(reserved, reserved), 1.0));
+        v = __dadd_rn(__dadd_rn(t1, __dmul_rn(c.cubic_c, reserved)), c.nu);
+      } else if (c.method == 0) {
+        const double y = __dadd_rn(reserved, c.shift_c);
+        v = __dmul_rn(__dmul_rn(0.5, y), y);
+      } else {
+        const double y = __dadd_rn(__dmul_rn(c.wh_sqrt_d, reserved), c.wh_one_m_d);
+        v = __dmul_rn(__dmul_rn(__dmul_rn(c.nu, y), y), y);
+      }
+      S = v;
+      if (!(v >= c.floor_v && fabs(v) < CUDART_INF)) {
+        if (!isfinite(reserved)) s.flags |= kFlagChi2NonFinite;
+        if (v < c.floor_v) {
+          ++s.clamp;
+          S = c.floor_v;
+        }
+      }
+    } else {
+      S = c.disable ? ss : chi2_draw(reserved, c, s.clamp, s.flags);
+    }
     const double r = ss > 0.0 ? __dsqrt_rn(__ddiv_rn(S, ss)) : 0.0;
     s.S[slot ^ 1] = S;
     s.r[slot ^ 1] = r;
@@ -718,7 +766,7 @@ __device__ __forceinline__ void neumaier_tile(const double* tb, double* pb, cons
 }
 
 template <typename T, int N>
-__device__ __noinline__ double neumaier_warp(const T* v, double* scr, int lane) {
+__device__ __forceinline__ double neumaier_warp_body(const T* v, double* scr, int lane) {
   static_assert(N % 32 == 0 && N >= 128, "whole tiles, at least four");
   constexpr int NT = N / 32;
   // scr: three slots of [terms 32 | partial sums 32 | errors 32], slot = tile mod 3
@@ -768,6 +816,14 @@ __device__ __noinline__ double neumaier_warp(const T* v, double* scr, int lane) 
   step(NT + 1, F{}, F{}, F{}, Y{});
   return __dadd_rn(sum, comp);
 }
+// Out of line (latency kernels: its registers stay out of the pass loop's
+// allocation) or inline (the consumer kernel: one warp per pool, nothing else
+// is live across the renormalisation but the accumulators, and a call's ABI
+// would spill them).
+template <typename T, int N>
+__device__ __noinline__ double neumaier_warp(const T* v, double* scr, int lane) {
+  return neumaier_warp_body<T, N>(v, scr, lane);
+}
 
 // generator.cpp:345-351 renormalize_.  Contains block barriers: call from
 // all threads.
@@ -776,13 +832,19 @@ __device__ __noinline__ double neumaier_warp(const T* v, double* scr, int lane) 
 // scr: dead shared memory (the other pool buffer) for the warp-parallel sum
 // (latency kernels only: in the throughput kernels other pools hide the
 // one-thread loop, and the call costs more than it saves there), or nullptr.
-template <typename T, int N, int THREADS, bool LAT, bool NB = false>
+template <typename T, int N, int THREADS, bool LAT, bool NB = false, bool INL = false>
 __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid, double* scr = nullptr) {
-  constexpr bool PAR = WB_NEUM_WARP && (LAT || WB_NEUM_WARP == 2) && N >= 128 && N % 32 == 0 && N * sizeof(T) >= 288 * sizeof(double);
+  constexpr bool PAR = WB_NEUM_WARP && (LAT || INL || WB_NEUM_WARP == 2) && N >= 128 && N % 32 == 0 &&
+                       N * sizeof(T) >= 288 * sizeof(double);
   const bool par = PAR && scr != nullptr;
+  auto warp_sum = [&]() -> double {
+    if constexpr (!PAR) return 0.0;
+    else if constexpr (INL) return neumaier_warp_body<T, N>(cur, scr, tid);
+    else return neumaier_warp<T, N>(cur, scr, tid);
+  };
   if (par ? tid < 32 : tid == 0) {
     double ss;
-    if constexpr (PAR) ss = par ? neumaier_warp<T, N>(cur, scr, tid) : neumaier_sq<T, LAT>(cur, N);
+    if constexpr (PAR) ss = par ? warp_sum() : neumaier_sq<T, LAT>(cur, N);
     else ss = neumaier_sq<T, LAT>(cur, N);
     if (tid == 0) {
       // generator.cpp:347 skips only ss <= 0: a NaN sum still rescales (by NaN)
@@ -798,7 +860,7 @@ __device__ __forceinline__ void renormalize(T* cur, SState& s, int tid, double* 
     loop_bar<NB, THREADS>();
     if (par ? tid < 32 : tid == 0) {
       double ss;
-      if constexpr (PAR) ss = par ? neumaier_warp<T, N>(cur, scr, tid) : neumaier_sq<T, LAT>(cur, N);
+      if constexpr (PAR) ss = par ? warp_sum() : neumaier_sq<T, LAT>(cur, N);
       else ss = neumaier_sq<T, LAT>(cur, N);
       if (tid == 0) s.sum_sq = ss;
     }
@@ -1623,7 +1685,11 @@ __device__ __forceinline__ void consume_chunk_pairs(const float (&X)[JCL][4], Co
   using G = Geo<float, LOG2N>;
   const uint64_t sc2 = pk2(sc, sc), zero2 = pk2(0.f, 0.f);
   const uint64_t k16 = pk2(16.f, 16.f), k128 = pk2(128.f, 128.f);
-  int bin[JCL][4];
+  // WB_CONS_RZBIN: the bin coordinates t stay as f32x2 pairs; floor(t) for
+  // t in [0, 256] is the low bits of t + 2^23 added toward zero (the sum lies
+  // in [2^23, 2^24), where the ulp is 1), one FADD2 per pair
+  uint64_t tc[JCL][2];
+  int bin[WB_CONS_RZBIN ? 1 : JCL][4];
   bool tail = false;  // this thread's last block is the pool's last
 #pragma unroll
   for (int j = 0; j < JCL; ++j) {
@@ -1642,25 +1708,63 @@ __device__ __forceinline__ void consume_chunk_pairs(const float (&X)[JCL][4], Co
       cons.p2 = add2_rn(cons.p2, q);
       cons.p3 = fma2_rn(q, y, cons.p3);
       cons.p4 = fma2_rn(q, q, cons.p4);
-      float t0, t1;
-      upk2(fma2_rn(y, k16, k128), t0, t1);
-      bin[j][h] = __float2int_rd(t0);
-      bin[j][h + 1] = __float2int_rd(t1);
+      if constexpr (WB_CONS_RZBIN) {
+        tc[j][h >> 1] = fma2_rn(y, k16, k128);
+      } else {
+        float t0, t1;
+        upk2(fma2_rn(y, k16, k128), t0, t1);
+        bin[j][h] = __float2int_rd(t0);
+        bin[j][h + 1] = __float2int_rd(t1);
+      }
     }
   }
   float q4lo, q4hi;
   upk2(cons.p4, q4lo, q4hi);
-  if (!(q4lo < 4096.f && q4hi < 4096.f)) {
+  const bool inside = q4lo < 4096.f && q4hi < 4096.f;  // every |y| so far < 8: t in [0, 256]
+  if constexpr (WB_CONS_RZBIN) {
+    if (inside) {
+      // hist[floor(t) + 1] = word (bits(t + 2^23) - bits(2^23) + 1): the
+      // constant folds into one base address
+      // (shared addresses mod 2^32: 4 * (1 - 0x4B000000) = 4 - 0x2C000000)
+      const uint64_t big2 = pk2(8388608.f, 8388608.f);
+      const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(cons.hist)) + 4u - 0x2C000000u;
+      auto count = [&](float f) {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hb + (__float_as_uint(f) << 2)));
+      };
+#pragma unroll
+      for (int j = 0; j < JCL; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float f0, f1;
+          upk2(add2_rz(tc[j][h], big2), f0, f1);
+          count(f0);
+          if (!(h == 1 && j == JCL - 1 && tail)) count(f1);
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < JCL; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float t0, t1;
+          upk2(tc[j][h], t0, t1);
+          atomicAdd(&cons.hist[max(-1, min(__float2int_rd(t0), 256)) + 1], 1u);
+          if (!(h == 1 && j == JCL - 1 && tail))
+            atomicAdd(&cons.hist[max(-1, min(__float2int_rd(t1), 256)) + 1], 1u);
+        }
+    }
+  } else {
+    if (!inside) {
+#pragma unroll
+      for (int j = 0; j < JCL; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bin[j][k] = max(-1, min(bin[j][k], 256));
+    }
 #pragma unroll
     for (int j = 0; j < JCL; ++j)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) bin[j][k] = max(-1, min(bin[j][k], 256));
+      for (int k = 0; k < 4; ++k)
+        if (!(k == 3 && j == JCL - 1 && tail)) atomicAdd(&cons.hist[bin[j][k] + 1], 1u);
   }
-#pragma unroll
-  for (int j = 0; j < JCL; ++j)
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (!(k == 3 && j == JCL - 1 && tail)) atomicAdd(&cons.hist[bin[j][k] + 1], 1u);
 }
 
 template <typename T, int LOG2N, int JCL>
@@ -2321,8 +2425,10 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         }
         if (renorm_now) {
           if (G::CHAINW) __syncthreads();  // the chain warp's draw precedes the rescale
-          renormalize<T, N, THREADS, G::LAT>(cur, s, tid,
-                                              G::INPLACE ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
+          // the consumer (one warp per pool): the warp-parallel sums, inline
+          constexpr bool INL = MODE == kModeConsume && WB_CONS_NEUM && THREADS == 32;
+          renormalize<T, N, THREADS, G::LAT, false, INL>(
+              cur, s, tid, G::INPLACE ? nullptr : reinterpret_cast<double*>(pbase + (cur_off ^ FLIP)));
           // refill_ reads sum_sq after step_pass renormalised (generator.cpp:342, 363)
           if (tid == 0) chain_rescale(s, slot, a.chi2, a.sigma);
           __syncthreads();
