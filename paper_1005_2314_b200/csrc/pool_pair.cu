@@ -1,0 +1,493 @@
+// pair_kernel: fp32 pools of N = 4096, wallace4 passes with stride mixing,
+// discard_every = 2 (BASELINE configs 2 and 3) -- two passes per shared-memory
+// round trip.
+//
+// One pass (generator.cpp:64-85) gathers row r = (off + b*STRIDE) mod ROWS of
+// the four columns and writes 4-block b.  The NEXT pass's butterfly for row
+// r2 reads element c*ROWS + r2 = slot r2 & 3 of 4-block c*ROWS/4 + (r2 >> 2):
+// the four 4-blocks q, q + 256, q + 512, q + 768 of one pass are exactly the
+// inputs of the next pass's rows 4q .. 4q+3 (a 4x4 transpose in registers).
+// A thread that owns those four 4-blocks runs both passes without the pool
+// going through shared memory in between: per pass pair the L1TEX data path
+// carries 4 B of gathers and 4 B of stores per value instead of 16 B.
+//
+// A pair is (pA, pB) = (emission e's second pass, emission e+1's first pass):
+// the emission sits between the two, in registers, as natural 4-blocks.
+//
+// Layout L of the pool between pairs (written by pB, gathered by the next
+// pA).  pB's outputs are the 4-blocks b' = ((4q + i - offB) * SINV) mod ROWS,
+// i = 0..3 (SINV = STRIDE^-1 mod ROWS), scattered; the next pA reads rows
+// rho = (offA + (q + 256c')*STRIDE) mod ROWS.  With
+//   - rows rotated by R = offA & ~3 inside each column (rho~ = rho - R; the
+//     plan of the next pass is known when pB stores), and
+//   - 16-byte slot P of rotated 4-block b~: P = (b~ >> 2) + 256 * (b~ & 3),
+// the word of element (column c, rho~) is
+//   256c + 1024*((rho~ >> 2) & 3) + 4*(rho~ >> 4) + (rho~ & 3)
+// and with the thread -> q map  q = SINV * (d - eps) mod 128 (+ 128 g),
+// eps = offA & 3, d = 16a + 4((a + warp) & 3) + k for lane = 4a + k:
+//   - gathers: rho~ mod 128 = d is static per lane, the bank is 4a + k:
+//     32 lanes, 32 banks;
+//   - stores: slot P mod 8 = (SINV*q + const) mod 8, and q mod 8 is distinct
+//     over each 8-lane phase of a 128-bit store;
+//   - the emission's 128-bit stores of natural 4-blocks q + 256c' into the
+//     staging row: q mod 8 distinct over each phase.
+// All three are bank-conflict-free for every plan offset.
+//
+// The emission (N-1 values, so row e of the output starts at an address that
+// is misaligned by e mod 4 elements) is staged as y = x*scale + mean in
+// natural order and sent by TMA tensor stores: their box coordinates are in
+// elements, so no realignment is needed (15 boxes of 256 + one of 252 + 3
+// scalar stores).
+//
+// The host (run_emit) selects this kernel per launch when the launch starts
+// at an emission boundary, no pass of it ends on a renormalisation
+// (pass_count % 256 == 0, generator.cpp:342) and the output rows are
+// 16-byte aligned; everything else runs pool_kernel.
+#include "wallace_pool.cuh"
+
+namespace wb {
+namespace pairk {
+
+constexpr int LOG2N = 12;
+constexpr int N = 1 << LOG2N, ROWS = N / 4, NQ = ROWS / 4;
+constexpr uint32_t S = default_stride_c(ROWS) % ROWS;
+constexpr uint32_t inv_pow2(uint32_t a) {  // a^-1 mod 2^32, a odd
+  uint32_t x = a;
+  for (int i = 0; i < 5; ++i) x *= 2u - a * x;
+  return x;
+}
+constexpr uint32_t SINV = inv_pow2(S) & (ROWS - 1);
+static_assert(((S * SINV) & (ROWS - 1)) == 1, "stride inverse");
+static_assert(NQ == 256, "thread -> q map is written for 256 block quads");
+constexpr uint32_t CSTEP = (NQ * S) & (ROWS - 1);  // row step between a quad's 4-blocks
+static_assert((CSTEP & 127) == 0, "quad rows agree mod 128");
+
+constexpr uint32_t BUF = N * 4;  // bytes per buffer
+// staging rows: 1 (the row is free again once its bulk copy has read it,
+// most of a pair before the next emission is staged) or 2
+#ifndef WB_PAIR_NSG
+#define WB_PAIR_NSG 1
+#endif
+constexpr int NSG = WB_PAIR_NSG;
+constexpr uint32_t SGS = BUF + 16;  // a row holds its emission shifted by up to 3 values
+constexpr uint32_t OFF_L0 = 0, OFF_SG0 = 2 * BUF, OFF_PLANS = OFF_SG0 + NSG * SGS;
+constexpr uint32_t MAX_PLAN_BYTES = 8 * 1024;
+
+// groups (block quads) per thread: 2 -> 128 threads, 1 -> 256 threads
+#ifndef WB_PAIR_G
+#define WB_PAIR_G 2
+#endif
+constexpr int G = WB_PAIR_G;
+constexpr int THREADS = 256 / G;
+constexpr int JB = 4 * G;  // 4-blocks per thread
+#ifndef WB_PAIR_NOCHAIN
+#define WB_PAIR_NOCHAIN 0  // timing only
+#endif
+#ifndef WB_PAIR_POLL_EARLY
+#define WB_PAIR_POLL_EARLY 0  // 1: flag polls behind the gathers (measured slower: 3.89 vs 3.68 ms)
+#endif
+#ifndef WB_PAIR_MINB
+#define WB_PAIR_MINB 4
+#endif
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, float a) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(a) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t addr, float a, float b) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+// butterfly + signed row permutation of J 4-blocks (apply_wallace4 op order,
+// transforms.hpp:89-103; generator.cpp:70-81)
+template <int J>
+__device__ __forceinline__ void bfly(const float (&v)[J][4], uint32_t plan, const float* hs_lut, float (&X)[J][4]) {
+  const uint32_t variant = plan >> 16;
+  const uint32_t perm = variant >> 4;
+  const float4 h = reinterpret_cast<const float4*>(hs_lut)[variant & 15u];
+  const float hs[4] = {h.x, h.y, h.z, h.w};
+  float z[J][4];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const float aa = add_rn(v[j][0], v[j][1]);
+    const float bb = sub_rn(v[j][0], v[j][1]);
+    const float cc = add_rn(v[j][2], v[j][3]);
+    const float dd = sub_rn(v[j][2], v[j][3]);
+    z[j][0] = sub_rn(aa, dd);
+    z[j][1] = add_rn(bb, cc);
+    z[j][2] = sub_rn(bb, cc);
+    z[j][3] = sub_rn(-aa, dd);
+  }
+  switch (perm) {
+#define WB_PERM_CASE(P)                                   \
+  case P:                                                 \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {       \
+      X[j][0] = mul_rn(hs[0], z[j][PermAt<P, 0>::v]);     \
+      X[j][1] = mul_rn(hs[1], z[j][PermAt<P, 1>::v]);     \
+      X[j][2] = mul_rn(hs[2], z[j][PermAt<P, 2>::v]);     \
+      X[j][3] = mul_rn(hs[3], z[j][PermAt<P, 3>::v]);     \
+    }                                                     \
+    break;
+    WB_PERM_CASE(0) WB_PERM_CASE(1) WB_PERM_CASE(2) WB_PERM_CASE(3) WB_PERM_CASE(4)
+    WB_PERM_CASE(5) WB_PERM_CASE(6) WB_PERM_CASE(7) WB_PERM_CASE(8) WB_PERM_CASE(9)
+    WB_PERM_CASE(10) WB_PERM_CASE(11) WB_PERM_CASE(12) WB_PERM_CASE(13) WB_PERM_CASE(14)
+    WB_PERM_CASE(15) WB_PERM_CASE(16) WB_PERM_CASE(17) WB_PERM_CASE(18) WB_PERM_CASE(19)
+    WB_PERM_CASE(20) WB_PERM_CASE(21) WB_PERM_CASE(22) WB_PERM_CASE(23)
+    default: __builtin_unreachable();  // perm = variant >> 4 < 24 (variant = w0 % 384)
+#undef WB_PERM_CASE
+  }
+}
+
+// pB: the pass over rows 4q .. 4q+3 of each group (inputs: slot i of the
+// group's four 4-blocks), stored in layout L rotated for the next pass.
+// X[g*4 + c][k]: 4-block q_g + 256c of the pool before the pass.
+__device__ __forceinline__ void pass_b(const float (&X)[JB][4], uint32_t plan, uint32_t off_next,
+                                       const uint32_t (&tq)[G], uint32_t lbuf, const float* hs_lut) {
+  float v[JB][4], Y[JB][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[g * 4 + i][c] = X[g * 4 + c][i];
+  bfly<JB>(v, plan, hs_lut, Y);
+  const uint32_t off = plan & 0xffffu;
+  const uint32_t rot = off_next >> 2;  // rotation of the next pass, in 4-blocks
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // output 4-block of row 4q + i: b' = ((4q + i - off) * SINV) mod ROWS
+    //   = 4*((q*SINV + m) mod 256) + n with (i - off)*SINV = 4m + n mod ROWS
+    const uint32_t ci = ((uint32_t(i) - off) * SINV) & (ROWS - 1);
+    const uint32_t cr = (ci - rot) & (ROWS - 1);  // low 8 bits: rotated inside the column
+    const uint32_t m1 = (ci >> 2) << 4;
+    const uint32_t m2 = (((cr >> 2) & 63u) << 4) + ((cr & 3u) << 12);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t a1 = (tq[g] << 4) + m1;          // bits 11:10: the column
+      const uint32_t a2 = ((tq[g] & 63u) << 4) + m2;  // bits 9:4: slot in the plane
+      const uint32_t addr = ((a1 & 0xC00u) | (a2 & ~0xC00u)) + lbuf;  // (lbuf is not 4 KiB aligned)
+      sts128(addr, Y[g * 4 + i][0], Y[g * 4 + i][1], Y[g * 4 + i][2], Y[g * 4 + i][3]);
+    }
+  }
+}
+
+// named barriers: 1 = the compute warps' pair barrier; 2, 3 = "staging row of
+// an even / odd emission complete" (compute warps arrive, the service warp waits)
+template <int ID, int NT>
+__device__ __forceinline__ void nbar_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NT) : "memory");
+}
+template <int ID, int NT>
+__device__ __forceinline__ void nbar_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(NT) : "memory");
+}
+// one lane polls, __syncwarp orders the other lanes' reads behind it
+__device__ __forceinline__ void warp_wait_ge(const uint32_t* flag, uint32_t v, int lane) {
+  if (lane == 0)
+    while (ld_acquire_cta(flag) < v) __nanosleep(20);
+  __syncwarp();
+}
+
+struct PairSync {
+  double xl[2];         // pool element N-1 of the emission in each slot (generator.cpp:373)
+  uint32_t xl_ready;    // emissions whose xl is published
+  uint32_t scale_ready; // emissions whose S / r / scale are final (+1: emission 0 at the prologue)
+  uint32_t copied;      // emissions whose staging row has left for global memory
+};
+
+__global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const __grid_constant__ FillArgs a) {
+  extern __shared__ __align__(1024) unsigned char dsm[];
+  uint32_t* const s_plans = reinterpret_cast<uint32_t*>(dsm + OFF_PLANS);
+  __shared__ SState s;
+  __shared__ PairSync ps;
+  __shared__ __align__(16) float s_hs[64];  // sign mask -> (0.5*sign_k)_k (transforms.cpp:88)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NTHR = THREADS + 32;   // compute warps + the service warp
+  constexpr int SERVICE = THREADS / 32;
+  const uint64_t pool = blockIdx.x;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
+  const bool mean_zero = a.mean_is_zero != 0;
+  const float mean_t = __double2float_rn(a.mean);
+
+  // ---- prologue: state, pool (natural order, into L1), plans ----
+  if (tid == 0) {
+    const PoolState& st = a.st_in[pool];
+    s.reserved_prev = st.reserved_prev;
+    s.sum_sq = st.sum_sq;
+    s.cur_scale = st.scale;
+    s.last_chi2 = st.last_chi2;
+    s.last_r = st.r;
+    s.last_scale = st.scale;
+    s.closed = -1;
+    s.clamp = 0;
+    s.flags = st.flags & ~kFlagChi2NonFinite;
+    chain_draw(s, 0, a.chi2, a.sigma);
+    ps.xl_ready = 0;
+    ps.scale_ready = 1;
+    ps.copied = 0;
+  }
+  for (int i = tid; i < 64; i += NTHR) s_hs[i] = ((i >> 2) >> (i & 3)) & 1 ? -0.5f : 0.5f;
+  {
+    const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(a.pools_in) + pool * N);
+    float4* dst = reinterpret_cast<float4*>(dsm + OFF_L0 + BUF);
+    for (int i = tid; i < N / 4; i += NTHR) dst[i] = __ldcs(src + i);
+  }
+  for (uint32_t i = tid; i < a.n_passes; i += NTHR) s_plans[i] = a.plans[pool * a.plan_stride + i];
+  const uint64_t pass0 = a.st_in[pool].pass_count;
+  __syncthreads();
+
+  float* const out_pool = static_cast<float*>(a.out) + pool * a.out_stride + a.out_offset + a.lead;
+  const uint32_t n_emit = a.n_emit;
+  const bool last_full = a.last_limit == uint32_t(N - 1);
+  const uint32_t n_full = last_full ? n_emit : n_emit - 1;  // emissions that go through the staging rows
+
+  if (warp == SERVICE) {
+    // ---- service warp: the per-emission chain (generator.cpp:358-364,
+    // 373-375; chi2.cpp:27-59) off the compute warps' critical path, and the
+    // staging rows to global memory.  Row e of the output starts e mod 4
+    // values off a 16-byte boundary, so the rows leave as 128-byte lines of
+    // 32-bit stores (lane l writes value l of a line) rather than by bulk copies.
+    for (uint32_t e = 0; e < n_full; ++e) {
+      const int slot = e & 1;
+      if (lane == 0) {
+        while (ld_acquire_cta(&ps.xl_ready) < e + 1) __nanosleep(20);
+        if (!WB_PAIR_NOCHAIN) owner_chain(s, slot, ps.xl[slot], e + 1 < n_emit, a.chi2, a.sigma);
+        st_release_cta(&ps.scale_ready, e + 2);
+      }
+      __syncwarp();
+      // every compute thread staged its values of emission e
+      if (e & 1u) nbar_sync<3, NTHR>();
+      else nbar_sync<2, NTHR>();
+      if (a.pad_ab < 2 || a.pad_ab == 4) {
+        // the row holds value i at slot i + sigma, so slot and global address
+        // agree mod 16 bytes: the aligned middle [delta, delta + L) leaves by
+        // one bulk copy, the <= 3 head and <= 3 tail values by scalar stores
+        const float* row = reinterpret_cast<const float*>(dsm + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS);
+        float* const gp = out_pool + size_t(e) * (N - 1);
+        float* gpa = gp;
+        if (a.pad_ab == 4) gpa = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
+        const uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(gpa) >> 2) & 3u;
+        const uint32_t delta = (4u - sigma) & 3u;
+        const uint32_t L = ((uint32_t(N - 1) - delta) / 4u) * 4u;
+        if (lane == 0) {
+          bulk_s2g(gpa + delta, static_cast<uint32_t>(__cvta_generic_to_shared(row + delta + sigma)), L * 4u);
+          bulk_commit();
+        } else if (uint32_t(lane) <= uint32_t(N - 1) - L) {
+          const uint32_t t = lane - 1;
+          const uint32_t i = t < delta ? t : L + t;
+          stg1(gp + i, row[i + sigma]);
+        }
+        __syncwarp();
+        if (lane == 0) bulk_wait_read();
+      }
+      __syncwarp();
+      if (lane == 0) st_release_cta(&ps.copied, e + 1);
+    }
+    if (lane == 0) bulk_wait_all();  // shared memory outlives the copies
+  } else {
+    // lane -> d = 16a + 4e + k (see the header): static part of every gather
+    const uint32_t la = uint32_t(lane) >> 2, lk = uint32_t(lane) & 3u, le = (la + uint32_t(warp)) & 3u;
+    const uint32_t d = 16u * la + 4u * le + lk;
+    const uint32_t lbase = 4u * (1024u * le + 4u * la + lk);
+    const uint32_t g0 = G == 2 ? 0u : (uint32_t(warp) >> 2);  // G == 1: warps 4..7 take the upper quads
+
+    // first pass of emission 0 (pB only): natural 4-blocks in, layout L out
+    {
+      uint32_t tq[G];
+      float X[JB][4];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint32_t q = ((SINV * d) & 127u) + 128u * (g0 + g);
+        tq[g] = (q * SINV) & 255u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 t = lds128(sbase + OFF_L0 + BUF + 16u * q + 4096u * c);
+          X[g * 4 + c][0] = t.x;
+          X[g * 4 + c][1] = t.y;
+          X[g * 4 + c][2] = t.z;
+          X[g * 4 + c][3] = t.w;
+        }
+      }
+      pass_b(X, s_plans[0], s_plans[1] & 0xffffu, tq, sbase + OFF_L0, s_hs);
+    }
+    nbar_sync<1, THREADS>();
+
+    // (a single loop over the passes with one butterfly site -- a third of
+    // the code -- measured slower: 4.00 vs 3.67 ms per 2^32 values)
+    for (uint32_t e = 0; e < n_emit; ++e) {
+      const int slot = e & 1;
+      const bool more = e + 1 < n_emit;
+      const bool full = more || last_full;
+      const uint32_t plan_a = s_plans[2 * e + 1];
+      const uint32_t eps = plan_a & 3u;
+      const uint32_t lcur = sbase + OFF_L0 + (e & 1u) * BUF;
+      const uint32_t lnxt = sbase + OFF_L0 + ((e + 1) & 1u) * BUF;
+
+      // ---- pA: gather from layout L, butterfly ----
+      uint32_t q[G], tq[G];
+      float v[JB][4], X[JB][4];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        q[g] = ((SINV * (d - eps)) & 127u) + 128u * (g0 + g);
+        tq[g] = (q[g] * SINV) & 255u;
+        const uint32_t u = eps + S * q[g];
+#pragma unroll
+        for (int c1 = 0; c1 < 4; ++c1) {
+          const uint32_t ga = lcur + lbase + ((u + CSTEP * c1) & 896u);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[g * 4 + c1][c] = lds32(ga + 1024u * c);
+        }
+      }
+      float sc = 0.f;
+      if (full && a.pad_ab != 3 && WB_PAIR_POLL_EARLY) {
+        // behind the gathers' latency: this emission's scale is final, and
+        // the staging row's previous contents have left
+        if (lane == 0) {
+          while (ld_acquire_cta(&ps.scale_ready) < e + 1) __nanosleep(20);
+          if (e >= uint32_t(NSG))
+            while (ld_acquire_cta(&ps.copied) < e + 1 - uint32_t(NSG)) __nanosleep(20);
+        }
+        __syncwarp();
+        sc = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
+      }
+      bfly<JB>(v, plan_a, s_hs, X);
+
+      // pool element N-1 (4-block ROWS-1 = quad 255, column 3, slot 3) to the chain
+      if (full && q[G - 1] == uint32_t(NQ - 1)) {
+        ps.xl[slot] = static_cast<double>(X[(G - 1) * 4 + 3][3]);
+        st_release_cta(&ps.xl_ready, e + 1);
+      }
+
+      // ---- the emission: y = x*scale + mean into the staging row ----
+      if (full && a.pad_ab != 3) {
+        if (!WB_PAIR_POLL_EARLY) {
+          if (lane == 0) {
+            while (ld_acquire_cta(&ps.scale_ready) < e + 1) __nanosleep(20);
+            if (e >= uint32_t(NSG))
+              while (ld_acquire_cta(&ps.copied) < e + 1 - uint32_t(NSG)) __nanosleep(20);
+          }
+          __syncwarp();
+          sc = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
+        }
+        // value i of the emission goes to slot i + sigma of the row (sigma:
+        // the output row's misalignment in values), so the row's 16-byte
+        // pieces line up with global memory for the bulk copy
+        uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
+        if (a.pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
+        const uint32_t sgs = sbase + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS + 4u * sigma;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int c1 = 0; c1 < 4; ++c1) {
+            const float(&x)[4] = X[g * 4 + c1];
+            const float y0 = emit_value(x[0], sc, mean_t, mean_zero), y1 = emit_value(x[1], sc, mean_t, mean_zero),
+                        y2 = emit_value(x[2], sc, mean_t, mean_zero), y3 = emit_value(x[3], sc, mean_t, mean_zero);
+            const uint32_t ad = sgs + 16u * q[g] + 4096u * c1;
+            if (sigma == 0) {
+              sts128(ad, y0, y1, y2, y3);
+            } else if (sigma == 2) {
+              sts64(ad, y0, y1);
+              sts64(ad + 8, y2, y3);
+            } else {  // 1, 3: the middle pair is 8-byte aligned
+              sts32(ad, y0);
+              sts64(ad + 4, y1, y2);
+              sts32(ad + 12, y3);
+            }
+          }
+        fence_proxy_async_smem();  // the staged values -> visible to the bulk copy
+      }
+      if (full) {
+        if (e & 1u) nbar_arrive<3, NTHR>();
+        else nbar_arrive<2, NTHR>();
+      }
+
+      // ---- pB (the next emission's first pass) or the final pool in natural order ----
+      if (more) {
+        pass_b(X, s_plans[2 * e + 2], s_plans[2 * e + 3] & 0xffffu, tq, lnxt, s_hs);
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int c1 = 0; c1 < 4; ++c1) {
+            const float(&x)[4] = X[g * 4 + c1];
+            sts128(lnxt + 16u * q[g] + 4096u * c1, x[0], x[1], x[2], x[3]);
+          }
+      }
+      nbar_sync<1, THREADS>();
+
+      if (!full) {
+        // the partial last emission, from the natural-order pool
+        warp_wait_ge(&ps.scale_ready, e + 1, lane);
+        const float* nat = reinterpret_cast<const float*>(dsm + OFF_L0 + ((e + 1) & 1u) * BUF);
+        const float scp = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
+        float* const gb = out_pool + size_t(e) * (N - 1);
+        for (uint32_t i = tid; i < a.last_limit; i += THREADS) stg1(gb + i, emit_value(nat[i], scp, mean_t, mean_zero));
+        if (tid == 0) chain_close(s, slot, static_cast<double>(nat[N - 1]));
+      }
+    }
+  }
+  __syncthreads();  // the service warp's last chain and the final pool precede the epilogue
+
+  // ---- epilogue: pool (natural order) and state back to HBM ----
+  {
+    const float4* src = reinterpret_cast<const float4*>(dsm + OFF_L0 + (n_emit & 1u) * BUF);
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.pools_out) + pool * N);
+    for (int i = tid; i < N / 4; i += NTHR) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    PoolState& so = a.st_out[pool];
+    so.reserved_prev = s.reserved_prev;
+    so.sum_sq = s.sum_sq;
+    so.pass_count = pass0 + a.n_passes;
+    so.clamp_count = a.st_in[pool].clamp_count + s.clamp;
+    uint32_t flags = s.flags;
+    // chi2_sample threw in the reference (chi2.cpp:29-31)
+    if (flags & kFlagChi2NonFinite) atomicOr(a.err_word, 1u);
+    flags &= ~(kFlagChi2NonFinite | kFlagLeftover);
+    so.scale = s.closed >= 0 ? s.scale[s.closed] : s.last_scale;
+    so.r = s.last_r;
+    so.last_chi2 = s.closed >= 0 ? s.S[s.closed] : s.last_chi2;
+    so.cursor = a.last_limit;
+    so.flags = flags;
+    so.seed = a.st_in[pool].seed;
+  }
+}
+
+}  // namespace pairk
+
+// a: mode kModeFillPair launch: lead == 0, d == 2, n_passes == 2 * n_emit >= 2
+cudaError_t launch_pair_kernel(const FillArgs& a, uint64_t n_pools, cudaStream_t stream) {
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+  const uint64_t dev_bit = uint64_t(1) << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & dev_bit)) {
+    cudaError_t e = cudaFuncSetAttribute(pairk::pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(pairk::pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(pairk::OFF_PLANS + pairk::MAX_PLAN_BYTES));
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(dev_bit, std::memory_order_release);
+  }
+  if (size_t(a.n_passes) * 4 > pairk::MAX_PLAN_BYTES || a.n_emit < 1 || a.n_passes != 2 * a.n_emit)
+    return cudaErrorInvalidValue;
+  const size_t smem = pairk::OFF_PLANS + ((size_t(a.n_passes) * 4 + 15) & ~size_t(15));
+  pairk::pair_kernel<<<dim3(unsigned(n_pools)), dim3(pairk::THREADS + 32), smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace wb

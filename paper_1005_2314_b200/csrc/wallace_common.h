@@ -72,6 +72,9 @@ enum Mode : int32_t {
                      // copy, a chain warp runs the per-emission chi2/scale
                      // recurrence off the passes' critical path, and
                      // rescale_kernel writes x*scale+mean to the output
+  kModeFillPair = 7, // pair_kernel (pool_pair.cu): fp32 N = 4096, wallace4 +
+                     // stride mixing, discard_every 2: two passes per
+                     // shared-memory round trip, TMA tensor-store emission
 };
 
 struct FillArgs {

@@ -42,6 +42,7 @@ cudaError_t launch_single_pass(int dtype, const FillArgs& a, void* buf_a, void* 
 cudaError_t launch_seed(int dtype, const uint64_t* d_seeds, uint64_t seed_base, uint32_t N, void* pools,
                         PoolState* st, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_plan_kernel(const PlanArgs& a, cudaStream_t s);
+cudaError_t launch_pair_kernel(const FillArgs& a, uint64_t n_pools, cudaStream_t stream);
 cudaError_t launch_rescale(int dtype, const FillArgs& a, uint32_t N, uint64_t n_pools, cudaStream_t s);
 cudaError_t launch_materialize(int dtype, const void* pools, PoolState* st, void* leftover,
                                uint64_t n_pools, uint32_t N, double mean, cudaStream_t s);
@@ -242,6 +243,7 @@ struct wallace_handle {
   bool bulk_ok = false;  // fills may use the bulk-emission kernel
   bool bulk_cfg_ok = false;  // ... as far as the configuration goes (finite pools)
   bool staged_ok = false;  // other fills may use the staged-emission kernel
+  bool pair_ok = false;  // fills may use pair_kernel (pool_pair.cu)
   bool lat_fill_ok = false;  // latency-geometry fills may decouple the chi2 chain (kModeFillLat)
   double* d_scales = nullptr;  // kModeFillLat: [n_pools][plan_cap] per-emission scales
   void* d_lat_raw = nullptr;   // kModeFillLat: [n_pools][lat_rows][N] raw emissions
@@ -516,8 +518,13 @@ wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
     if (k + 1 < ls.size() && (st = plans(k + 1))) return st;
     const wb::FillArgs& a = ls[k].a;
     if (a.n_passes > 0) WB_CUDA(cudaStreamWaitEvent(h->stream, h->ev_planned[k & 1], 0));
-    WB_CUDA(timed(h, h->ev_pool, h->stream,
-                  [&] { return wb::launch_pool_kernel(h->dtype, h->key, a, h->n_pools, h->stream); }));
+    if (a.mode == wb::kModeFillPair) {
+      WB_CUDA(timed(h, h->ev_pool, h->stream,
+                    [&] { return wb::launch_pair_kernel(a, h->n_pools, h->stream); }));
+    } else {
+      WB_CUDA(timed(h, h->ev_pool, h->stream,
+                    [&] { return wb::launch_pool_kernel(h->dtype, h->key, a, h->n_pools, h->stream); }));
+    }
     ++g_launches;
     if (a.mode == wb::kModeFillLat && a.n_emit > 0) {  // the chain's scales onto the raw emissions
       WB_CUDA(wb::launch_rescale(h->dtype, a, static_cast<uint32_t>(h->N), h->n_pools, h->stream));
@@ -617,11 +624,43 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     const uint64_t remaining = count - produced - lead;
     uint64_t e_total = (remaining + n1 - 1) / n1;
     uint64_t e = 0, passes = 0;
+    // pair_kernel: launches that start at an emission and hold no
+    // renormalisation; a partially consumed emission is drained first, and
+    // the emission whose passes reach pass_count % 256 == 0 goes through
+    // pool_kernel on its own
+    const bool pair = h->pair_ok && mode == wb::kModeFill &&
+                      (a.mode == wb::kModeFillBulk || a.mode == wb::kModeFillStaged) && e_total > 0 && out;
+    if (pair && lead > 0) {
+      a.lead = static_cast<uint32_t>(lead);
+      a.n_emit = 0;
+      a.n_passes = 0;
+      a.last_limit = 0;
+      a.lg_pass0 = h->pass_count;
+      ls.push_back(Launch{a});
+      h->cursor += static_cast<uint32_t>(lead);
+      produced += lead;
+      first = false;
+      continue;
+    }
     if (e_total > 0) {
       if (d <= h->plan_cap) {
         e = std::min<uint64_t>(e_total, h->plan_cap / d);
         if (a.mode == wb::kModeFillLat) e = std::min<uint64_t>(e, h->lat_rows);
         if (h->max_emit > 0) e = std::min<uint64_t>(e, h->max_emit);
+        if (pair) {
+          // the first pass of this launch that ends on a renormalisation
+          // (generator.cpp:342) and the emission it belongs to
+          const uint64_t jstar = 256 - h->pass_count % 256;
+          const uint64_t er = (jstar - 1) / d;
+          if (er == 0) {
+            e = 1;
+          } else {
+            e = std::min(e, er);
+            a.mode = wb::kModeFillPair;
+            const char* nt = std::getenv("WALLACE_B200_PAIR_DEBUG");  // timing-only ablations
+            a.pad_ab = nt ? std::atoi(nt) : 0;
+          }
+        }
         passes = e * d;
       } else {
         // an emission longer than one launch: run d-1 passes first, then a
@@ -901,6 +940,14 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
     // sent by bulk copies (WALLACE_B200_NO_STAGED=1: register emission)
     const char* ns = std::getenv("WALLACE_B200_NO_STAGED");
     h->staged_ok = h->pass_type < 2 && !(ns && ns[0] == '1');
+    // fp32 pools of 4096, wallace4 + stride mixing, two passes per emission,
+    // throughput geometry: pair_kernel (pool_pair.cu), opt-in with
+    // WALLACE_B200_PAIR=1 -- bit-exact, but at its current 3.67 ms per 2^32
+    // values it only matches pool_kernel's staged fills and loses to its bulk
+    // fills (profiles/r02_summary.md)
+    const char* np = std::getenv("WALLACE_B200_PAIR");
+    h->pair_ok = dtype == WALLACE_F32 && h->log2n == 12 && h->pass_type == 0 && cfg->discard_every == 2 &&
+                 !h->large && np && np[0] == '1';
     // latency geometry (few pools), wallace4, up to 512 compute threads plus
     // the chain warp (WALLACE_B200_NO_LATFILL=1: the coupled chain)
     const char* nl = std::getenv("WALLACE_B200_NO_LATFILL");

@@ -248,6 +248,15 @@ static_assert(PermAt<1, 2>::v == 3 && PermAt<23, 0>::v == 3 && PermAt<9, 3>::v =
 #ifndef WB_HS_LUT
 #define WB_HS_LUT 1
 #endif
+// wallace4 + stride passes: 8 of the 24 output row permutations folded into
+// the order of the four column gathers (perm3_entry below), 3-way dispatch.
+// Bit-exact (the parity suite passes) but measured slower: the column
+// offsets are not uniform registers for ptxas, so every gather pays an
+// address add, and the table lookup lengthens each pass's preamble
+// (cfg2 3.13 -> 5.70 ms, profiles/r02_summary.md).  Off.
+#ifndef WB_PERM3
+#define WB_PERM3 0
+#endif
 
 // Kernel geometry.  The template key is log2(N) for the throughput kernel
 // (many pools: few warps per pool, 8 4-blocks per thread) and log2(N) + 16
@@ -1328,6 +1337,33 @@ __device__ __forceinline__ void affine_gather4(const char* base, uint32_t buf, u
 // the next buffer.  sb = b0*STRIDE + off for this thread's first block.
 // hook(): work issued right after the pass's gathers (in-order issue: it
 // then overlaps their latency instead of lengthening the pass).
+// The butterfly z(v) = {a-d, b+c, b-c, -a-d}, a = v0+v1, b = v0-v1, c = v2+v3,
+// d = v2-v3 (transforms.hpp:89-103) is, bit for bit, invariant up to an output
+// permutation and output signs under the 8 input permutations generated by
+// v0<->v1, v2<->v3 and (v0,v1)<->(v2,v3): fp addition commutes, x-y = -(y-x)
+// and -x-y = -(x+y) exactly.  Those 8 input orders induce 8 output row
+// permutations (a subgroup of S4 with three cosets), so every one of the 24
+// row permutations src of a variant is   X[k] = (+-hs[k]) * z_{R_t[k]}(v o Q)
+// with R_t one of {0123, 0132, 0312}, Q one of the 8 input orders and a sign
+// mask.  Q is free: the four column gathers are issued in the order Q (their
+// address offsets are warp-uniform), the signs fold into the row factors,
+// and the 24-way register-move dispatch becomes a 3-way one.
+// Entry p (lexicographic permutation index, transforms.cpp:24-35):
+// t | Q[0..3] << 2 (2 bits each) | sign mask << 10.  Derived and checked
+// bitwise on random inputs by tools/perm3_table.py.
+__device__ __forceinline__ uint32_t perm3_entry(uint32_t p) {
+  constexpr uint32_t kTab[24] = {0x390,  0x391,  0x1b84, 0x2b85, 0x392,  0x3386, 0x06d,  0x06c,
+                                 0x06e,  0x307a, 0x1878, 0x2879, 0x152d, 0x252c, 0xd2e,  0x3d3a,
+                                 0x3d38, 0x3d39, 0xed2,  0x3ec6, 0x16d1, 0x26d0, 0x3ec5, 0x3ec4};
+  return kTab[p];
+}
+template <int T_, int K>
+struct Perm3Rep {
+  static constexpr int v = T_ == 0 ? K : (T_ == 1 ? (K == 2 ? 3 : (K == 3 ? 2 : K)) : (K == 0 ? 0 : (K == 1 ? 3 : K - 1)));
+};
+static_assert(Perm3Rep<2, 0>::v == 0 && Perm3Rep<2, 1>::v == 3 && Perm3Rep<2, 2>::v == 1 && Perm3Rep<2, 3>::v == 2,
+              "coset representatives");
+
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -1344,17 +1380,29 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
   const uint32_t off = plan & 0xffffu;
   const uint32_t variant = plan >> 16;
   const uint32_t perm = variant >> 4;
+  constexpr bool P3 = WB_PERM3 && PT == 0 && !((WB_PACKED & 1) && sizeof(T) == 4);
+  // P3: byte offsets of the four column gathers in the order Q, the coset
+  // representative and the signs that fold into the row factors
+  uint32_t co[4] = {0u, uint32_t(ROWS * sizeof(T)), uint32_t(2 * ROWS * sizeof(T)), uint32_t(3 * ROWS * sizeof(T))};
+  uint32_t rep = 0, smask = variant & 15u;
+  if constexpr (P3) {
+    const uint32_t pe = perm3_entry(perm);
+    rep = pe & 3u;
+    smask ^= (pe >> 10) & 15u;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) co[c] = ((pe >> (2 + 2 * c)) & 3u) * uint32_t(ROWS * sizeof(T));
+  }
   T hs[4];
   if constexpr (WB_HS_LUT && sizeof(T) == 4) {
     // the four +-1/2 row factors of this variant's sign mask, one 128-bit load
-    const float4 h = reinterpret_cast<const float4*>(hs_lut)[variant & 15u];
+    const float4 h = reinterpret_cast<const float4*>(hs_lut)[smask];
     hs[0] = h.x;
     hs[1] = h.y;
     hs[2] = h.z;
     hs[3] = h.w;
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) hs[k] = ((variant >> k) & 1u) ? T(-0.5) : T(0.5);
+    for (int k = 0; k < 4; ++k) hs[k] = ((smask >> k) & 1u) ? T(-0.5) : T(0.5);
   }
   // byte offset of row r_j = (off + b_j*STRIDE) mod ROWS, b_j = b0 + 32j
   const uint32_t r0 = (b0 * G::STRIDE + off) * sizeof(T);
@@ -1419,11 +1467,9 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
       vg[j][0] = vg[j][1] = vg[j][2] = vg[j][3] = T(0);
       if ((ROWS >= 32 || b0 + 32 * j < ROWS) && PT == 0) {
         constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
-        const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) + cur_off));
-        vg[j][0] = row[0];
-        vg[j][1] = row[ROWS];
-        vg[j][2] = row[2 * ROWS];
-        vg[j][3] = row[3 * ROWS];
+        const char* row = base + (((r0 + j * step) & MASK4) + cur_off);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) vg[j][c] = *reinterpret_cast<const T*>(row + co[c]);
       }
     }
     hook();
@@ -1439,11 +1485,11 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
     } else if (ROWS >= 32 || b0 + 32 * j < ROWS) {
       if constexpr (PT == 0) {
         constexpr uint32_t step = 32u * G::STRIDE * sizeof(T);
-        const T* row = reinterpret_cast<const T*>(base + (((r0 + j * step) & MASK4) + cur_off));
-        v0 = row[0];
-        v1 = row[ROWS];
-        v2 = row[2 * ROWS];
-        v3 = row[3 * ROWS];
+        const char* row = base + (((r0 + j * step) & MASK4) + cur_off);
+        v0 = *reinterpret_cast<const T*>(row + co[0]);
+        v1 = *reinterpret_cast<const T*>(row + co[1]);
+        v2 = *reinterpret_cast<const T*>(row + co[2]);
+        v3 = *reinterpret_cast<const T*>(row + co[3]);
       } else {
         // affine (generator.cpp:86-110): element 4b+c of the gathered
         // sequence sits at (off + (4b+c)*alpha) mod N
@@ -1467,6 +1513,23 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
     z[j][3] = sub_rn(-aa, dd);
   }
   // signed row permutation: X[k] = (0.5*sign_k) * z[src_k]
+  if constexpr (P3) {
+    switch (rep) {
+#define WB_REP_CASE(R)                                      \
+  case R:                                                   \
+    _Pragma("unroll") for (int j = 0; j < J; ++j) {         \
+      X[j][0] = mul_rn(hs[0], z[j][Perm3Rep<R, 0>::v]);     \
+      X[j][1] = mul_rn(hs[1], z[j][Perm3Rep<R, 1>::v]);     \
+      X[j][2] = mul_rn(hs[2], z[j][Perm3Rep<R, 2>::v]);     \
+      X[j][3] = mul_rn(hs[3], z[j][Perm3Rep<R, 3>::v]);     \
+    }                                                       \
+    break;
+      WB_REP_CASE(0) WB_REP_CASE(1)
+      default:
+        WB_REP_CASE(2)
+#undef WB_REP_CASE
+    }
+  } else
   switch (perm) {
 #define WB_PERM_CASE(P)                                     \
   case P:                                                   \
