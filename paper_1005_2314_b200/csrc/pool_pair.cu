@@ -83,9 +83,6 @@ constexpr int JB = 4 * G;  // 4-blocks per thread
 #ifndef WB_PAIR_NOCHAIN
 #define WB_PAIR_NOCHAIN 0  // timing only
 #endif
-#ifndef WB_PAIR_POLL_EARLY
-#define WB_PAIR_POLL_EARLY 0  // 1: flag polls behind the gathers (measured slower: 3.89 vs 3.68 ms)
-#endif
 #ifndef WB_PAIR_MINB
 #define WB_PAIR_MINB 4
 #endif
@@ -193,19 +190,56 @@ template <int ID, int NT>
 __device__ __forceinline__ void nbar_arrive() {
   asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(NT) : "memory");
 }
-// one lane polls, __syncwarp orders the other lanes' reads behind it
-__device__ __forceinline__ void warp_wait_ge(const uint32_t* flag, uint32_t v, int lane) {
-  if (lane == 0)
-    while (ld_acquire_cta(flag) < v) __nanosleep(20);
-  __syncwarp();
+// service warp <-> compute warps, all through mbarriers (count 1; arrive =
+// release, try_wait = acquire): emission e uses slot e & 1 of xl / scale and
+// waits for completion e >> 1 of that slot's barrier; staging row e % NSG is
+// free again at completion e / NSG (+1: pre-arrived in the prologue).
+struct PairSync {
+  double xl[2];                       // pool element N-1 of the emission in each slot (generator.cpp:373)
+  __align__(8) uint64_t mb_xl[2];     // xl[slot] published (owner thread)
+  __align__(8) uint64_t mb_scale[2];  // S / r / scale of the slot final (service warp; slot 0 pre-arrived)
+  __align__(8) uint64_t mb_copied[2]; // staging row read by its bulk copy (service warp; pre-arrived)
+};
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m)))
+               : "memory");
 }
 
-struct PairSync {
-  double xl[2];         // pool element N-1 of the emission in each slot (generator.cpp:373)
-  uint32_t xl_ready;    // emissions whose xl is published
-  uint32_t scale_ready; // emissions whose S / r / scale are final (+1: emission 0 at the prologue)
-  uint32_t copied;      // emissions whose staging row has left for global memory
-};
+// the emission's values y = x*scale + mean of one thread's JB natural
+// 4-blocks into the staging row: value i at slot i + sigma (sigma = the
+// output row's misalignment in values), so the row's 16-byte pieces line up
+// with global memory for the bulk copy.  SG = sigma class: 0 aligned, 2 even,
+// 1 odd (the middle pair is 8-byte aligned for sigma = 1 and 3).
+template <bool MZ, int SG>
+__device__ __forceinline__ void stage_rows(const float (&X)[JB][4], const uint32_t (&q)[G], uint32_t sgs, float sc,
+                                           float mean_t) {
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int c1 = 0; c1 < 4; ++c1) {
+      const float(&x)[4] = X[g * 4 + c1];
+      const float y0 = emit_value(x[0], sc, mean_t, MZ), y1 = emit_value(x[1], sc, mean_t, MZ),
+                  y2 = emit_value(x[2], sc, mean_t, MZ), y3 = emit_value(x[3], sc, mean_t, MZ);
+      const uint32_t ad = sgs + 16u * q[g] + 4096u * c1;
+      if (SG == 0) {
+        sts128(ad, y0, y1, y2, y3);
+      } else if (SG == 2) {
+        sts64(ad, y0, y1);
+        sts64(ad + 8, y2, y3);
+      } else {
+        sts32(ad, y0);
+        sts64(ad + 4, y1, y2);
+        sts32(ad + 12, y3);
+      }
+    }
+}
+template <bool MZ>
+__device__ __forceinline__ void stage_emission(const float (&X)[JB][4], const uint32_t (&q)[G], uint32_t sgs,
+                                               uint32_t sigma, float sc, float mean_t) {
+  if (sigma == 0) stage_rows<MZ, 0>(X, q, sgs, sc, mean_t);
+  else if (sigma == 2) stage_rows<MZ, 2>(X, q, sgs, sc, mean_t);
+  else stage_rows<MZ, 1>(X, q, sgs, sc, mean_t);
+}
 
 __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const __grid_constant__ FillArgs a) {
   extern __shared__ __align__(1024) unsigned char dsm[];
@@ -235,9 +269,14 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     s.clamp = 0;
     s.flags = st.flags & ~kFlagChi2NonFinite;
     chain_draw(s, 0, a.chi2, a.sigma);
-    ps.xl_ready = 0;
-    ps.scale_ready = 1;
-    ps.copied = 0;
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&ps.mb_xl[i], 1);
+      mbar_init(&ps.mb_scale[i], 1);
+      mbar_init(&ps.mb_copied[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive(&ps.mb_scale[0]);  // emission 0's scale: chain_draw above
+    for (int i = 0; i < NSG; ++i) mbar_arrive(&ps.mb_copied[i]);  // the rows start free
   }
   for (int i = tid; i < 64; i += NTHR) s_hs[i] = ((i >> 2) >> (i & 3)) & 1 ? -0.5f : 0.5f;
   {
@@ -263,9 +302,9 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     for (uint32_t e = 0; e < n_full; ++e) {
       const int slot = e & 1;
       if (lane == 0) {
-        while (ld_acquire_cta(&ps.xl_ready) < e + 1) __nanosleep(20);
+        mbar_wait_parity(&ps.mb_xl[slot], (e >> 1) & 1u);
         if (!WB_PAIR_NOCHAIN) owner_chain(s, slot, ps.xl[slot], e + 1 < n_emit, a.chi2, a.sigma);
-        st_release_cta(&ps.scale_ready, e + 2);
+        mbar_arrive(&ps.mb_scale[slot ^ 1]);
       }
       __syncwarp();
       // every compute thread staged its values of emission e
@@ -294,7 +333,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         if (lane == 0) bulk_wait_read();
       }
       __syncwarp();
-      if (lane == 0) st_release_cta(&ps.copied, e + 1);
+      if (lane == 0) mbar_arrive(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u]);
     }
     if (lane == 0) bulk_wait_all();  // shared memory outlives the copies
   } else {
@@ -351,62 +390,26 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
           for (int c = 0; c < 4; ++c) v[g * 4 + c1][c] = lds32(ga + 1024u * c);
         }
       }
-      float sc = 0.f;
-      if (full && a.pad_ab != 3 && WB_PAIR_POLL_EARLY) {
-        // behind the gathers' latency: this emission's scale is final, and
-        // the staging row's previous contents have left
-        if (lane == 0) {
-          while (ld_acquire_cta(&ps.scale_ready) < e + 1) __nanosleep(20);
-          if (e >= uint32_t(NSG))
-            while (ld_acquire_cta(&ps.copied) < e + 1 - uint32_t(NSG)) __nanosleep(20);
-        }
-        __syncwarp();
-        sc = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
-      }
       bfly<JB>(v, plan_a, s_hs, X);
 
       // pool element N-1 (4-block ROWS-1 = quad 255, column 3, slot 3) to the chain
       if (full && q[G - 1] == uint32_t(NQ - 1)) {
         ps.xl[slot] = static_cast<double>(X[(G - 1) * 4 + 3][3]);
-        st_release_cta(&ps.xl_ready, e + 1);
+        mbar_arrive(&ps.mb_xl[slot]);
       }
 
       // ---- the emission: y = x*scale + mean into the staging row ----
       if (full && a.pad_ab != 3) {
-        if (!WB_PAIR_POLL_EARLY) {
-          if (lane == 0) {
-            while (ld_acquire_cta(&ps.scale_ready) < e + 1) __nanosleep(20);
-            if (e >= uint32_t(NSG))
-              while (ld_acquire_cta(&ps.copied) < e + 1 - uint32_t(NSG)) __nanosleep(20);
-          }
-          __syncwarp();
-          sc = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
-        }
-        // value i of the emission goes to slot i + sigma of the row (sigma:
-        // the output row's misalignment in values), so the row's 16-byte
-        // pieces line up with global memory for the bulk copy
+        // this emission's scale is final, and the staging row's previous
+        // contents have left
+        mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
+        mbar_wait_parity(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u], (NSG == 2 ? (e >> 1) : e) & 1u);
+        const float sc = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
         uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
         if (a.pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
         const uint32_t sgs = sbase + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS + 4u * sigma;
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-          for (int c1 = 0; c1 < 4; ++c1) {
-            const float(&x)[4] = X[g * 4 + c1];
-            const float y0 = emit_value(x[0], sc, mean_t, mean_zero), y1 = emit_value(x[1], sc, mean_t, mean_zero),
-                        y2 = emit_value(x[2], sc, mean_t, mean_zero), y3 = emit_value(x[3], sc, mean_t, mean_zero);
-            const uint32_t ad = sgs + 16u * q[g] + 4096u * c1;
-            if (sigma == 0) {
-              sts128(ad, y0, y1, y2, y3);
-            } else if (sigma == 2) {
-              sts64(ad, y0, y1);
-              sts64(ad + 8, y2, y3);
-            } else {  // 1, 3: the middle pair is 8-byte aligned
-              sts32(ad, y0);
-              sts64(ad + 4, y1, y2);
-              sts32(ad + 12, y3);
-            }
-          }
+        if (mean_zero) stage_emission<true>(X, q, sgs, sigma, sc, mean_t);
+        else stage_emission<false>(X, q, sgs, sigma, sc, mean_t);
         fence_proxy_async_smem();  // the staged values -> visible to the bulk copy
       }
       if (full) {
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
 
       if (!full) {
         // the partial last emission, from the natural-order pool
-        warp_wait_ge(&ps.scale_ready, e + 1, lane);
+        mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
         const float* nat = reinterpret_cast<const float*>(dsm + OFF_L0 + ((e + 1) & 1u) * BUF);
         const float scp = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
         float* const gb = out_pool + size_t(e) * (N - 1);
