@@ -147,6 +147,51 @@ __device__ __forceinline__ void bfly(const float (&v)[J][4], uint32_t plan, cons
   }
 }
 
+// Row permutation p as packed 2-bit fields: bits 2k+1:2k = src[k] (slot k of
+// an output block is z[src[k]], transforms.cpp:24-35), bits 8+2m+1:8+2m =
+// the slot that z[m] goes to.
+constexpr uint32_t perm_pack(int p) {
+  uint32_t w = 0;
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t m = uint32_t(perm_at(p, k));
+    w |= m << (2 * k);
+    w |= uint32_t(k) << (8 + 2 * m);
+  }
+  return w;
+}
+#define WB_PP4(a) perm_pack(a), perm_pack(a + 1), perm_pack(a + 2), perm_pack(a + 3)
+__constant__ uint32_t c_perm_pack[24] = {WB_PP4(0), WB_PP4(4), WB_PP4(8), WB_PP4(12), WB_PP4(16), WB_PP4(20)};
+#undef WB_PP4
+
+// butterfly whose output blocks keep z's order: Y[j][m] = (0.5*sign_k) * z[m]
+// with k the slot z[m] belongs to -- the same products as bfly, slot k of the
+// block held in position src[k].  No dispatch over the permutation: pB's
+// blocks go to shared memory like this and the next pA's gathers (one slot
+// per lane) read position src[slot] instead.
+template <int J>
+__device__ __forceinline__ void bfly_raw(const float (&v)[J][4], uint32_t plan, const float* hs_lut,
+                                         float (&Y)[J][4]) {
+  const uint32_t variant = plan >> 16;
+  const uint32_t pk = c_perm_pack[variant >> 4] >> 8;
+  const float* hsv = hs_lut + 4u * (variant & 15u);
+  const float hm[4] = {hsv[pk & 3u], hsv[(pk >> 2) & 3u], hsv[(pk >> 4) & 3u], hsv[(pk >> 6) & 3u]};
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const float aa = add_rn(v[j][0], v[j][1]);
+    const float bb = sub_rn(v[j][0], v[j][1]);
+    const float cc = add_rn(v[j][2], v[j][3]);
+    const float dd = sub_rn(v[j][2], v[j][3]);
+    Y[j][0] = mul_rn(hm[0], sub_rn(aa, dd));
+    Y[j][1] = mul_rn(hm[1], add_rn(bb, cc));
+    Y[j][2] = mul_rn(hm[2], sub_rn(bb, cc));
+    Y[j][3] = mul_rn(hm[3], sub_rn(-aa, dd));
+  }
+}
+// position of slot k in a block stored by bfly_raw under `plan`
+__device__ __forceinline__ uint32_t raw_slot(uint32_t plan, uint32_t k) {
+  return (c_perm_pack[plan >> 20] >> (2u * k)) & 3u;
+}
+
 // pB: the pass over rows 4q .. 4q+3 of each group (inputs: slot i of the
 // group's four 4-blocks), stored in layout L rotated for the next pass.
 // X[g*4 + c][k]: 4-block q_g + 256c of the pool before the pass.
@@ -159,7 +204,7 @@ __device__ __forceinline__ void pass_b(const float (&X)[JB][4], uint32_t plan, u
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[g * 4 + i][c] = X[g * 4 + c][i];
-  bfly<JB>(v, plan, hs_lut, Y);
+  bfly_raw<JB>(v, plan, hs_lut, Y);
   const uint32_t off = plan & 0xffffu;
   const uint32_t rot = off_next >> 2;  // rotation of the next pass, in 4-blocks
 #pragma unroll
@@ -340,7 +385,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     // lane -> d = 16a + 4e + k (see the header): static part of every gather
     const uint32_t la = uint32_t(lane) >> 2, lk = uint32_t(lane) & 3u, le = (la + uint32_t(warp)) & 3u;
     const uint32_t d = 16u * la + 4u * le + lk;
-    const uint32_t lbase = 4u * (1024u * le + 4u * la + lk);
+    const uint32_t lbase = 4u * (1024u * le + 4u * la);  // + the lane's slot position (raw_slot)
     const uint32_t g0 = G == 2 ? 0u : (uint32_t(warp) >> 2);  // G == 1: warps 4..7 take the upper quads
 
     // first pass of emission 0 (pB only): natural 4-blocks in, layout L out
@@ -372,7 +417,8 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       const bool full = more || last_full;
       const uint32_t plan_a = s_plans[2 * e + 1];
       const uint32_t eps = plan_a & 3u;
-      const uint32_t lcur = sbase + OFF_L0 + (e & 1u) * BUF;
+      // the blocks in shared memory were stored by bfly_raw under the previous pass's plan
+      const uint32_t lcur = sbase + OFF_L0 + (e & 1u) * BUF + 4u * raw_slot(s_plans[2 * e], lk);
       const uint32_t lnxt = sbase + OFF_L0 + ((e + 1) & 1u) * BUF;
 
       // ---- pA: gather from layout L, butterfly ----
