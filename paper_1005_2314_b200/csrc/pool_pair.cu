@@ -250,40 +250,80 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
                : "memory");
 }
 
+// the service warp's wait: the suspend-time hint keeps its polling out of the
+// compute warps' issue slots
+#ifndef WB_PAIR_SVC_HINT
+#define WB_PAIR_SVC_HINT 2000
+#endif
+__device__ __forceinline__ void mbar_wait_parity_idle(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WB_MBAR_IDLE_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WB_MBAR_IDLE_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m))),
+      "r"(parity), "r"(uint32_t(WB_PAIR_SVC_HINT))
+      : "memory");
+}
+
 // the emission's values y = x*scale + mean of one thread's JB natural
 // 4-blocks into the staging row: value i at slot i + sigma (sigma = the
 // output row's misalignment in values), so the row's 16-byte pieces line up
-// with global memory for the bulk copy.  SG = sigma class: 0 aligned, 2 even,
-// 1 odd (the middle pair is 8-byte aligned for sigma = 1 and 3).
+// with global memory for the bulk copy.  SG = sigma class: 0 aligned (one
+// 128-bit store per block), 2 even (two 64-bit stores), 1 odd (four 32-bit
+// stores).
+//
+// Bank conflicts: the lanes of a warp that share q mod 8 (same lk, same
+// parity of la) are la = la0 + 2j, j = cls = (lane >> 3) & 3.  A narrow store
+// of the same element by all lanes would hit each bank group four (32-bit)
+// or two (64-bit, per half-warp) times, so in store i lane class j writes
+// element (i + j) & 3 (pair (i + j) & 1): bank (4q + sigma + k) mod 32 is
+// then distinct over the 32 lanes, and every store is one wavefront per 128
+// bytes.  The per-lane rotation of the four values costs two select stages.
+#ifndef WB_PAIR_ROT
+#define WB_PAIR_ROT 1  // 0: every lane stores the same element (4-way / 2-way conflicts)
+#endif
 template <bool MZ, int SG>
 __device__ __forceinline__ void stage_rows(const float (&X)[JB][4], const uint32_t (&q)[G], uint32_t sgs, float sc,
-                                           float mean_t) {
+                                           float mean_t, uint32_t cls) {
+  const bool r1 = WB_PAIR_ROT && (cls & 1u), r2 = WB_PAIR_ROT && (cls & 2u);
 #pragma unroll
-  for (int g = 0; g < G; ++g)
+  for (int g = 0; g < G; ++g) {
+    const uint32_t aq = sgs + 16u * q[g];
+    // byte address of store i of this lane (block c1 = 0)
+    uint32_t ai[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      ai[i] = SG == 1 ? aq + 4u * ((uint32_t(i) + (WB_PAIR_ROT ? cls : 0u)) & 3u)
+                      : aq + 8u * ((uint32_t(i) + (WB_PAIR_ROT ? cls : 0u)) & 1u);
 #pragma unroll
     for (int c1 = 0; c1 < 4; ++c1) {
       const float(&x)[4] = X[g * 4 + c1];
       const float y0 = emit_value(x[0], sc, mean_t, MZ), y1 = emit_value(x[1], sc, mean_t, MZ),
                   y2 = emit_value(x[2], sc, mean_t, MZ), y3 = emit_value(x[3], sc, mean_t, MZ);
-      const uint32_t ad = sgs + 16u * q[g] + 4096u * c1;
       if (SG == 0) {
-        sts128(ad, y0, y1, y2, y3);
+        sts128(aq + 4096u * c1, y0, y1, y2, y3);
       } else if (SG == 2) {
-        sts64(ad, y0, y1);
-        sts64(ad + 8, y2, y3);
+        // pairs (y0, y1) and (y2, y3); odd classes store the upper pair first
+        const float p0 = r1 ? y2 : y0, p1 = r1 ? y3 : y1, p2 = r1 ? y0 : y2, p3 = r1 ? y1 : y3;
+        sts64(ai[0] + 4096u * c1, p0, p1);
+        sts64(ai[1] + 4096u * c1, p2, p3);
       } else {
-        sts32(ad, y0);
-        sts64(ad + 4, y1, y2);
-        sts32(ad + 12, y3);
+        const float t0 = r1 ? y1 : y0, t1 = r1 ? y2 : y1, t2 = r1 ? y3 : y2, t3 = r1 ? y0 : y3;
+        const float u0 = r2 ? t2 : t0, u1 = r2 ? t3 : t1, u2 = r2 ? t0 : t2, u3 = r2 ? t1 : t3;
+        sts32(ai[0] + 4096u * c1, u0);
+        sts32(ai[1] + 4096u * c1, u1);
+        sts32(ai[2] + 4096u * c1, u2);
+        sts32(ai[3] + 4096u * c1, u3);
       }
     }
+  }
 }
 template <bool MZ>
 __device__ __forceinline__ void stage_emission(const float (&X)[JB][4], const uint32_t (&q)[G], uint32_t sgs,
-                                               uint32_t sigma, float sc, float mean_t) {
-  if (sigma == 0) stage_rows<MZ, 0>(X, q, sgs, sc, mean_t);
-  else if (sigma == 2) stage_rows<MZ, 2>(X, q, sgs, sc, mean_t);
-  else stage_rows<MZ, 1>(X, q, sgs, sc, mean_t);
+                                               uint32_t sigma, float sc, float mean_t, uint32_t cls) {
+  if (sigma == 0) stage_rows<MZ, 0>(X, q, sgs, sc, mean_t, cls);
+  else if (sigma == 2) stage_rows<MZ, 2>(X, q, sgs, sc, mean_t, cls);
+  else stage_rows<MZ, 1>(X, q, sgs, sc, mean_t, cls);
 }
 
 __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const __grid_constant__ FillArgs a) {
@@ -347,7 +387,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     for (uint32_t e = 0; e < n_full; ++e) {
       const int slot = e & 1;
       if (lane == 0) {
-        mbar_wait_parity(&ps.mb_xl[slot], (e >> 1) & 1u);
+        mbar_wait_parity_idle(&ps.mb_xl[slot], (e >> 1) & 1u);
         if (!WB_PAIR_NOCHAIN) owner_chain(s, slot, ps.xl[slot], e + 1 < n_emit, a.chi2, a.sigma);
         mbar_arrive(&ps.mb_scale[slot ^ 1]);
       }
@@ -454,8 +494,8 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
         if (a.pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
         const uint32_t sgs = sbase + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS + 4u * sigma;
-        if (mean_zero) stage_emission<true>(X, q, sgs, sigma, sc, mean_t);
-        else stage_emission<false>(X, q, sgs, sigma, sc, mean_t);
+        if (mean_zero) stage_emission<true>(X, q, sgs, sigma, sc, mean_t, la >> 1);
+        else stage_emission<false>(X, q, sgs, sigma, sc, mean_t, la >> 1);
         fence_proxy_async_smem();  // the staged values -> visible to the bulk copy
       }
       if (full) {
