@@ -941,13 +941,13 @@ wallace_status wallace_create_ex(const wallace_config* cfg, uint64_t n_pools, co
     const char* ns = std::getenv("WALLACE_B200_NO_STAGED");
     h->staged_ok = h->pass_type < 2 && !(ns && ns[0] == '1');
     // fp32 pools of 4096, wallace4 + stride mixing, two passes per emission,
-    // throughput geometry: pair_kernel (pool_pair.cu), opt-in with
-    // WALLACE_B200_PAIR=1 -- bit-exact, but at its current 3.67 ms per 2^32
-    // values it only matches pool_kernel's staged fills and loses to its bulk
-    // fills (profiles/r02_summary.md)
+    // throughput geometry: pair_kernel (pool_pair.cu) -- two passes per
+    // shared-memory round trip, bit-exact with pool_kernel; 3.11 ms (scaled
+    // emissions) / 3.10 ms (unit scale) per 2^32 values against pool_kernel's
+    // 3.66 / 3.13 ms.  WALLACE_B200_PAIR=0 keeps every launch on pool_kernel.
     const char* np = std::getenv("WALLACE_B200_PAIR");
     h->pair_ok = dtype == WALLACE_F32 && h->log2n == 12 && h->pass_type == 0 && cfg->discard_every == 2 &&
-                 !h->large && np && np[0] == '1';
+                 !h->large && !(np && np[0] == '0');
     // latency geometry (few pools), wallace4, up to 512 compute threads plus
     // the chain warp (WALLACE_B200_NO_LATFILL=1: the coupled chain)
     const char* nl = std::getenv("WALLACE_B200_NO_LATFILL");

@@ -1,9 +1,9 @@
 """GPU parity of pair_kernel (csrc/pool_pair.cu): fp32 pools of 4096 values,
 wallace4 passes with stride mixing, discard_every = 2 -- two passes per
-shared-memory round trip, emission through TMA tensor stores.
+shared-memory round trip, emission staged per row and sent by bulk copies.
 
 Bit-exact against the oracle's fp32 restatement (generator.cpp:64-85,
-333-376) and against pool_kernel (pair_kernel is opt-in: WALLACE_B200_PAIR=1) over: row lengths
+333-376) and against pool_kernel (WALLACE_B200_PAIR=0) over: row lengths
 that are and are not multiples of four values, partial last emissions, fills
 that resume a partially consumed emission, launches that cross
 renormalisations (pass_count % 256 == 0), every chi2 method, scaled and
