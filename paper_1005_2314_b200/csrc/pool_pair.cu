@@ -226,7 +226,10 @@ __device__ __forceinline__ void pass_b(const float (&X)[JB][4], uint32_t plan, u
 }
 
 // named barriers: 1 = the compute warps' pair barrier; 2, 3 = "staging row of
-// an even / odd emission complete" (compute warps arrive, the service warp waits)
+// an even / odd emission complete", 4, 5 = "pool element N-1 of an even / odd
+// emission published" (compute warps arrive, the service warp waits; two
+// ids each: an arrival for emission e + 2 follows the service warp's wait
+// for emission e through the staging row's hand-back)
 template <int ID, int NT>
 __device__ __forceinline__ void nbar_sync() {
   asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NT) : "memory");
@@ -235,34 +238,19 @@ template <int ID, int NT>
 __device__ __forceinline__ void nbar_arrive() {
   asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(NT) : "memory");
 }
-// service warp <-> compute warps, all through mbarriers (count 1; arrive =
-// release, try_wait = acquire): emission e uses slot e & 1 of xl / scale and
-// waits for completion e >> 1 of that slot's barrier; staging row e % NSG is
-// free again at completion e / NSG (+1: pre-arrived in the prologue).
+// service warp -> compute warps through mbarriers (count 1; arrive =
+// release, try_wait = acquire; normally complete when waited for): emission
+// e uses slot e & 1 of xl / scale and waits for completion e >> 1 of the
+// slot's barrier; staging row e % NSG is free again at completion e / NSG
+// (+1: pre-arrived in the prologue).  Compute -> service: named barriers.
 struct PairSync {
   double xl[2];                       // pool element N-1 of the emission in each slot (generator.cpp:373)
-  __align__(8) uint64_t mb_xl[2];     // xl[slot] published (owner thread)
   __align__(8) uint64_t mb_scale[2];  // S / r / scale of the slot final (service warp; slot 0 pre-arrived)
   __align__(8) uint64_t mb_copied[2]; // staging row read by its bulk copy (service warp; pre-arrived)
 };
 __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m)))
                : "memory");
-}
-
-// the service warp's wait: the suspend-time hint keeps its polling out of the
-// compute warps' issue slots
-#ifndef WB_PAIR_SVC_HINT
-#define WB_PAIR_SVC_HINT 2000
-#endif
-__device__ __forceinline__ void mbar_wait_parity_idle(uint64_t* m, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WB_MBAR_IDLE_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WB_MBAR_IDLE_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m))),
-      "r"(parity), "r"(uint32_t(WB_PAIR_SVC_HINT))
-      : "memory");
 }
 
 // the emission's values y = x*scale + mean of one thread's JB natural
@@ -355,7 +343,6 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     s.flags = st.flags & ~kFlagChi2NonFinite;
     chain_draw(s, 0, a.chi2, a.sigma);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&ps.mb_xl[i], 1);
       mbar_init(&ps.mb_scale[i], 1);
       mbar_init(&ps.mb_copied[i], 1);
     }
@@ -386,8 +373,11 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     // 32-bit stores (lane l writes value l of a line) rather than by bulk copies.
     for (uint32_t e = 0; e < n_full; ++e) {
       const int slot = e & 1;
+      // xl[slot] is published: a hardware barrier, so the service warp
+      // takes no issue slots while it waits
+      if (e & 1u) nbar_sync<5, NTHR>();
+      else nbar_sync<4, NTHR>();
       if (lane == 0) {
-        mbar_wait_parity_idle(&ps.mb_xl[slot], (e >> 1) & 1u);
         if (!WB_PAIR_NOCHAIN) owner_chain(s, slot, ps.xl[slot], e + 1 < n_emit, a.chi2, a.sigma);
         mbar_arrive(&ps.mb_scale[slot ^ 1]);
       }
@@ -479,9 +469,11 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       bfly<JB>(v, plan_a, s_hs, X);
 
       // pool element N-1 (4-block ROWS-1 = quad 255, column 3, slot 3) to the chain
-      if (full && q[G - 1] == uint32_t(NQ - 1)) {
-        ps.xl[slot] = static_cast<double>(X[(G - 1) * 4 + 3][3]);
-        mbar_arrive(&ps.mb_xl[slot]);
+      if (full) {
+        if (q[G - 1] == uint32_t(NQ - 1)) ps.xl[slot] = static_cast<double>(X[(G - 1) * 4 + 3][3]);
+        __syncwarp();
+        if (e & 1u) nbar_arrive<5, NTHR>();
+        else nbar_arrive<4, NTHR>();
       }
 
       // ---- the emission: y = x*scale + mean into the staging row ----
