@@ -107,6 +107,48 @@ __device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c,
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
+// Packed f32x2 butterfly stages (FADD2 on sm_100: two independently rounded
+// lanes per instruction, bit-identical to the scalar adds; the negations fold
+// into operand modifiers).  lo / hi = two 4-blocks; z as in apply_wallace4
+// (transforms.hpp:89-103): z0 = a - d, z1 = b + c, z2 = b - c, z3 = -a - d.
+#ifndef WB_PAIR_PACKED
+#define WB_PAIR_PACKED 1
+#endif
+__device__ __forceinline__ uint64_t neg2(uint64_t a) {
+  float lo, hi;
+  upk2(a, lo, hi);
+  return pk2(-lo, -hi);
+}
+__device__ __forceinline__ void bfly_z2(const float (&vl)[4], const float (&vh)[4], float (&zl)[4], float (&zh)[4]) {
+  const uint64_t v0 = pk2(vl[0], vh[0]), v1 = pk2(vl[1], vh[1]), v2 = pk2(vl[2], vh[2]), v3 = pk2(vl[3], vh[3]);
+  const uint64_t aa = add2_rn(v0, v1), bb = add2_rn(v0, neg2(v1)), cc = add2_rn(v2, v3), dd = add2_rn(v2, neg2(v3));
+  upk2(add2_rn(aa, neg2(dd)), zl[0], zh[0]);
+  upk2(add2_rn(bb, cc), zl[1], zh[1]);
+  upk2(add2_rn(bb, neg2(cc)), zl[2], zh[2]);
+  upk2(add2_rn(neg2(aa), neg2(dd)), zl[3], zh[3]);
+}
+__device__ __forceinline__ void bfly_z1(const float (&v)[4], float (&z)[4]) {
+  const float aa = add_rn(v[0], v[1]);
+  const float bb = sub_rn(v[0], v[1]);
+  const float cc = add_rn(v[2], v[3]);
+  const float dd = sub_rn(v[2], v[3]);
+  z[0] = sub_rn(aa, dd);
+  z[1] = add_rn(bb, cc);
+  z[2] = sub_rn(bb, cc);
+  z[3] = sub_rn(-aa, dd);
+}
+template <int J>
+__device__ __forceinline__ void bfly_z(const float (&v)[J][4], float (&z)[J][4]) {
+  static_assert(J % 2 == 0, "blocks in pairs");
+  if (WB_PAIR_PACKED) {
+#pragma unroll
+    for (int j = 0; j < J; j += 2) bfly_z2(v[j], v[j + 1], z[j], z[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < J; ++j) bfly_z1(v[j], z[j]);
+  }
+}
+
 // butterfly + signed row permutation of J 4-blocks (apply_wallace4 op order,
 // transforms.hpp:89-103; generator.cpp:70-81)
 template <int J>
@@ -116,17 +158,7 @@ __device__ __forceinline__ void bfly(const float (&v)[J][4], uint32_t plan, cons
   const float4 h = reinterpret_cast<const float4*>(hs_lut)[variant & 15u];
   const float hs[4] = {h.x, h.y, h.z, h.w};
   float z[J][4];
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const float aa = add_rn(v[j][0], v[j][1]);
-    const float bb = sub_rn(v[j][0], v[j][1]);
-    const float cc = add_rn(v[j][2], v[j][3]);
-    const float dd = sub_rn(v[j][2], v[j][3]);
-    z[j][0] = sub_rn(aa, dd);
-    z[j][1] = add_rn(bb, cc);
-    z[j][2] = sub_rn(bb, cc);
-    z[j][3] = sub_rn(-aa, dd);
-  }
+  bfly_z<J>(v, z);
   switch (perm) {
 #define WB_PERM_CASE(P)                                   \
   case P:                                                 \
@@ -175,17 +207,12 @@ __device__ __forceinline__ void bfly_raw(const float (&v)[J][4], uint32_t plan, 
   const uint32_t pk = c_perm_pack[variant >> 4] >> 8;
   const float* hsv = hs_lut + 4u * (variant & 15u);
   const float hm[4] = {hsv[pk & 3u], hsv[(pk >> 2) & 3u], hsv[(pk >> 4) & 3u], hsv[(pk >> 6) & 3u]};
+  float z[J][4];
+  bfly_z<J>(v, z);
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const float aa = add_rn(v[j][0], v[j][1]);
-    const float bb = sub_rn(v[j][0], v[j][1]);
-    const float cc = add_rn(v[j][2], v[j][3]);
-    const float dd = sub_rn(v[j][2], v[j][3]);
-    Y[j][0] = mul_rn(hm[0], sub_rn(aa, dd));
-    Y[j][1] = mul_rn(hm[1], add_rn(bb, cc));
-    Y[j][2] = mul_rn(hm[2], sub_rn(bb, cc));
-    Y[j][3] = mul_rn(hm[3], sub_rn(-aa, dd));
-  }
+  for (int j = 0; j < J; ++j)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) Y[j][m] = mul_rn(hm[m], z[j][m]);
 }
 // position of slot k in a block stored by bfly_raw under `plan`
 __device__ __forceinline__ uint32_t raw_slot(uint32_t plan, uint32_t k) {
@@ -286,8 +313,16 @@ __device__ __forceinline__ void stage_rows(const float (&X)[JB][4], const uint32
 #pragma unroll
     for (int c1 = 0; c1 < 4; ++c1) {
       const float(&x)[4] = X[g * 4 + c1];
-      const float y0 = emit_value(x[0], sc, mean_t, MZ), y1 = emit_value(x[1], sc, mean_t, MZ),
-                  y2 = emit_value(x[2], sc, mean_t, MZ), y3 = emit_value(x[3], sc, mean_t, MZ);
+      float y0, y1, y2, y3;
+      if (MZ && WB_PAIR_PACKED) {
+        // fma(x, scale, +0) on slot pairs (emit_value's mean-zero form)
+        const uint64_t sc2 = pk2(sc, sc), z2 = pk2(0.f, 0.f);
+        upk2(fma2_rn(pk2(x[0], x[1]), sc2, z2), y0, y1);
+        upk2(fma2_rn(pk2(x[2], x[3]), sc2, z2), y2, y3);
+      } else {
+        y0 = emit_value(x[0], sc, mean_t, MZ), y1 = emit_value(x[1], sc, mean_t, MZ);
+        y2 = emit_value(x[2], sc, mean_t, MZ), y3 = emit_value(x[3], sc, mean_t, MZ);
+      }
       if (SG == 0) {
         sts128(aq + 4096u * c1, y0, y1, y2, y3);
       } else if (SG == 2) {
