@@ -272,6 +272,7 @@ __device__ __forceinline__ void nbar_arrive() {
 // (+1: pre-arrived in the prologue).  Compute -> service: named barriers.
 struct PairSync {
   double xl[2];                       // pool element N-1 of the emission in each slot (generator.cpp:373)
+  float scf[2];                       // (float)scale of the emission in each slot
   __align__(8) uint64_t mb_scale[2];  // S / r / scale of the slot final (service warp; slot 0 pre-arrived)
   __align__(8) uint64_t mb_copied[2]; // staging row read by its bulk copy (service warp; pre-arrived)
 };
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       mbar_init(&ps.mb_copied[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    ps.scf[0] = __double2float_rn(s.scale[0]);
     mbar_arrive(&ps.mb_scale[0]);  // emission 0's scale: chain_draw above
     for (int i = 0; i < NSG; ++i) mbar_arrive(&ps.mb_copied[i]);  // the rows start free
   }
@@ -414,6 +416,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       else nbar_sync<4, NTHR>();
       if (lane == 0) {
         if (!WB_PAIR_NOCHAIN) owner_chain(s, slot, ps.xl[slot], e + 1 < n_emit, a.chi2, a.sigma);
+        ps.scf[slot ^ 1] = __double2float_rn(s.scale[slot ^ 1]);
         mbar_arrive(&ps.mb_scale[slot ^ 1]);
       }
       __syncwarp();
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         // contents have left
         mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
         mbar_wait_parity(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u], (NSG == 2 ? (e >> 1) : e) & 1u);
-        const float sc = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
+        const float sc = *static_cast<volatile float*>(&ps.scf[slot]);
         uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
         if (a.pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
         const uint32_t sgs = sbase + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS + 4u * sigma;
@@ -548,7 +551,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         // the partial last emission, from the natural-order pool
         mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
         const float* nat = reinterpret_cast<const float*>(dsm + OFF_L0 + ((e + 1) & 1u) * BUF);
-        const float scp = __double2float_rn(*static_cast<volatile double*>(&s.scale[slot]));
+        const float scp = *static_cast<volatile float*>(&ps.scf[slot]);
         float* const gb = out_pool + size_t(e) * (N - 1);
         for (uint32_t i = tid; i < a.last_limit; i += THREADS) stg1(gb + i, emit_value(nat[i], scp, mean_t, mean_zero));
         if (tid == 0) chain_close(s, slot, static_cast<double>(nat[N - 1]));
