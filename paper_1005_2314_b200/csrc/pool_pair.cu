@@ -252,6 +252,52 @@ __device__ __forceinline__ void pass_b(const float (&X)[JB][4], uint32_t plan, u
   }
 }
 
+// The plan-dependent constants of pass_b, one set per row i of a quad:
+// m1 / m2 as in pass_b and hm = bfly_raw's factors.  Uniform over the CTA,
+// so the service warp's lanes 0..3 compute them one pair ahead (make_passb)
+// and the compute warps read them with three broadcast loads (pass_b_desc).
+struct PassB {
+  uint32_t m1[4], m2[4];
+  float hm[4];
+};
+__device__ __forceinline__ void make_passb(uint32_t plan, uint32_t off_next, uint32_t i, const float* hs_lut,
+                                           uint32_t& m1, uint32_t& m2, float& hm) {
+  const uint32_t off = plan & 0xffffu, rot = off_next >> 2;
+  const uint32_t ci = ((i - off) * SINV) & (ROWS - 1);
+  const uint32_t cr = (ci - rot) & (ROWS - 1);
+  m1 = (ci >> 2) << 4;
+  m2 = (((cr >> 2) & 63u) << 4) + ((cr & 3u) << 12);
+  const uint32_t variant = plan >> 16;
+  const uint32_t pk = c_perm_pack[variant >> 4] >> 8;
+  hm = hs_lut[4u * (variant & 15u) + ((pk >> (2u * i)) & 3u)];
+}
+__device__ __forceinline__ void pass_b_desc(const float (&X)[JB][4], const PassB& d, const uint32_t (&tq)[G],
+                                            uint32_t lbuf) {
+  float v[JB][4], z[JB][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[g * 4 + i][c] = X[g * 4 + c][i];
+  bfly_z<JB>(v, z);
+  uint32_t t16[G], t6[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    t16[g] = tq[g] << 4;
+    t6[g] = (tq[g] & 63u) << 4;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t a1 = t16[g] + d.m1[i], a2 = t6[g] + d.m2[i];
+      const uint32_t addr = ((a1 & 0xC00u) | (a2 & ~0xC00u)) + lbuf;
+      const float(&zz)[4] = z[g * 4 + i];
+      sts128(addr, mul_rn(d.hm[0], zz[0]), mul_rn(d.hm[1], zz[1]), mul_rn(d.hm[2], zz[2]), mul_rn(d.hm[3], zz[3]));
+    }
+}
+
 // named barriers: 1 = the compute warps' pair barrier; 2, 3 = "staging row of
 // an even / odd emission complete", 4, 5 = "pool element N-1 of an even / odd
 // emission published" (compute warps arrive, the service warp waits; two
@@ -273,6 +319,10 @@ __device__ __forceinline__ void nbar_arrive() {
 struct PairSync {
   double xl[2];                       // pool element N-1 of the emission in each slot (generator.cpp:373)
   float scf[2];                       // (float)scale of the emission in each slot
+  // pB of the pair in each slot, precomputed by the service warp (PassB)
+  __align__(16) uint32_t d_m1[2][4];
+  __align__(16) uint32_t d_m2[2][4];
+  __align__(16) float d_hm[2][4];
   __align__(8) uint64_t mb_scale[2];  // S / r / scale of the slot final (service warp; slot 0 pre-arrived)
   __align__(8) uint64_t mb_copied[2]; // staging row read by its bulk copy (service warp; pre-arrived)
 };
@@ -396,6 +446,9 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
   for (uint32_t i = tid; i < a.n_passes; i += NTHR) s_plans[i] = a.plans[pool * a.plan_stride + i];
   const uint64_t pass0 = a.st_in[pool].pass_count;
   __syncthreads();
+  if (tid < 4 && a.n_emit > 1)
+    make_passb(s_plans[2], s_plans[3] & 0xffffu, tid, s_hs, ps.d_m1[0][tid], ps.d_m2[0][tid], ps.d_hm[0][tid]);
+  __syncthreads();
 
   float* const out_pool = static_cast<float*>(a.out) + pool * a.out_stride + a.out_offset + a.lead;
   const uint32_t n_emit = a.n_emit;
@@ -417,8 +470,13 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       if (lane == 0) {
         if (!WB_PAIR_NOCHAIN) owner_chain(s, slot, ps.xl[slot], e + 1 < n_emit, a.chi2, a.sigma);
         ps.scf[slot ^ 1] = __double2float_rn(s.scale[slot ^ 1]);
-        mbar_arrive(&ps.mb_scale[slot ^ 1]);
       }
+      // pB of pair e + 1 (plans 2e + 4, 2e + 5), handed over with the scale
+      if (lane < 4 && e + 2 < n_emit)
+        make_passb(s_plans[2 * e + 4], s_plans[2 * e + 5] & 0xffffu, lane, s_hs, ps.d_m1[slot ^ 1][lane],
+                   ps.d_m2[slot ^ 1][lane], ps.d_hm[slot ^ 1][lane]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.mb_scale[slot ^ 1]);
       __syncwarp();
       // every compute thread staged its values of emission e
       if (e & 1u) nbar_sync<3, NTHR>();
@@ -515,10 +573,10 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       }
 
       // ---- the emission: y = x*scale + mean into the staging row ----
+      // this emission's scale (and the pair's pB constants) are final
+      if (full) mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
       if (full && a.pad_ab != 3) {
-        // this emission's scale is final, and the staging row's previous
-        // contents have left
-        mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
+        // the staging row's previous contents have left
         mbar_wait_parity(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u], (NSG == 2 ? (e >> 1) : e) & 1u);
         const float sc = *static_cast<volatile float*>(&ps.scf[slot]);
         uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
@@ -535,7 +593,18 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
 
       // ---- pB (the next emission's first pass) or the final pool in natural order ----
       if (more) {
-        pass_b(X, s_plans[2 * e + 2], s_plans[2 * e + 3] & 0xffffu, tq, lnxt, s_hs);
+        PassB d;
+        {
+          const float4 m1 = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ps.d_m1[slot])));
+          const float4 m2 = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ps.d_m2[slot])));
+          const float4 hm = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ps.d_hm[slot])));
+          d.m1[0] = __float_as_uint(m1.x), d.m1[1] = __float_as_uint(m1.y);
+          d.m1[2] = __float_as_uint(m1.z), d.m1[3] = __float_as_uint(m1.w);
+          d.m2[0] = __float_as_uint(m2.x), d.m2[1] = __float_as_uint(m2.y);
+          d.m2[2] = __float_as_uint(m2.z), d.m2[3] = __float_as_uint(m2.w);
+          d.hm[0] = hm.x, d.hm[1] = hm.y, d.hm[2] = hm.z, d.hm[3] = hm.w;
+        }
+        pass_b_desc(X, d, tq, lnxt);
       } else {
 #pragma unroll
         for (int g = 0; g < G; ++g)
