@@ -248,6 +248,7 @@ def measure(cfg_id, steps, warmup, e2e_steps, pools_override=0, rank=0, world=1,
     if dist:
         dist.barrier()
     launches0 = pb.kernel_launches()
+    pair0 = pb.pair_kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     L = pb._capi.load()
@@ -267,6 +268,8 @@ def measure(cfg_id, steps, warmup, e2e_steps, pools_override=0, rank=0, world=1,
     batch.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = pb.kernel_launches() - launches0
+    # fp32 N=4096 d=2 wallace4/stride fills run pair_kernel (csrc/pool_pair.cu)
+    kname = "pair_kernel" if pb.pair_kernel_launches() > pair0 else "pool_kernel"
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -284,7 +287,7 @@ def measure(cfg_id, steps, warmup, e2e_steps, pools_override=0, rank=0, world=1,
         tr = ncu_traffic(cfg_id)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
-                    "kernel": "pool_kernel", "kernel_ms": per_launch_ms,
+                    "kernel": kname, "kernel_ms": per_launch_ms,
                     "kernel_share_of_step": pool_ms.value / max(1e-9, pool_ms.value + plan_ms.value),
                     "algorithmic_bytes_per_launch": alg_bytes}
     else:

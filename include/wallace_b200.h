@@ -289,6 +289,11 @@ wallace_status wallace_synchronize(wallace_handle* h);
 
 /* Number of kernels this library has launched (all handles). */
 uint64_t wallace_kernel_launches(void);
+/* ... of which pair_kernel (fp32 pools of 4096, wallace4 + stride mixing,
+ * discard_every = 2: two passes per shared-memory round trip; the other
+ * fills run pool_kernel).  WALLACE_B200_PAIR=0 keeps every fill on
+ * pool_kernel. */
+uint64_t wallace_pair_kernel_launches(void);
 
 /* Message of the last failed call on this thread. */
 const char* wallace_last_error(void);

@@ -29,7 +29,7 @@ from . import _capi
 
 __all__ = ["GeneratorConfig", "PoolBatch", "ConfigError", "InvalidParameterError",
            "UnsupportedError", "CudaError", "boxmuller_consume", "baseline_consume", "BaselineStreams",
-           "BaselineState", "chi2_sample", "kernel_launches"]
+           "BaselineState", "chi2_sample", "kernel_launches", "pair_kernel_launches"]
 
 
 class ConfigError(ValueError):
@@ -461,6 +461,11 @@ def chi2_sample(x: float, nu: int, method: int = 2):
 
 def kernel_launches() -> int:
     return int(_capi.load().wallace_kernel_launches())
+
+
+def pair_kernel_launches() -> int:
+    """Launches of pair_kernel (csrc/pool_pair.cu) among kernel_launches()."""
+    return int(_capi.load().wallace_pair_kernel_launches())
 
 
 def moment_reports(sums, n: int):

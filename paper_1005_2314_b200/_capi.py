@@ -115,6 +115,7 @@ SYMBOLS = [
     ("wallace_set_stream", i32, [vp, vp]),
     ("wallace_synchronize", i32, [vp]),
     ("wallace_kernel_launches", u64, []),
+    ("wallace_pair_kernel_launches", u64, []),
     ("wallace_last_error", C.c_char_p, []),
     ("wallace_validate_config", i32, [P(wallace_config)]),
     ("wallace_host_seed_pool", i32, [P(wallace_config), u64, P(f64), P(f64), P(f64), P(u64), P(u64)]),

@@ -34,10 +34,27 @@
 // All three are bank-conflict-free for every plan offset.
 //
 // The emission (N-1 values, so row e of the output starts at an address that
-// is misaligned by e mod 4 elements) is staged as y = x*scale + mean in
-// natural order and sent by TMA tensor stores: their box coordinates are in
-// elements, so no realignment is needed (15 boxes of 256 + one of 252 + 3
-// scalar stores).
+// is misaligned by sigma = e mod 4 elements) is staged as y = x*scale + mean
+// with value i at slot i + sigma of a staging row, so the row's 16-byte
+// pieces line up with global memory, and leaves by one cp.async.bulk (the
+// <= 3 head / tail values by scalar stores).  The blocks of a misaligned row
+// go out as 32- or 64-bit stores; lane class j = (lane >> 3) & 3 writes
+// element (i + j) & 3 in store i so that the 32 lanes hit 32 banks
+// (stage_rows).  (TMA tensor stores would take element coordinates, but
+// their global address must be 16-byte aligned: tools/probes/tma_probe.cu.)
+//
+// pB keeps no 24-way dispatch over the row permutation: its blocks go to
+// shared memory in butterfly order (bfly_raw) and the next pA -- one slot per
+// lane -- gathers position src[slot]; only pA, whose blocks are emitted,
+// needs the natural slot order.  The add stages of both butterflies and the
+// emission scaling run on f32x2 pairs (FADD2 / FFMA2, bit-identical).
+//
+// A service warp (warp THREADS/32) runs the per-emission chi2 chain
+// (generator.cpp:358-364, 373-375), precomputes the next pair's pB
+// constants (make_passb) and issues the bulk copies.  Compute -> service
+// hand-offs are named barriers (the service warp sleeps in hardware),
+// service -> compute hand-offs are mbarriers that are normally complete when
+// waited for.
 //
 // The host (run_emit) selects this kernel per launch when the launch starts
 // at an emission boundary, no pass of it ends on a renormalisation
@@ -481,12 +498,13 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       // every compute thread staged its values of emission e
       if (e & 1u) nbar_sync<3, NTHR>();
       else nbar_sync<2, NTHR>();
-      if (a.pad_ab < 2 || a.pad_ab == 4) {
+      if (a.pad_ab < 2 || a.pad_ab >= 4) {
         // the row holds value i at slot i + sigma, so slot and global address
         // agree mod 16 bytes: the aligned middle [delta, delta + L) leaves by
         // one bulk copy, the <= 3 head and <= 3 tail values by scalar stores
         const float* row = reinterpret_cast<const float*>(dsm + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS);
-        float* const gp = out_pool + size_t(e) * (N - 1);
+        // (5, timing only: four output rows per pool, resident in L2)
+        float* const gp = out_pool + size_t(a.pad_ab == 5 ? (e & 3u) : e) * (N - 1);
         float* gpa = gp;
         if (a.pad_ab == 4) gpa = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
         const uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(gpa) >> 2) & 3u;

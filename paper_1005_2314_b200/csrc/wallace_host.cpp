@@ -62,6 +62,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_pair_launches{0};  // of which pair_kernel (pool_pair.cu)
 
 wallace_status fail(wallace_status code, const char* fmt, ...) {
   char buf[512];
@@ -521,6 +522,7 @@ wallace_status issue(wallace_handle* h, std::vector<Launch>& ls) {
     if (a.mode == wb::kModeFillPair) {
       WB_CUDA(timed(h, h->ev_pool, h->stream,
                     [&] { return wb::launch_pair_kernel(a, h->n_pools, h->stream); }));
+      ++g_pair_launches;
     } else {
       WB_CUDA(timed(h, h->ev_pool, h->stream,
                     [&] { return wb::launch_pool_kernel(h->dtype, h->key, a, h->n_pools, h->stream); }));
@@ -750,6 +752,7 @@ extern "C" {
 const char* wallace_last_error(void) { return g_err.c_str(); }
 
 uint64_t wallace_kernel_launches(void) { return g_launches.load(); }
+uint64_t wallace_pair_kernel_launches(void) { return g_pair_launches.load(); }
 
 wallace_status wallace_validate_config(const wallace_config* cfg) { return validate(cfg); }
 
