@@ -510,8 +510,18 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         const uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(gpa) >> 2) & 3u;
         const uint32_t delta = (4u - sigma) & 3u;
         const uint32_t L = ((uint32_t(N - 1) - delta) / 4u) * 4u;
+#ifndef WB_PAIR_SPLIT
+#define WB_PAIR_SPLIT 1  // bulk copies per row (measurement knob)
+#endif
         if (lane == 0) {
-          bulk_s2g(gpa + delta, static_cast<uint32_t>(__cvta_generic_to_shared(row + delta + sigma)), L * 4u);
+          const uint32_t src0 = static_cast<uint32_t>(__cvta_generic_to_shared(row + delta + sigma));
+          constexpr uint32_t PIECE = (uint32_t(N) / WB_PAIR_SPLIT) * 4u;  // bytes, a multiple of 16
+#pragma unroll
+          for (int k = 0; k < WB_PAIR_SPLIT; ++k) {
+            const uint32_t o = uint32_t(k) * PIECE;
+            const uint32_t bytes = k + 1 < WB_PAIR_SPLIT ? PIECE : L * 4u - o;
+            bulk_s2g(reinterpret_cast<char*>(gpa + delta) + o, src0 + o, bytes);
+          }
           bulk_commit();
         } else if (uint32_t(lane) <= uint32_t(N - 1) - L) {
           const uint32_t t = lane - 1;
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
           stg1(gp + i, row[i + sigma]);
         }
         __syncwarp();
-        if (lane == 0) bulk_wait_read();
+        if (lane == 0 && a.pad_ab != 6) bulk_wait_read();  // (6, timing only: the row is handed back at once)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u]);
