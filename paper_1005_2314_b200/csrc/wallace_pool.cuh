@@ -477,6 +477,18 @@ static __device__ double chi2_draw(double x, const Chi2Consts& c, uint32_t& clam
   return s;
 }
 
+// 128-bit shared store of p ? (b0, b1) : (a0, a1), selected as 32-bit halves
+#ifndef WB_F64_SWZ_B32
+#define WB_F64_SWZ_B32 1
+#endif
+__device__ __forceinline__ void sts_sel_b32(uint32_t addr, bool p, double a0, double a1, double b0, double b1) {
+  const uint32_t r0 = p ? uint32_t(__double2loint(b0)) : uint32_t(__double2loint(a0));
+  const uint32_t r1 = p ? uint32_t(__double2hiint(b0)) : uint32_t(__double2hiint(a0));
+  const uint32_t r2 = p ? uint32_t(__double2loint(b1)) : uint32_t(__double2loint(a1));
+  const uint32_t r3 = p ? uint32_t(__double2hiint(b1)) : uint32_t(__double2hiint(a1));
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+}
+
 struct SState {
   double reserved_prev;
   double sum_sq;
@@ -1011,10 +1023,16 @@ __device__ __forceinline__ void emit_chunk(const T (&X)[Geo<T, LOG2N>::JC][4], i
   auto put_block = [&](T* p, const T* w) {
     if constexpr (VEC == 2 && (SMD || STAGED)) {
       const bool sw = (lane & 4) != 0;
-      const T fa[2] = {sw ? w[2] : w[0], sw ? w[3] : w[1]};
-      const T fb[2] = {sw ? w[0] : w[2], sw ? w[1] : w[3]};
-      put_vec(p + (sw ? 2 : 0), fa);
-      put_vec(p + (sw ? 0 : 2), fb);
+      if constexpr (WB_F64_SWZ_B32) {
+        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+        sts_sel_b32(a0 + (sw ? 16u : 0u), sw, w[0], w[1], w[2], w[3]);
+        sts_sel_b32(a0 + (sw ? 0u : 16u), sw, w[2], w[3], w[0], w[1]);
+      } else {
+        const T fa[2] = {sw ? w[2] : w[0], sw ? w[3] : w[1]};
+        const T fb[2] = {sw ? w[0] : w[2], sw ? w[1] : w[3]};
+        put_vec(p + (sw ? 2 : 0), fa);
+        put_vec(p + (sw ? 0 : 2), fb);
+      }
     } else {
 #pragma unroll
       for (int v = 0; v < 4; v += VEC) put_vec(p + v, w + v);
@@ -1574,7 +1592,14 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
         double2* q = reinterpret_cast<double2*>(nb + 4 * b);
         const double2 lo = make_double2(X[j][0], X[j][1]);
         const double2 hi = make_double2(X[j][2], X[j][3]);
-        if constexpr (SWZ) {
+        if constexpr (SWZ && WB_F64_SWZ_B32) {
+          // the same two stores with the selects on 32-bit halves and the
+          // data as four 32-bit registers (keeps ptxas from funnelling every
+          // store through one register quad)
+          const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(q));
+          sts_sel_b32(a0 + (swz ? 16u : 0u), swz, X[j][0], X[j][1], X[j][2], X[j][3]);
+          sts_sel_b32(a0 + (swz ? 0u : 16u), swz, X[j][2], X[j][3], X[j][0], X[j][1]);
+        } else if constexpr (SWZ) {
           q[swz ? 1 : 0] = swz ? hi : lo;
           q[swz ? 0 : 1] = swz ? lo : hi;
         } else {
@@ -1599,10 +1624,16 @@ template <typename T>
 __device__ __forceinline__ void store_block(T* nb, uint32_t b, T x0, T x1, T x2, T x3) {
   if constexpr (sizeof(T) == 8) {
     const bool swz = (b >> 2) & 1;
-    double2* q = reinterpret_cast<double2*>(nb + 4 * b);
-    const double2 lo = make_double2(x0, x1), hi = make_double2(x2, x3);
-    q[swz ? 1 : 0] = swz ? hi : lo;
-    q[swz ? 0 : 1] = swz ? lo : hi;
+    if constexpr (WB_F64_SWZ_B32) {
+      const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(nb + 4 * b));
+      sts_sel_b32(a0 + (swz ? 16u : 0u), swz, x0, x1, x2, x3);
+      sts_sel_b32(a0 + (swz ? 0u : 16u), swz, x2, x3, x0, x1);
+    } else {
+      double2* q = reinterpret_cast<double2*>(nb + 4 * b);
+      const double2 lo = make_double2(x0, x1), hi = make_double2(x2, x3);
+      q[swz ? 1 : 0] = swz ? hi : lo;
+      q[swz ? 0 : 1] = swz ? lo : hi;
+    }
   } else {
     sts4(nb + 4 * b, x0, x1, x2, x3);
   }
