@@ -510,6 +510,9 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         const uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(gpa) >> 2) & 3u;
         const uint32_t delta = (4u - sigma) & 3u;
         const uint32_t L = ((uint32_t(N - 1) - delta) / 4u) * 4u;
+#ifndef WB_PAIR_L2HINT
+#define WB_PAIR_L2HINT 0  // 1 evict_first, 2 evict_last on the output copies (measurement knob)
+#endif
 #ifndef WB_PAIR_SPLIT
 #define WB_PAIR_SPLIT 1  // bulk copies per row (measurement knob)
 #endif
@@ -520,7 +523,19 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
           for (int k = 0; k < WB_PAIR_SPLIT; ++k) {
             const uint32_t o = uint32_t(k) * PIECE;
             const uint32_t bytes = k + 1 < WB_PAIR_SPLIT ? PIECE : L * 4u - o;
+#if WB_PAIR_L2HINT
+            {
+              uint64_t pol;
+              if (WB_PAIR_L2HINT == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+              else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+              asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                               reinterpret_cast<char*>(gpa + delta) + o),
+                           "r"(src0 + o), "r"(bytes), "l"(pol)
+                           : "memory");
+            }
+#else
             bulk_s2g(reinterpret_cast<char*>(gpa + delta) + o, src0 + o, bytes);
+#endif
           }
           bulk_commit();
         } else if (uint32_t(lane) <= uint32_t(N - 1) - L) {
