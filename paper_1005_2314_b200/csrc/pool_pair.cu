@@ -328,6 +328,12 @@ template <int ID, int NT>
 __device__ __forceinline__ void nbar_arrive() {
   asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(NT) : "memory");
 }
+// The compute warps' pair barrier, split: a warp arrives when its pB stores
+// are done and waits just before the next pair's first gather, so the next
+// pair's address arithmetic runs while the other warps finish.
+#ifndef WB_PAIR_SPLITBAR
+#define WB_PAIR_SPLITBAR 0  // measured equal (2.849 vs 2.847 ms): the named barrier stays
+#endif
 // service warp -> compute warps through mbarriers (count 1; arrive =
 // release, try_wait = acquire; normally complete when waited for): emission
 // e uses slot e & 1 of xl / scale and waits for completion e >> 1 of the
@@ -342,6 +348,7 @@ struct PairSync {
   __align__(16) float d_hm[2][4];
   __align__(8) uint64_t mb_scale[2];  // S / r / scale of the slot final (service warp; slot 0 pre-arrived)
   __align__(8) uint64_t mb_copied[2]; // staging row read by its bulk copy (service warp; pre-arrived)
+  __align__(8) uint64_t mb_pair;      // WB_PAIR_SPLITBAR: the compute warps' pair barrier (one arrival per warp)
 };
 __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(m)))
@@ -449,6 +456,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       mbar_init(&ps.mb_scale[i], 1);
       mbar_init(&ps.mb_copied[i], 1);
     }
+    mbar_init(&ps.mb_pair, THREADS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     ps.scf[0] = __double2float_rn(s.scale[0]);
     mbar_arrive(&ps.mb_scale[0]);  // emission 0's scale: chain_draw above
@@ -576,7 +584,12 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       }
       pass_b(X, s_plans[0], s_plans[1] & 0xffffu, tq, sbase + OFF_L0, s_hs);
     }
-    nbar_sync<1, THREADS>();
+    if (WB_PAIR_SPLITBAR) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.mb_pair);
+    } else {
+      nbar_sync<1, THREADS>();
+    }
 
     // (a single loop over the passes with one butterfly site -- a third of
     // the code -- measured slower: 4.00 vs 3.67 ms per 2^32 values)
@@ -593,18 +606,23 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       // ---- pA: gather from layout L, butterfly ----
       uint32_t q[G], tq[G];
       float v[JB][4], X[JB][4];
+      uint32_t ga[G][4];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         q[g] = ((SINV * (d - eps)) & 127u) + 128u * (g0 + g);
         tq[g] = (q[g] * SINV) & 255u;
         const uint32_t u = eps + S * q[g];
 #pragma unroll
-        for (int c1 = 0; c1 < 4; ++c1) {
-          const uint32_t ga = lcur + lbase + ((u + CSTEP * c1) & 896u);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) v[g * 4 + c1][c] = lds32(ga + 1024u * c);
-        }
+        for (int c1 = 0; c1 < 4; ++c1) ga[g][c1] = lcur + lbase + ((u + CSTEP * c1) & 896u);
       }
+      // every warp's pB stores of the previous pair (completion e of mb_pair)
+      if (WB_PAIR_SPLITBAR) mbar_wait_parity(&ps.mb_pair, e & 1u);
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int c1 = 0; c1 < 4; ++c1)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[g * 4 + c1][c] = lds32(ga[g][c1] + 1024u * c);
       bfly<JB>(v, plan_a, s_hs, X);
 
       // pool element N-1 (4-block ROWS-1 = quad 255, column 3, slot 3) to the chain
@@ -657,9 +675,15 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
             sts128(lnxt + 16u * q[g] + 4096u * c1, x[0], x[1], x[2], x[3]);
           }
       }
-      nbar_sync<1, THREADS>();
+      if (WB_PAIR_SPLITBAR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ps.mb_pair);
+      } else {
+        nbar_sync<1, THREADS>();
+      }
 
       if (!full) {
+        if (WB_PAIR_SPLITBAR) mbar_wait_parity(&ps.mb_pair, (e + 1) & 1u);
         // the partial last emission, from the natural-order pool
         mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
         const float* nat = reinterpret_cast<const float*>(dsm + OFF_L0 + ((e + 1) & 1u) * BUF);
