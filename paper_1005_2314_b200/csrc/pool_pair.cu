@@ -288,9 +288,14 @@ __device__ __forceinline__ void make_passb(uint32_t plan, uint32_t off_next, uin
   const uint32_t pk = c_perm_pack[variant >> 4] >> 8;
   hm = hs_lut[4u * (variant & 15u) + ((pk >> (2u * i)) & 3u)];
 }
-__device__ __forceinline__ void pass_b_desc(const float (&X)[JB][4], const PassB& d, const uint32_t (&tq)[G],
-                                            uint32_t lbuf) {
-  float v[JB][4], z[JB][4];
+// pB in two parts: the add stages (X -> z) and the factors + stores.  With
+// WB_PAIR_LATE_STAGE the emission is staged between the two, so the wait for
+// the staging row comes one add stage later.
+#ifndef WB_PAIR_LATE_STAGE
+#define WB_PAIR_LATE_STAGE 0  // measured slower (3.14 vs 2.85 ms: register pressure, 40 bytes of spills)
+#endif
+__device__ __forceinline__ void pass_b_adds(const float (&X)[JB][4], float (&z)[JB][4]) {
+  float v[JB][4];
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
@@ -298,6 +303,9 @@ __device__ __forceinline__ void pass_b_desc(const float (&X)[JB][4], const PassB
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[g * 4 + i][c] = X[g * 4 + c][i];
   bfly_z<JB>(v, z);
+}
+__device__ __forceinline__ void pass_b_stores(const float (&z)[JB][4], const PassB& d, const uint32_t (&tq)[G],
+                                              uint32_t lbuf) {
   uint32_t t16[G], t6[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -633,6 +641,10 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
         else nbar_arrive<4, NTHR>();
       }
 
+      // pB's add stages ahead of the staging (WB_PAIR_LATE_STAGE)
+      float zb[JB][4];
+      if (WB_PAIR_LATE_STAGE && more) pass_b_adds(X, zb);
+
       // ---- the emission: y = x*scale + mean into the staging row ----
       // this emission's scale (and the pair's pB constants) are final
       if (full) mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
@@ -665,7 +677,8 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
           d.m2[2] = __float_as_uint(m2.z), d.m2[3] = __float_as_uint(m2.w);
           d.hm[0] = hm.x, d.hm[1] = hm.y, d.hm[2] = hm.z, d.hm[3] = hm.w;
         }
-        pass_b_desc(X, d, tq, lnxt);
+        if (!WB_PAIR_LATE_STAGE) pass_b_adds(X, zb);
+        pass_b_stores(zb, d, tq, lnxt);
       } else {
 #pragma unroll
         for (int g = 0; g < G; ++g)
