@@ -38,7 +38,8 @@ def assert_same(got, want, what=""):
 
 @pytest.fixture(autouse=True)
 def pair_on(monkeypatch):
-    """pair_kernel is opt-in (read at handle creation)."""
+    """WALLACE_B200_PAIR is read at handle creation (pair_kernel is on by
+    default; the tests that compare with pool_kernel set it themselves)."""
     monkeypatch.setenv("WALLACE_B200_PAIR", "1")
 
 
@@ -121,3 +122,36 @@ def test_pair_many_pools_cfg3_shape(cuda):
         want = OracleGen(Cfg(seed=1 + p, pool_size=N, discard_every=2), "f32").fill(count)
         assert_same(out[p].cpu().numpy(), want, f"pool {p}")
     b.close()
+
+
+def test_pair_is_the_default_path(cuda, monkeypatch):
+    """Without the switch a cfg2/cfg3-shaped fill launches pair_kernel (the
+    counter of the C-ABI moves); WALLACE_B200_PAIR=0 keeps it on pool_kernel;
+    other shapes (fp64, N != 4096, discard_every != 2) never use it."""
+    monkeypatch.delenv("WALLACE_B200_PAIR", raising=False)
+    seeds = list(range(1, 161))  # above the few-pool latency geometry
+    n0 = pb.pair_kernel_launches()
+    b = pb.PoolBatch(pb.GeneratorConfig(pool_size=N, discard_every=2), n_pools=len(seeds), seeds=seeds, dtype="f32")
+    out = b.fill(3 * (N - 1)).cpu().numpy()
+    b.close()
+    assert pb.pair_kernel_launches() > n0
+    want = OracleGen(Cfg(seed=160, pool_size=N, discard_every=2), "f32").fill(3 * (N - 1))
+    assert_same(out[159], want, "default path, pool 159")
+
+    monkeypatch.setenv("WALLACE_B200_PAIR", "0")
+    n1 = pb.pair_kernel_launches()
+    b = pb.PoolBatch(pb.GeneratorConfig(pool_size=N, discard_every=2), n_pools=len(seeds), seeds=seeds, dtype="f32")
+    out0 = b.fill(3 * (N - 1)).cpu().numpy()
+    b.close()
+    assert pb.pair_kernel_launches() == n1
+    assert_same(out0, out, "pool_kernel vs pair_kernel")
+
+    monkeypatch.delenv("WALLACE_B200_PAIR", raising=False)
+    for kw, dtype in ((dict(pool_size=N, discard_every=2), "f64"), (dict(pool_size=2048, discard_every=2), "f32"),
+                      (dict(pool_size=N, discard_every=3), "f32")):
+        n2 = pb.pair_kernel_launches()
+        b = pb.PoolBatch(pb.GeneratorConfig(**kw), n_pools=len(seeds), seeds=seeds, dtype=dtype)
+        b.fill(2 * kw["pool_size"])
+        b.synchronize()
+        b.close()
+        assert pb.pair_kernel_launches() == n2, (kw, dtype)
