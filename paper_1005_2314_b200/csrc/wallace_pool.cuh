@@ -2134,12 +2134,17 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         }
         pub = false;
       };
-      for (uint32_t e = 0; e < a.n_emit; ++e) {
-        for (uint32_t q = 1; q <= a.d; ++q, ++p) {
-          const bool emit_pass = q == a.d;
+      // this thread's first 4-block in the pitched row of emission e: one
+      // pointer advanced by N per emission (the loop is one warp per
+      // scheduler: every instruction of a pass is on its critical path)
+      T* row_t = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows) * N + 4 * b0;
+      const uint32_t lat_n_emit = a.n_emit, lat_d = a.d, lat_n_passes = a.n_passes;
+      for (uint32_t e = 0; e < lat_n_emit; ++e, row_t += N) {
+        for (uint32_t q = 1; q <= lat_d; ++q, ++p) {
+          const bool emit_pass = q == lat_d;
           const bool renorm_now = pc == 0;
           const uint32_t plan_p = plan;
-          plan = s_plans[p + 1 < a.n_passes ? p + 1 : p];  // next pass's plan
+          plan = s_plans[p + 1 < lat_n_passes ? p + 1 : p];  // next pass's plan
           T X[G::J][4];
           if (WB_LAT_DEFER_PUB)
             run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs, true, false, [&] {
@@ -2147,7 +2152,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
             });
           else
             run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
-          T* const row = static_cast<T*>(a.lat_raw) + (pool * a.lat_rows + e) * N;
+          T* const row = row_t - 4 * b0;
           if (emit_pass && !renorm_now && tid == G::OWNER) {
             pub_x = static_cast<double>(X[G::J - 1][3]);
             pub_e = e;
@@ -2159,7 +2164,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
             // 4-blocks go to the pitched row straight from registers
 #pragma unroll
             for (int j = 0; j < G::J; ++j) {
-              T* const d = row + 4 * (b0 + 32 * j);
+              T* const d = row_t + 128 * j;
               stg_vec(d, X[j]);
               if constexpr (sizeof(T) == 8) stg_vec(d + 2, X[j] + 2);
             }
@@ -2184,7 +2189,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
 #pragma unroll
               for (int j = 0; j < G::J; ++j) {
                 const T* const v = cur + 4 * (b0 + 32 * j);
-                T* const d = row + 4 * (b0 + 32 * j);
+                T* const d = row_t + 128 * j;
                 stg_vec(d, v);
                 if constexpr (sizeof(T) == 8) stg_vec(d + 2, v + 2);
               }
