@@ -1385,11 +1385,13 @@ static_assert(Perm3Rep<2, 0>::v == 0 && Perm3Rep<2, 1>::v == 3 && Perm3Rep<2, 2>
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
-template <typename T, int LOG2N, int J, int PT = 0, class Hook = NoHook>
+template <typename T, int LOG2N, int J, int PT = 0, class Hook = NoHook, bool HSA = false>
 __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uint32_t nxt_off,
                                          uint32_t plan, uint32_t b0, T (&X)[J][4],
                                          const float* hs_lut, bool store = true,
-                                         bool wait_stage = false, Hook hook = Hook{}) {
+                                         bool wait_stage = false, Hook hook = Hook{}, uint32_t hs_saddr = 0) {
+  // HSA: hs_saddr is hs_lut's shared-window address, kept in a register by
+  // the caller (the latency fill: ptxas otherwise rebuilds it every pass)
   constexpr bool HOOK = !std::is_same<Hook, NoHook>::value;
   static_assert(PT == 0 || PT == 1, "wallace4 pass types");
   using G = Geo<T, LOG2N>;
@@ -1413,7 +1415,11 @@ __device__ __forceinline__ void run_pass(const char* base, uint32_t cur_off, uin
   T hs[4];
   if constexpr (WB_HS_LUT && sizeof(T) == 4) {
     // the four +-1/2 row factors of this variant's sign mask, one 128-bit load
-    const float4 h = reinterpret_cast<const float4*>(hs_lut)[smask];
+    float4 h;
+    if constexpr (HSA)
+      asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(h.x), "=f"(h.y), "=f"(h.z), "=f"(h.w) : "r"(hs_saddr + 16u * smask));
+    else
+      h = reinterpret_cast<const float4*>(hs_lut)[smask];
     hs[0] = h.x;
     hs[1] = h.y;
     hs[2] = h.z;
@@ -2122,17 +2128,29 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
       bool pub = false;          // the owner holds an unpublished entry
       double pub_x = 0.0;
       uint32_t pub_e = 0;
+      // rank 1's ring and batch mbarriers in the cluster window, and the
+      // row-factor table's shared address, once
+      uint32_t ring_r = 0, mbar_r = 0;
+      if constexpr (CLU) {
+        ring_r = dsmem_addr(ring, 1);
+        mbar_r = dsmem_addr(rmbar, 1);
+      }
+      uint32_t hs_sa;  // (through an asm so that it is kept, not rebuilt from the CTA id each pass)
+      asm volatile("mov.u32 %0, %1;" : "=r"(hs_sa) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_hs))));
       auto publish = [&] {
         if constexpr (CLU) {
           // into the chain CTA's ring, completing its batch mbarrier
           if (WB_ABLATE != 18)
-            st_async_f64x2(dsmem_addr(ring + 2 * pub_e, 1), pub_x, ss_reg, dsmem_addr(rmbar + pub_e / WB_LAT_CBATCH, 1));
+            st_async_f64x2(ring_r + 16u * pub_e, pub_x, ss_reg, mbar_r + 8u * (pub_e / WB_LAT_CBATCH));
         } else {
           ring[2 * pub_e] = pub_x;
           ring[2 * pub_e + 1] = ss_reg;
           if ((pub_e + 1) % WB_LAT_BATCH == 0 || pub_e + 1 == a.n_emit) st_release_cta(&s.produced, pub_e + 1);
         }
         pub = false;
+      };
+      auto pub_hook = [&] {
+        if (pub) publish();
       };
       // this thread's first 4-block in the pitched row of emission e: one
       // pointer advanced by N per emission (the loop is one warp per
@@ -2147,11 +2165,11 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           plan = s_plans[p + 1 < lat_n_passes ? p + 1 : p];  // next pass's plan
           T X[G::J][4];
           if (WB_LAT_DEFER_PUB)
-            run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs, true, false, [&] {
-              if (pub) publish();
-            });
+            run_pass<T, LOG2N, G::J, PT, decltype(pub_hook), true>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs, true,
+                                                                   false, pub_hook, hs_sa);
           else
-            run_pass<T, LOG2N, G::J, PT>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs);
+            run_pass<T, LOG2N, G::J, PT, NoHook, true>(cbase, cur_off, cur_off ^ FLIP, plan_p, b0, X, s_hs, true, false,
+                                                       NoHook{}, hs_sa);
           T* const row = row_t - 4 * b0;
           if (emit_pass && !renorm_now && tid == G::OWNER) {
             pub_x = static_cast<double>(X[G::J - 1][3]);
