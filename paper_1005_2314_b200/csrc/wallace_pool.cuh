@@ -2126,7 +2126,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
       // barrier (measured: ~115 cycles per pass on the critical path).
       double ss_reg = s.sum_sq;  // sum_sq changes only at renormalisations
       bool pub = false;          // the owner holds an unpublished entry
-      double pub_x = 0.0;
+      T pub_x = T(0);  // (converted in publish: the owner alone pays for it)
       uint32_t pub_e = 0;
       // rank 1's ring and batch mbarriers in the cluster window, and the
       // row-factor table's shared address, once
@@ -2141,9 +2141,10 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
         if constexpr (CLU) {
           // into the chain CTA's ring, completing its batch mbarrier
           if (WB_ABLATE != 18)
-            st_async_f64x2(ring_r + 16u * pub_e, pub_x, ss_reg, mbar_r + 8u * (pub_e / WB_LAT_CBATCH));
+            st_async_f64x2(ring_r + 16u * pub_e, static_cast<double>(pub_x), ss_reg,
+                           mbar_r + 8u * (pub_e / WB_LAT_CBATCH));
         } else {
-          ring[2 * pub_e] = pub_x;
+          ring[2 * pub_e] = static_cast<double>(pub_x);
           ring[2 * pub_e + 1] = ss_reg;
           if ((pub_e + 1) % WB_LAT_BATCH == 0 || pub_e + 1 == a.n_emit) st_release_cta(&s.produced, pub_e + 1);
         }
@@ -2174,7 +2175,7 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
                                                        NoHook{}, hs_sa);
           T* const row = row_t - 4 * b0;
           if (emit_pass && !renorm_now && tid == G::OWNER) {
-            pub_x = static_cast<double>(X[G::J - 1][3]);
+            pub_x = X[G::J - 1][3];
             pub_e = e;
             pub = true;
             if (!WB_LAT_DEFER_PUB) publish();
