@@ -586,6 +586,8 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
   const uint64_t d = h->cfg.discard_every;
   uint64_t produced = 0;
   bool first = true;
+  uint64_t lat_ramp = 128;  // passes of the next ramped latency launch
+  if (const char* r = std::getenv("WALLACE_B200_NO_LATRAMP"); r && r[0] == '1') lat_ramp = ~0ull >> 1;
   std::vector<Launch> ls;
   while (produced < count) {
     wb::FillArgs a = base_args(h);
@@ -647,7 +649,17 @@ wallace_status run_emit(wallace_handle* h, void* out, uint64_t count, int mode,
     if (e_total > 0) {
       if (d <= h->plan_cap) {
         e = std::min<uint64_t>(e_total, h->plan_cap / d);
-        if (a.mode == wb::kModeFillLat) e = std::min<uint64_t>(e, h->lat_rows);
+        if (a.mode == wb::kModeFillLat) {
+          e = std::min<uint64_t>(e, h->lat_rows);
+          // A long latency fill ramps its launches up (128, 256, ... passes):
+          // plan_kernel walks a launch's plan words on one thread (~84 ns
+          // per pass against the pool kernel's ~270 ns), and only the first
+          // launch's planning is not hidden behind the previous pool launch.
+          if (e_total * d >= 1024 && lat_ramp < e * d) {
+            e = std::max<uint64_t>(1, lat_ramp / d);
+            lat_ramp *= 2;
+          }
+        }
         if (h->max_emit > 0) e = std::min<uint64_t>(e, h->max_emit);
         if (pair) {
           // the first pass of this launch that ends on a renormalisation
