@@ -2346,8 +2346,10 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
     for (uint32_t e = 0; e < a.n_emit; ++e, gbase += N - 1) {
       const int slot = e & 1;
       const uint32_t limit = (e + 1 == a.n_emit) ? a.last_limit : uint32_t(N - 1);
-      for (uint32_t q = 1; q <= a.d; ++q, ++p) {
-        const bool emit_pass = q == a.d;
+      // one pass of emission e (emit_pass: its last).  The consumer instantiates
+      // the body twice so that discard_every = 1 runs it with emit_pass folded.
+      auto pass_body = [&](auto emit_tag, bool emit_rt) __attribute__((always_inline)) {
+        const bool emit_pass = decltype(emit_tag)::value ? true : emit_rt;
         const bool renorm_now = pc == 0;
         const bool fast = FAST && emit_pass && !renorm_now && limit == uint32_t(N - 1);
         // the emission scale is final before this pass (published behind at
@@ -2612,6 +2614,12 @@ __global__ void __launch_bounds__(kernel_threads<T, LOG2N, MODE>(), kernel_minb<
           __syncthreads();
         }
         pc = (pc + 1) & 255u;
+      };
+      if (MODE == kModeConsume && a.d == 1) {
+        pass_body(std::true_type{}, true);
+        ++p;
+      } else {
+        for (uint32_t q = 1; q <= a.d; ++q, ++p) pass_body(std::false_type{}, q == a.d);
       }
     }
     if constexpr (BULK_OK) {
