@@ -363,6 +363,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
                : "memory");
 }
 
+// The same on shared-window addresses: the compute loop keeps PairSync's
+// address in a register (ptxas otherwise rebuilds it from SR_CgaCtaId, a
+// long-latency read, in every pair).
+__device__ __forceinline__ void mbar_wait_parity_sa(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WB_MBAR_WAITSA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WB_MBAR_WAITSA_%=;\n}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ float lds32_volatile(uint32_t addr) {
+  float v;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
 // the emission's values y = x*scale + mean of one thread's JB natural
 // 4-blocks into the staging row: value i at slot i + sigma (sigma = the
 // output row's misalignment in values), so the row's 16-byte pieces line up
@@ -572,6 +593,8 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
     const uint32_t d = 16u * la + 4u * le + lk;
     const uint32_t lbase = 4u * (1024u * le + 4u * la);  // + the lane's slot position (raw_slot)
     const uint32_t g0 = G == 2 ? 0u : (uint32_t(warp) >> 2);  // G == 1: warps 4..7 take the upper quads
+    uint32_t ps_sa;  // PairSync's shared-window address, kept in a register
+    asm volatile("mov.u32 %0, %1;" : "=r"(ps_sa) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&ps))));
 
     // first pass of emission 0 (pB only): natural 4-blocks in, layout L out
     {
@@ -635,7 +658,8 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
 
       // pool element N-1 (4-block ROWS-1 = quad 255, column 3, slot 3) to the chain
       if (full) {
-        if (q[G - 1] == uint32_t(NQ - 1)) ps.xl[slot] = static_cast<double>(X[(G - 1) * 4 + 3][3]);
+        if (q[G - 1] == uint32_t(NQ - 1))
+          sts_f64(ps_sa + uint32_t(offsetof(PairSync, xl)) + 8u * uint32_t(slot), static_cast<double>(X[(G - 1) * 4 + 3][3]));
         __syncwarp();
         if (e & 1u) nbar_arrive<5, NTHR>();
         else nbar_arrive<4, NTHR>();
@@ -647,11 +671,12 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
 
       // ---- the emission: y = x*scale + mean into the staging row ----
       // this emission's scale (and the pair's pB constants) are final
-      if (full) mbar_wait_parity(&ps.mb_scale[slot], (e >> 1) & 1u);
+      if (full) mbar_wait_parity_sa(ps_sa + uint32_t(offsetof(PairSync, mb_scale)) + 8u * uint32_t(slot), (e >> 1) & 1u);
       if (full && a.pad_ab != 3) {
         // the staging row's previous contents have left
-        mbar_wait_parity(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u], (NSG == 2 ? (e >> 1) : e) & 1u);
-        const float sc = *static_cast<volatile float*>(&ps.scf[slot]);
+        mbar_wait_parity_sa(ps_sa + uint32_t(offsetof(PairSync, mb_copied)) + 8u * (NSG == 2 ? (e & 1u) : 0u),
+                            (NSG == 2 ? (e >> 1) : e) & 1u);
+        const float sc = lds32_volatile(ps_sa + uint32_t(offsetof(PairSync, scf)) + 4u * uint32_t(slot));
         uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
         if (a.pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
         const uint32_t sgs = sbase + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS + 4u * sigma;
@@ -668,9 +693,9 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       if (more) {
         PassB d;
         {
-          const float4 m1 = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ps.d_m1[slot])));
-          const float4 m2 = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ps.d_m2[slot])));
-          const float4 hm = lds128(static_cast<uint32_t>(__cvta_generic_to_shared(ps.d_hm[slot])));
+          const float4 m1 = lds128(ps_sa + uint32_t(offsetof(PairSync, d_m1)) + 16u * uint32_t(slot));
+          const float4 m2 = lds128(ps_sa + uint32_t(offsetof(PairSync, d_m2)) + 16u * uint32_t(slot));
+          const float4 hm = lds128(ps_sa + uint32_t(offsetof(PairSync, d_hm)) + 16u * uint32_t(slot));
           d.m1[0] = __float_as_uint(m1.x), d.m1[1] = __float_as_uint(m1.y);
           d.m1[2] = __float_as_uint(m1.z), d.m1[3] = __float_as_uint(m1.w);
           d.m2[0] = __float_as_uint(m2.x), d.m2[1] = __float_as_uint(m2.y);
