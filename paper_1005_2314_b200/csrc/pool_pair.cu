@@ -97,6 +97,9 @@ constexpr uint32_t MAX_PLAN_BYTES = 8 * 1024;
 constexpr int G = WB_PAIR_G;
 constexpr int THREADS = 256 / G;
 constexpr int JB = 4 * G;  // 4-blocks per thread
+#ifndef WB_PAIR_DEBUGKNOBS
+#define WB_PAIR_DEBUGKNOBS 0  // 1: WALLACE_B200_PAIR_DEBUG (FillArgs::pad_ab) selects a timing-only ablation
+#endif
 #ifndef WB_PAIR_NOCHAIN
 #define WB_PAIR_NOCHAIN 0  // timing only
 #endif
@@ -466,6 +469,9 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
   const uint64_t pool = blockIdx.x;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
   const bool mean_zero = a.mean_is_zero != 0;
+  // timing-only ablations (tools/dbg/pair_abl.sh): compiled in with
+  // -DWB_PAIR_DEBUGKNOBS=1 only, so the product kernel carries no checks
+  const int pad_ab = WB_PAIR_DEBUGKNOBS ? a.pad_ab : 0;
   const float mean_t = __double2float_rn(a.mean);
 
   // ---- prologue: state, pool (natural order, into L1), plans ----
@@ -535,15 +541,15 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       // every compute thread staged its values of emission e
       if (e & 1u) nbar_sync<3, NTHR>();
       else nbar_sync<2, NTHR>();
-      if (a.pad_ab < 2 || a.pad_ab >= 4) {
+      if (pad_ab < 2 || pad_ab >= 4) {
         // the row holds value i at slot i + sigma, so slot and global address
         // agree mod 16 bytes: the aligned middle [delta, delta + L) leaves by
         // one bulk copy, the <= 3 head and <= 3 tail values by scalar stores
         const float* row = reinterpret_cast<const float*>(dsm + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS);
         // (5, timing only: four output rows per pool, resident in L2)
-        float* const gp = out_pool + size_t(a.pad_ab == 5 ? (e & 3u) : e) * (N - 1);
+        float* const gp = out_pool + size_t(pad_ab == 5 ? (e & 3u) : e) * (N - 1);
         float* gpa = gp;
-        if (a.pad_ab == 4) gpa = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
+        if (pad_ab == 4) gpa = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15));
         const uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(gpa) >> 2) & 3u;
         const uint32_t delta = (4u - sigma) & 3u;
         const uint32_t L = ((uint32_t(N - 1) - delta) / 4u) * 4u;
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
           stg1(gp + i, row[i + sigma]);
         }
         __syncwarp();
-        if (lane == 0 && a.pad_ab != 6) bulk_wait_read();  // (6, timing only: the row is handed back at once)
+        if (lane == 0 && pad_ab != 6) bulk_wait_read();  // (6, timing only: the row is handed back at once)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.mb_copied[NSG == 2 ? (e & 1u) : 0u]);
@@ -672,13 +678,13 @@ __global__ void __launch_bounds__(THREADS + 32, WB_PAIR_MINB) pair_kernel(const 
       // ---- the emission: y = x*scale + mean into the staging row ----
       // this emission's scale (and the pair's pB constants) are final
       if (full) mbar_wait_parity_sa(ps_sa + uint32_t(offsetof(PairSync, mb_scale)) + 8u * uint32_t(slot), (e >> 1) & 1u);
-      if (full && a.pad_ab != 3) {
+      if (full && pad_ab != 3) {
         // the staging row's previous contents have left
         mbar_wait_parity_sa(ps_sa + uint32_t(offsetof(PairSync, mb_copied)) + 8u * (NSG == 2 ? (e & 1u) : 0u),
                             (NSG == 2 ? (e >> 1) : e) & 1u);
         const float sc = lds32_volatile(ps_sa + uint32_t(offsetof(PairSync, scf)) + 4u * uint32_t(slot));
         uint32_t sigma = uint32_t(reinterpret_cast<uintptr_t>(out_pool + size_t(e) * (N - 1)) >> 2) & 3u;
-        if (a.pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
+        if (pad_ab == 4) sigma = 0;  // (timing only: every row aligned)
         const uint32_t sgs = sbase + OFF_SG0 + (NSG == 2 ? (e & 1u) : 0u) * SGS + 4u * sigma;
         if (mean_zero) stage_emission<true>(X, q, sgs, sigma, sc, mean_t, la >> 1);
         else stage_emission<false>(X, q, sgs, sigma, sc, mean_t, la >> 1);
